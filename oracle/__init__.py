@@ -1,0 +1,258 @@
+"""CPU oracle for the Nekbone unpreconditioned-CG hot path (arXiv 2405.11065).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product path (``paper_2405_11065_b200``) never imports it and
+shares no code with it; see ``oracle/nbk_oracle.c`` for the arithmetic and the
+paper passages each function follows.
+
+This module is a thin ctypes wrapper: argument marshalling only.  ``build()``
+compiles ``nbk_oracle.c`` with ``gcc -O2 -ffp-contract=off -fopenmp`` (IEEE
+binary64/binary32, no contraction except explicit fma, no FTZ).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "nbk_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+c_i32, c_i64, c_u64, c_dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+_p = ctypes.c_void_p
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle shared library in-tree (gcc, no GPU needed)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+               "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        L.ora_splitmix64.restype = c_u64
+        L.ora_splitmix64.argtypes = [c_u64, c_u64]
+        L.ora_uniform_pm1.restype = c_dbl
+        L.ora_uniform_pm1.argtypes = [c_u64, c_u64]
+        L.ora_gll.restype = ctypes.c_int
+        L.ora_gll.argtypes = [ctypes.c_int, _p, _p, _p]
+        L.ora_sizes.restype = None
+        L.ora_sizes.argtypes = [ctypes.c_int] * 4 + [_p]
+        L.ora_setup.restype = ctypes.c_int
+        L.ora_setup.argtypes = [ctypes.c_int] * 4 + [c_dbl, c_u64, c_u64, c_i64, c_i64] + [_p] * 7
+        for nm in ("ora_ax_local64", "ora_ax_local32"):
+            getattr(L, nm).restype = None
+            getattr(L, nm).argtypes = [c_i64, ctypes.c_int, _p, _p, _p, _p]
+        for nm in ("ora_dssum64", "ora_dssum32"):
+            getattr(L, nm).restype = None
+            getattr(L, nm).argtypes = [ctypes.c_int] * 4 + [_p, ctypes.c_int]
+        for nm in ("ora_mask64", "ora_mask32"):
+            getattr(L, nm).restype = None
+            getattr(L, nm).argtypes = [ctypes.c_int] * 4 + [_p]
+        for nm in ("ora_ax64", "ora_ax32"):
+            getattr(L, nm).restype = None
+            getattr(L, nm).argtypes = [ctypes.c_int] * 4 + [_p] * 4 + [ctypes.c_int]
+        L.ora_fsum.restype = c_dbl
+        L.ora_fsum.argtypes = [c_i64, _p]
+        for nm in ("ora_glsc3_64", "ora_glsc3_32"):
+            getattr(L, nm).restype = c_dbl
+            getattr(L, nm).argtypes = [c_i64, _p, _p, _p]
+        L.ora_multiplicity_weight.restype = None
+        L.ora_multiplicity_weight.argtypes = [ctypes.c_int] * 4 + [_p]
+        for nm in ("ora_cg64", "ora_cg32"):
+            getattr(L, nm).restype = ctypes.c_int
+            getattr(L, nm).argtypes = [ctypes.c_int] * 4 + [_p] * 3 + [ctypes.c_int] + [_p] * 3
+        L.ora_true_residual.restype = c_dbl
+        L.ora_true_residual.argtypes = [ctypes.c_int] * 4 + [_p] * 5
+        L.ora_num_threads.restype = ctypes.c_int
+        L.ora_num_threads.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Mesh:
+    """Box of ex*ey*ez hexahedra, N GLL points per direction (reading R1/R5)."""
+    ex: int
+    ey: int
+    ez: int
+    N: int
+    jitter: float = 0.0
+    seed_geom: int = 0
+    seed_rhs: int = 0
+
+    @property
+    def E(self) -> int:
+        return self.ex * self.ey * self.ez
+
+    @property
+    def dims(self):
+        return (self.ex, self.ey, self.ez, self.N)
+
+    def sizes(self) -> dict:
+        out = np.zeros(4, dtype=np.int64)
+        lib().ora_sizes(self.ex, self.ey, self.ez, self.N, _ptr(out))
+        return dict(n_local=int(out[0]), n_global=int(out[1]), n_interior=int(out[2]),
+                    n_shared=int(out[3]))
+
+
+def splitmix64(seed: int, i: int) -> int:
+    return int(lib().ora_splitmix64(seed & (2**64 - 1), i))
+
+
+def uniform_pm1(seed: int, i: int) -> float:
+    return float(lib().ora_uniform_pm1(seed & (2**64 - 1), i))
+
+
+def gll(N: int):
+    """GLL nodes, weights and derivative matrix D[a, b] = l_b'(xi_a)."""
+    xi = np.zeros(N)
+    rho = np.zeros(N)
+    D = np.zeros((N, N))
+    rc = lib().ora_gll(N, _ptr(xi), _ptr(rho), _ptr(D))
+    if rc:
+        raise ValueError(f"ora_gll failed ({rc})")
+    return xi, rho, D
+
+
+def setup(mesh: Mesh, e0: int = 0, e1: int | None = None, want=("G", "f")):
+    """FP64 set-up arrays for elements [e0, e1): dict of numpy arrays."""
+    e1 = mesh.E if e1 is None else e1
+    E = e1 - e0
+    out = {}
+    shapes = {"G": ((E, 6, mesh.N, mesh.N, mesh.N), np.float64),
+              "f": ((E, mesh.N, mesh.N, mesh.N), np.float64),
+              "mass": ((E, mesh.N, mesh.N, mesh.N), np.float64),
+              "gid": ((E, mesh.N, mesh.N, mesh.N), np.int64),
+              "mult": ((E, mesh.N, mesh.N, mesh.N), np.int32),
+              "mask": ((E, mesh.N, mesh.N, mesh.N), np.uint8),
+              "xyz": ((E, 3, mesh.N, mesh.N, mesh.N), np.float64)}
+    for k in want:
+        shp, dt = shapes[k]
+        out[k] = np.zeros(shp, dtype=dt)
+    rc = lib().ora_setup(mesh.ex, mesh.ey, mesh.ez, mesh.N, float(mesh.jitter),
+                         mesh.seed_geom & (2**64 - 1), mesh.seed_rhs & (2**64 - 1), e0, e1,
+                         *[_ptr(out.get(k)) for k in ("G", "f", "mass", "gid", "mult", "mask", "xyz")])
+    if rc:
+        raise ValueError(f"ora_setup failed ({rc})")
+    return out
+
+
+def multiplicity_weight(mesh: Mesh) -> np.ndarray:
+    c = np.zeros((mesh.E, mesh.N, mesh.N, mesh.N))
+    lib().ora_multiplicity_weight(*mesh.dims, _ptr(c))
+    return c
+
+
+def ax_local(D, G, u):
+    """Per-element ax_e = D^T G D u_e in the canonical order (C1-C3)."""
+    u = np.ascontiguousarray(u)
+    w = np.empty_like(u)
+    E, N = u.shape[0], u.shape[-1]
+    if u.dtype == np.float64:
+        lib().ora_ax_local64(E, N, _ptr(np.ascontiguousarray(D, np.float64)),
+                             _ptr(np.ascontiguousarray(G, np.float64)), _ptr(u), _ptr(w))
+    elif u.dtype == np.float32:
+        lib().ora_ax_local32(E, N, _ptr(np.ascontiguousarray(D, np.float32)),
+                             _ptr(np.ascontiguousarray(G, np.float32)), _ptr(u), _ptr(w))
+    else:
+        raise TypeError(u.dtype)
+    return w
+
+
+def dssum(mesh: Mesh, w, apply_mask: bool = False):
+    w = np.array(w, copy=True, order="C")
+    fn = lib().ora_dssum64 if w.dtype == np.float64 else lib().ora_dssum32
+    fn(*mesh.dims, _ptr(w), int(apply_mask))
+    return w
+
+
+def mask(mesh: Mesh, w):
+    w = np.array(w, copy=True, order="C")
+    fn = lib().ora_mask64 if w.dtype == np.float64 else lib().ora_mask32
+    fn(*mesh.dims, _ptr(w))
+    return w
+
+
+def ax(mesh: Mesh, D, G, u, apply_mask: bool = True):
+    """w = mask(dssum(ax_e(u)))  (T1 line 5)."""
+    return dssum(mesh, ax_local(D, G, u), apply_mask=apply_mask)
+
+
+def fsum(t) -> float:
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    return float(lib().ora_fsum(t.size, _ptr(t)))
+
+
+def glsc3(a, b, c) -> float:
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    assert a.dtype == b.dtype and a.size == b.size == c.size
+    fn = lib().ora_glsc3_64 if a.dtype == np.float64 else lib().ora_glsc3_32
+    return float(fn(a.size, _ptr(a), _ptr(b), _ptr(c)))
+
+
+@dataclass
+class CgResult:
+    x: np.ndarray
+    hist: np.ndarray   # h_0..h_niter
+    trace: np.ndarray  # (niter, 5): rtz1, beta, alpha, pap, rtr
+    defect: int
+
+
+def cg(mesh: Mesh, D, G, f, niter: int, precision: str = "fp64") -> CgResult:
+    """Fixed-iteration CG (T1).  precision 'fp64' or 'fp32' (mixed: FP64 set-up
+    data rounded once to binary32, FP64 accumulation of glsc3)."""
+    D = np.ascontiguousarray(D, np.float64)
+    G = np.ascontiguousarray(G, np.float64)
+    f = np.ascontiguousarray(f, np.float64)
+    hist = np.zeros(niter + 1)
+    trace = np.zeros((niter, 5))
+    if precision == "fp64":
+        x = np.zeros_like(f)
+        rc = lib().ora_cg64(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), niter, _ptr(x), _ptr(hist),
+                            _ptr(trace))
+    elif precision == "fp32":
+        x = np.zeros(f.shape, np.float32)
+        rc = lib().ora_cg32(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), niter, _ptr(x), _ptr(hist),
+                            _ptr(trace))
+    else:
+        raise ValueError(precision)
+    return CgResult(x=x, hist=hist, trace=trace, defect=int(rc))
+
+
+def true_residual(mesh: Mesh, D, G, f, x):
+    """Final FP64 check (C12): (||f - A x64||_c, h0)."""
+    x64 = np.ascontiguousarray(x, dtype=np.float64)
+    h0 = ctypes.c_double(0.0)
+    r = lib().ora_true_residual(*mesh.dims, _ptr(np.ascontiguousarray(D, np.float64)),
+                                _ptr(np.ascontiguousarray(G, np.float64)),
+                                _ptr(np.ascontiguousarray(f, np.float64)), _ptr(x64),
+                                ctypes.cast(ctypes.pointer(h0), ctypes.c_void_p))
+    return float(r), float(h0.value)
+
+
+def num_threads() -> int:
+    return int(lib().ora_num_threads())

@@ -1,0 +1,450 @@
+"""Pins of the CPU oracle against facts the paper's setting and the mathematics
+fix (not against itself).  Each test names the pin id of DESIGN.md / SURVEY
+8(c) c4 and the passage it follows.  CPU only (no GPU)."""
+import math
+
+import numpy as np
+import pytest
+
+from tests import inputs
+
+pytestmark = pytest.mark.filterwarnings("ignore::RuntimeWarning")
+
+
+# ---------------------------------------------------------------- helpers
+def dense_stiffness(ora, mesh):
+    """Brute force: assemble the global stiffness A = sum_e Q_e^T A_e Q_e with
+    A_e = sum_mn D_m^T diag(g_mn) D_n built from Kronecker products (i fastest),
+    independent of the oracle's tensor-product loops (pin P9)."""
+    s = ora.setup(mesh, want=("G", "gid"))
+    _, _, D = ora.gll(mesh.N)
+    N = mesh.N
+    I = np.eye(N)
+    Dr = np.kron(I, np.kron(I, D))
+    Ds = np.kron(I, np.kron(D, I))
+    Dt = np.kron(D, np.kron(I, I))
+    Dm = [Dr, Ds, Dt]
+    comp = {(0, 0): 0, (0, 1): 1, (0, 2): 2, (1, 1): 3, (1, 2): 4, (2, 2): 5}
+    ng = mesh.sizes()["n_global"]
+    A = np.zeros((ng, ng))
+    for e in range(mesh.E):
+        Ge = s["G"][e].reshape(6, -1)
+        Ae = np.zeros((N ** 3, N ** 3))
+        for m in range(3):
+            for n in range(3):
+                g = Ge[comp[(min(m, n), max(m, n))]]
+                Ae += Dm[m].T @ (g[:, None] * Dm[n])
+        gid = s["gid"][e].reshape(-1)
+        A[np.ix_(gid, gid)] += Ae
+    return A, s["gid"].reshape(-1)
+
+
+def global_mask(ora, mesh):
+    s = ora.setup(mesh, want=("gid", "mask"))
+    ng = mesh.sizes()["n_global"]
+    mg = np.zeros(ng, dtype=bool)
+    mg[s["gid"].reshape(-1)] = s["mask"].reshape(-1).astype(bool)
+    return mg
+
+
+def continuous(ora, mesh, vglob):
+    gid = ora.setup(mesh, want=("gid",))["gid"]
+    return vglob[gid]
+
+
+# ------------------------------------------------------------ RNG (R5/R7)
+def test_splitmix64_reference_vector(ora):
+    # Published SplitMix64 output stream for state 0 (Steele, Lea & Flood 2014;
+    # Vigna's reference splitmix64.c): z_i for i = 0, 1, 2.
+    assert ora.splitmix64(0, 0) == 0xE220A8397B1DCDAF
+    assert ora.splitmix64(0, 1) == 0x6E789E6AA1B965F4
+    assert ora.splitmix64(0, 2) == 0x06C45D188009454F
+    # random access: index i of seed s equals index 0 of seed s + i*gamma
+    g = 0x9E3779B97F4A7C15
+    assert ora.splitmix64(12345, 7) == ora.splitmix64((12345 + 7 * g) % 2**64, 0)
+    v = [ora.uniform_pm1(1001, i) for i in range(2000)]
+    assert min(v) >= -1.0 and max(v) < 1.0 and abs(np.mean(v)) < 0.05
+
+
+# ------------------------------------------------------------- P1 GLL
+def test_gll_closed_forms(ora):
+    xi, rho, D = ora.gll(2)
+    assert xi.tolist() == [-1.0, 1.0] and rho.tolist() == [1.0, 1.0]
+    assert D.tolist() == [[-0.5, 0.5], [-0.5, 0.5]]
+    xi, rho, D = ora.gll(3)  # Simpson: {1/3, 4/3, 1/3}
+    assert xi.tolist() == [-1.0, 0.0, 1.0]
+    np.testing.assert_allclose(rho, [1 / 3, 4 / 3, 1 / 3], rtol=0, atol=4e-16)
+
+
+@pytest.mark.parametrize("N", list(range(2, 17)))
+def test_gll_nodes_weights_vs_library(ora, N):
+    xi, rho, _ = ora.gll(N)
+    p = N - 1
+    roots = np.sort(np.polynomial.legendre.Legendre.basis(p).deriv().roots().real) if p > 1 else []
+    ref = np.concatenate([[-1.0], roots, [1.0]])
+    np.testing.assert_allclose(xi, ref, rtol=0, atol=2e-14)
+    assert abs(math.fsum(rho) - 2.0) <= 2e-15
+    # GLL quadrature is exact for degree <= 2N-3
+    for q in range(0, 2 * N - 2):
+        exact = 0.0 if q % 2 else 2.0 / (q + 1)
+        assert abs(np.dot(rho, xi ** q) - exact) <= 2e-14, (N, q)
+
+
+# --------------------------------------------------------------- P2 D
+@pytest.mark.parametrize("N", [2, 3, 5, 8, 10, 12, 16])
+def test_derivative_matrix_exact_on_polynomials(ora, N):
+    xi, _, D = ora.gll(N)
+    assert np.abs(D @ np.ones(N)).max() <= 1e-13
+    for q in range(1, N):
+        err = np.abs(D @ xi ** q - q * xi ** (q - 1)).max()
+        assert err <= 2e-12 * q, (N, q, err)
+
+
+# ------------------------------------------------ P3 / P4 geometry
+@pytest.mark.parametrize("N", [3, 8])
+def test_undeformed_geometric_factors_closed_form(ora, N):
+    m = ora.Mesh(3, 2, 2, N)
+    G = ora.setup(m, want=("G",))["G"]
+    _, rho, _ = ora.gll(N)
+    W = rho[None, None, :] * rho[None, :, None] * rho[:, None, None]  # [k][j][i]
+    h = 1.0 / m.ex
+    for c in (0, 3, 5):
+        ref = np.broadcast_to(0.5 * h * W, G[:, c].shape)
+        # D-based Jacobian: rounding-level agreement in the max norm
+        assert np.abs(G[:, c] - ref).max() <= 2e-14 * np.abs(ref).max()
+    for c in (1, 2, 4):
+        assert np.abs(G[:, c]).max() <= 2e-14 * np.abs(G[:, 0]).max()
+
+
+@pytest.mark.parametrize("N", [4, 8, 12])
+def test_jittered_mass_sums_to_volume(ora, N):
+    m = ora.Mesh(3, 3, 2, N, jitter=0.1, seed_geom=2003)
+    s = ora.setup(m, want=("mass", "G", "xyz"))
+    vol = 1.0 * (m.ey / m.ex) * (m.ez / m.ex)
+    assert abs(s["mass"].sum() - vol) <= 1e-13
+    assert s["mass"].min() > 0
+    # the metric is symmetric positive definite at every point
+    Gc = s["G"]
+    M = np.stack([np.stack([Gc[:, 0], Gc[:, 1], Gc[:, 2]], -1),
+                  np.stack([Gc[:, 1], Gc[:, 3], Gc[:, 4]], -1),
+                  np.stack([Gc[:, 2], Gc[:, 4], Gc[:, 5]], -1)], -2)
+    assert np.linalg.eigvalsh(M.reshape(-1, 3, 3)).min() > 0
+    # the jitter moves interior vertices only: the box boundary is exact
+    x = s["xyz"]
+    assert abs(x[:, 0].min()) <= 4e-16 and abs(x[:, 0].max() - 1.0) <= 4e-16
+
+
+def test_coordinates_continuous_across_elements(ora):
+    m = ora.Mesh(3, 2, 2, 6, jitter=0.1, seed_geom=7)
+    s = ora.setup(m, want=("xyz", "gid"))
+    xyz = np.moveaxis(s["xyz"], 1, -1).reshape(-1, 3)
+    gid = s["gid"].reshape(-1)
+    ref = np.zeros((gid.max() + 1, 3))
+    ref[gid] = xyz
+    assert np.abs(ref[gid] - xyz).max() <= 1e-15
+
+
+# --------------------------------------------------- P5 gid / c / mask
+def test_multiplicity_and_mask_structure(ora):
+    m = ora.Mesh(2, 1, 1, 5)  # 2x1x1 interface has m = 2
+    s = ora.setup(m, want=("mult", "mask", "gid"))
+    assert (s["mult"][0, :, :, 4] == 2).all() and (s["mult"][1, :, :, 0] == 2).all()
+    assert (s["mult"][0, :, :, :4] == 1).all()
+    m = ora.Mesh(2, 2, 2, 2)  # centre corner of 2x2x2 has m = 8
+    s = ora.setup(m, want=("mult", "gid"))
+    centre = s["gid"][0, 1, 1, 1]
+    assert (s["mult"][s["gid"] == centre] == 8).all() and (s["gid"] == centre).sum() == 8
+    for mesh in (ora.Mesh(2, 2, 2, 8), ora.Mesh(3, 2, 4, 5)):
+        sz = mesh.sizes()
+        s = ora.setup(mesh, want=("mult", "mask", "gid"))
+        one = np.ones((mesh.E, mesh.N, mesh.N, mesh.N))
+        assert (ora.dssum(mesh, one) == s["mult"]).all()  # dssum(1) = m
+        c = ora.multiplicity_weight(mesh)
+        assert (c * s["mult"] == 1.0).all()  # c m = 1 exactly (R8)
+        ng = sz["n_global"]
+        assert np.unique(s["gid"]).size == ng
+        mg = np.zeros(ng, bool)
+        mg[s["gid"].reshape(-1)] = s["mask"].reshape(-1).astype(bool)
+        assert ng - mg.sum() == sz["n_interior"]
+        assert (np.bincount(s["gid"].reshape(-1)) > 1).sum() == sz["n_shared"]
+
+
+def test_sizes_match_survey_table(ora):
+    # SURVEY 8 per-config size table (Appendix B formulas)
+    assert ora.Mesh(2, 2, 2, 8).sizes() == dict(n_local=4096, n_global=3375, n_interior=2197,
+                                                n_shared=631)
+    c2 = ora.Mesh(16, 16, 16, 8).sizes()
+    assert (c2["n_local"], c2["n_global"], c2["n_interior"]) == (2097152, 1442897, 1367631)
+    c3 = ora.Mesh(32, 32, 32, 12).sizes()
+    assert (c3["n_local"], c3["n_global"]) == (56623104, 43986977)
+    c5 = ora.Mesh(64, 64, 64, 10).sizes()
+    assert c5["n_global"] == 192100033
+
+
+# ---------------------------------------------------------- dssum / mask
+def test_dssum_chain_order_bruteforce(ora):
+    """C4: copies summed in ascending local index, pure-Python loop."""
+    m = ora.Mesh(2, 2, 2, 3)
+    gid = ora.setup(m, want=("gid",))["gid"].reshape(-1)
+    w = inputs.uniform_field(gid.size, 11)
+    out = ora.dssum(m, w.reshape(m.E, 3, 3, 3)).reshape(-1)
+    acc = {}
+    for L in range(gid.size):
+        g = int(gid[L])
+        acc[g] = float(w[L]) if g not in acc else acc[g] + float(w[L])
+    ref = np.array([acc[int(g)] for g in gid])
+    assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
+    for dt in (np.float32,):
+        w32 = w.astype(dt)
+        out32 = ora.dssum(m, w32.reshape(m.E, 3, 3, 3)).reshape(-1)
+        acc = {}
+        for L in range(gid.size):
+            g = int(gid[L])
+            acc[g] = w32[L] if g not in acc else np.float32(acc[g] + w32[L])
+        assert np.array_equal(out32, np.array([acc[int(g)] for g in gid], dtype=dt))
+
+
+def test_dssum_idempotent_with_multiplicity(ora):
+    m = ora.Mesh(2, 2, 2, 4)  # gs(c * gs(f)) == gs(f)
+    f = inputs.uniform_field((m.E, 4, 4, 4), 3)
+    c = ora.multiplicity_weight(m)
+    g = ora.dssum(m, f)
+    np.testing.assert_allclose(ora.dssum(m, c * g), g, rtol=1e-15, atol=1e-15)
+    msk = ora.setup(m, want=("mask",))["mask"].astype(bool)
+    gm = ora.dssum(m, f, apply_mask=True)
+    assert (gm[msk] == 0).all() and not np.signbit(gm[msk]).any()  # C5: +0 assigned
+    assert np.array_equal(gm[~msk], g[~msk])
+
+
+# ---------------------------------------------------- operator pins
+@pytest.mark.parametrize("mesh_args", [(1, 1, 1, 3, 0.0), (2, 1, 1, 4, 0.0), (2, 2, 2, 3, 0.1),
+                                       (2, 2, 1, 5, 0.1)])
+def test_ax_matches_dense_assembled_matrix(ora, mesh_args):
+    ex, ey, ez, N, jit = mesh_args
+    m = ora.Mesh(ex, ey, ez, N, jitter=jit, seed_geom=5)
+    A, gid = dense_stiffness(ora, m)
+    assert np.abs(A - A.T).max() <= 1e-15 * np.abs(A).max()
+    v = inputs.uniform_global(A.shape[0], 21)
+    u = v[gid].reshape(m.E, N, N, N)
+    _, _, D = ora.gll(N)
+    G = ora.setup(m, want=("G",))["G"]
+    w = ora.ax(m, D, G, u, apply_mask=False)
+    ref = (A @ v)[gid].reshape(w.shape)
+    assert np.abs(w - ref).max() <= 1e-14 * np.abs(ref).max()
+    # masked operator = dense with Dirichlet rows zeroed
+    mg = global_mask(ora, m)
+    wm = ora.ax(m, D, G, u, apply_mask=True)
+    refm = np.where(mg, 0.0, A @ v)[gid].reshape(w.shape)
+    assert np.abs(wm - refm).max() <= 1e-14 * np.abs(ref).max()
+
+
+def test_c1_dense_and_spd(ora):
+    """P9 + P10 on C1 (2x2x2, N=8): dense agreement and SPD interior block."""
+    m = ora.Mesh(2, 2, 2, 8)
+    A, gid = dense_stiffness(ora, m)
+    mg = global_mask(ora, m)
+    Ai = A[np.ix_(~mg, ~mg)]
+    ev = np.linalg.eigvalsh(Ai)
+    assert ev.min() > 0 and Ai.shape[0] == 2197
+    v = inputs.uniform_global(A.shape[0], 99)
+    _, _, D = ora.gll(8)
+    G = ora.setup(m, want=("G",))["G"]
+    w = ora.ax(m, D, G, v[gid].reshape(m.E, 8, 8, 8), apply_mask=False)
+    ref = (A @ v)[gid].reshape(w.shape)
+    assert np.abs(w - ref).max() <= 2e-15 * np.abs(ref).max() * 8
+
+
+@pytest.mark.parametrize("jit", [0.0, 0.1])
+def test_null_space_of_unmasked_operator(ora, jit):
+    m = ora.Mesh(3, 2, 2, 8, jitter=jit, seed_geom=2005)  # north_star: constants in null space
+    _, _, D = ora.gll(8)
+    G = ora.setup(m, want=("G",))["G"]
+    w = ora.ax(m, D, G, np.ones((m.E, 8, 8, 8)), apply_mask=False)
+    assert np.abs(w).max() <= 2e-15 * np.abs(G).max() * 64
+
+
+def _poly_check(ora, m, fun, lap, tol):
+    _, _, D = ora.gll(m.N)
+    s = ora.setup(m, want=("G", "xyz", "mass", "mask"))
+    x, y, z = s["xyz"][:, 0], s["xyz"][:, 1], s["xyz"][:, 2]
+    w = ora.ax(m, D, s["G"], fun(x, y, z), apply_mask=False)
+    B = ora.dssum(m, s["mass"])
+    ref = -B * lap(x, y, z)
+    um = ~s["mask"].astype(bool)
+    err = np.abs(w - ref)[um].max() / np.abs(ref[um]).max()
+    assert err <= tol, err
+
+
+@pytest.mark.parametrize("N", [4, 8])
+def test_polynomial_exactness_undeformed_tensor_degree_p(ora, N):
+    """P7 (north_star: 'ax is exact for polynomials of degree <= p on the
+    undeformed box'): A u = -B Laplace(u) at unmasked points, u in Q_p."""
+    p = N - 1
+    m = ora.Mesh(2, 2, 2, N)
+    _poly_check(ora, m, lambda x, y, z: x ** p * y ** p * z ** p + x * x,
+                lambda x, y, z: p * (p - 1) * (x ** (p - 2) * y ** p * z ** p
+                                               + x ** p * y ** (p - 2) * z ** p
+                                               + x ** p * y ** p * z ** (p - 2)) + 2.0,
+                2e-12)
+    _poly_check(ora, m, lambda x, y, z: x * x + y * y + z * z, lambda x, y, z: 6.0 + 0 * x, 2e-13)
+
+
+@pytest.mark.parametrize("N", [8, 10, 12])
+def test_polynomial_exactness_jittered_degree2_and_patch(ora, N):
+    m = ora.Mesh(3, 3, 3, N, jitter=0.1, seed_geom=2003)
+    _poly_check(ora, m, lambda x, y, z: x * x - 2 * y * z + 3 * z * z + x,
+                lambda x, y, z: 2.0 + 6.0 + 0 * x, 5e-11)
+    _, _, D = ora.gll(N)
+    s = ora.setup(m, want=("G", "xyz", "mask"))
+    lin = 1.0 + 2 * s["xyz"][:, 0] - s["xyz"][:, 1] + 0.5 * s["xyz"][:, 2]
+    w = ora.ax(m, D, s["G"], lin, apply_mask=False)
+    um = ~s["mask"].astype(bool)
+    assert np.abs(w[um]).max() <= 1e-13  # patch test
+
+
+def test_operator_symmetry_random_continuous(ora):
+    """P8: glsc3(x, c, A y) = glsc3(y, c, A x) for continuous masked x, y."""
+    m = ora.Mesh(3, 2, 2, 8, jitter=0.1, seed_geom=9)
+    _, _, D = ora.gll(8)
+    s = ora.setup(m, want=("G", "gid", "mask"))
+    ng = m.sizes()["n_global"]
+    msk = s["mask"].astype(bool)
+    x = np.where(msk, 0.0, inputs.uniform_global(ng, 1)[s["gid"]])
+    y = np.where(msk, 0.0, inputs.uniform_global(ng, 2)[s["gid"]])
+    c = ora.multiplicity_weight(m)
+    a = ora.glsc3(x, ora.ax(m, D, s["G"], y), c)
+    b = ora.glsc3(y, ora.ax(m, D, s["G"], x), c)
+    assert abs(a - b) <= 1e-14 * abs(a)
+    assert ora.glsc3(x, ora.ax(m, D, s["G"], x), c) > 0  # positive definite
+
+
+def test_fp32_ax_accuracy(ora):
+    """P15: binary32 ax on binary32-rounded inputs vs binary64 ax of the same
+    inputs: max-norm relative error well under the north_star 2e-6."""
+    m = ora.Mesh(3, 3, 2, 10, jitter=0.1, seed_geom=4)
+    xi, _, D = ora.gll(10)
+    G = ora.setup(m, want=("G",))["G"]
+    u = inputs.uniform_field((m.E, 10, 10, 10), 8)
+    D32, G32, u32 = D.astype(np.float32), G.astype(np.float32), u.astype(np.float32)
+    w32 = ora.ax(m, D32, G32, u32)
+    w64 = ora.ax(m, D32.astype(np.float64), G32.astype(np.float64), u32.astype(np.float64))
+    err = np.abs(w32 - w64).max() / np.abs(w64).max()
+    assert err < 2e-6 and err > 0
+    assert ora.ax(m, D32, G32, np.zeros_like(u32)).max() == 0  # ax(0) = 0
+
+
+# -------------------------------------------------------- P14 glsc3
+def test_glsc3_examples(ora):
+    assert ora.glsc3(np.ones(3), np.ones(3), np.ones(3)) == 3.0
+    assert ora.glsc3(np.array([1.0, 2.0]), np.array([3.0, 4.0]), np.array([1.0, 0.5])) == 7.0
+    assert ora.glsc3(np.zeros(0), np.zeros(0), np.zeros(0)) == 0.0
+
+
+@pytest.mark.parametrize("n,cancel", [(1, False), (4096, False), (4096, True), (200_000, True),
+                                      (70_001, False)])
+def test_fsum_correctly_rounded(ora, n, cancel):
+    for seed in range(6):
+        t = inputs.lognormal_terms(n, seed * 13 + n, cancel=cancel)
+        assert ora.fsum(t) == math.fsum(t)
+        c = np.ones(n)
+        assert ora.glsc3(t, np.ones(n), c) == math.fsum(t)
+
+
+def test_fsum_halfway_cases(ora):
+    cases = [[1.0, 2.0 ** -53, 2.0 ** -106], [1.0, -2.0 ** -54, -2.0 ** -108],
+             [2.0 ** 53, 1.0, 2.0 ** -30], [0.1] * 10,
+             [1.0, 1e100, 1.0, -1e100]]
+    for t in cases:
+        assert ora.fsum(np.array(t)) == math.fsum(t), t
+
+
+def test_glsc3_fp32_terms_are_exact(ora):
+    """FP32 loop (north_star: FP64 accumulation): t = (double)a (double)b c is exact."""
+    a = inputs.uniform_field(50_000, 1, np.float32)
+    b = inputs.uniform_field(50_000, 2, np.float32)
+    c = np.random.default_rng(3).choice([1.0, 0.5, 0.25, 0.125], size=50_000)
+    ref = math.fsum(float(x) * float(y) * float(z) for x, y, z in zip(a, b, c))
+    assert ora.glsc3(a, b, c) == ref
+
+
+# ---------------------------------------------------------- CG pins
+@pytest.mark.parametrize("mesh_args", [(2, 1, 1, 4), (2, 2, 2, 3), (3, 2, 2, 3), (2, 2, 1, 4)])
+def test_cg_finite_termination(ora, mesh_args):
+    """P11 (north_star: CG converges in at most n_dof iterations on tiny problems)."""
+    m = ora.Mesh(*mesh_args, seed_rhs=17)
+    _, _, D = ora.gll(m.N)
+    s = ora.setup(m, want=("G", "f"))
+    ndof = m.sizes()["n_interior"]
+    r = ora.cg(m, D, s["G"], s["f"], ndof + 5)
+    rel = r.hist / r.hist[0]
+    assert (rel[: ndof + 1] < 1e-12).any(), (ndof, rel.min())
+    assert r.defect == 0
+
+
+def test_cg_matches_dense_solve_and_energy_decreases(ora):
+    """S:392 dense-solve agreement; S:417 monotone A-norm error."""
+    m = ora.Mesh(2, 2, 1, 4, jitter=0.1, seed_geom=3, seed_rhs=5)
+    _, _, D = ora.gll(4)
+    s = ora.setup(m, want=("G", "f", "gid"))
+    A, gid = dense_stiffness(ora, m)
+    mg = global_mask(ora, m)
+    fg = np.zeros(A.shape[0])
+    fg[gid] = s["f"].reshape(-1)
+    xg = np.zeros_like(fg)
+    Ai = A[np.ix_(~mg, ~mg)]
+    xg[~mg] = np.linalg.solve(Ai, fg[~mg])
+    errs = []
+    for it in range(1, 40):
+        r = ora.cg(m, D, s["G"], s["f"], it)
+        e = r.x.reshape(-1)
+        eg = np.zeros_like(xg)
+        eg[gid] = e
+        d = (eg - xg)[~mg]
+        errs.append(d @ Ai @ d)
+    assert all(errs[i + 1] <= errs[i] * (1 + 1e-9) + 1e-28 for i in range(len(errs) - 1))
+    r = ora.cg(m, D, s["G"], s["f"], 60)
+    assert np.abs(r.x.reshape(-1) - xg[gid]).max() <= 1e-9
+    # scalar trace consistency: h_k = sqrt(rtr_k), rtz1_k = rtr_{k-1}, beta_1 = 0
+    np.testing.assert_array_equal(r.hist[1:], np.sqrt(r.trace[:, 4]))
+    np.testing.assert_array_equal(r.trace[1:, 0], r.trace[:-1, 4])
+    assert r.trace[0, 1] == 0.0
+
+
+def test_cg_zero_rhs(ora):
+    """f = 0 gives x = 0 and residual 0, no defect (C9)."""
+    m = ora.Mesh(2, 2, 2, 4)
+    _, _, D = ora.gll(4)
+    G = ora.setup(m, want=("G",))["G"]
+    f = np.zeros((m.E, 4, 4, 4))
+    for prec in ("fp64", "fp32"):
+        r = ora.cg(m, D, G, f, 10, prec)
+        assert (r.hist == 0).all() and (r.x == 0).all() and r.defect == 0
+
+
+def test_cg_defect_on_indefinite_operator(ora):
+    """pap <= 0 is a defect signal (operator not SPD)."""
+    m = ora.Mesh(2, 2, 2, 4, seed_rhs=3)
+    _, _, D = ora.gll(4)
+    s = ora.setup(m, want=("G", "f"))
+    r = ora.cg(m, D, -s["G"], s["f"], 5)
+    assert r.defect == 1
+
+
+def test_cg_c1_fp64_and_fp32(ora):
+    """P12 / P16 plausibility on C1: FP64 converges ~1e-10 in 100 iterations;
+    the FP32 solver tracks FP64 early, its true FP64 residual floors ~1e-6 h0."""
+    m = ora.Mesh(2, 2, 2, 8, seed_rhs=1001)
+    _, _, D = ora.gll(8)
+    s = ora.setup(m, want=("G", "f"))
+    r64 = ora.cg(m, D, s["G"], s["f"], 100, "fp64")
+    r32 = ora.cg(m, D, s["G"], s["f"], 100, "fp32")
+    assert r64.defect == 0 and r32.defect == 0
+    assert r64.hist[100] / r64.hist[0] < 1e-8
+    rel = np.abs(r32.hist[:20] - r64.hist[:20]) / r64.hist[:20]
+    assert rel.max() < 1e-4
+    tr64, h0 = ora.true_residual(m, D, s["G"], s["f"], r64.x)
+    tr32, _ = ora.true_residual(m, D, s["G"], s["f"], r32.x)
+    assert tr64 / h0 < 1e-8
+    assert 1e-9 < tr32 / h0 < 1e-4
+    xe = np.abs(r32.x - r64.x).max() / np.abs(r64.x).max()
+    assert 1e-9 < xe < 1e-4
