@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native Nekbone CG hot path (arXiv 2405.11065).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl nbk|reference]
+
+A "step" is one complete fixed-iteration CG solve (all SURVEY 8(a) rows a1-a8:
+the fused p/x update + ax_e + mask, dssum, glsc3 reductions, r update, device
+scalars, and the final FP64 residual check) of BASELINE.json's configs[1]
+workload (C2: 16^3 hex elements, N = 8, 100 iterations) by the mixed FP32
+solver, replayed as one CUDA graph with all inputs resident in HBM.  The FP64
+solver is timed the same way and reported beside it.
+
+metric = GDOF*iter/s = n_global * niter / step time (DOF = unique global GLL
+nodes, reading R19).  Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CG GDOF·iter/s FP64 vs FP32 solver; ax/CG-vector HBM GB/s vs B200 peak"
+UNIT = "GDOF*iter/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--impl", default="nbk", choices=["nbk", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg_name, precision):
+    """dram bytes per launch of the fused ax kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d[cfg_name][precision]["k_ax_fused"]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- oracle
+def oracle_sample(cfg, precision, niter_sample, threads=None):
+    """The oracle as it stands, timed on this host's cores on a bounded sample:
+    the FP64 set-up (untimed) and `niter_sample` CG iterations of the workload."""
+    import oracle
+    om = oracle.Mesh(**cfg.mesh_args())
+    _, _, D = oracle.gll(cfg.N)
+    s = oracle.setup(om)
+    t0 = time.perf_counter()
+    oracle.cg(om, D, s["G"], s["f"], niter_sample, precision)
+    dt = time.perf_counter() - t0
+    return om.sizes()["n_global"] * niter_sample / dt / 1e9, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2405_11065_b200.configs import CONFIGS
+    import oracle
+    cfg = CONFIGS[args.config]
+    iters = 20
+    om = oracle.Mesh(**cfg.mesh_args())
+    _, _, D = oracle.gll(cfg.N)
+    s = oracle.setup(om)
+    ng = om.sizes()["n_global"]
+    for _ in range(args.warmup):
+        oracle.cg(om, D, s["G"], s["f"], iters, args.precision)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.cg(om, D, s["G"], s["f"], iters, args.precision)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = ng * iters * args.steps / tot / 1e9
+    cores = oracle.num_threads()
+    sample = (f"{args.config} {args.precision} oracle CG, {iters} of {cfg.niter} iterations per step "
+              f"(set-up untimed), OpenMP threads={cores}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, args.precision), "niter_per_step": iters},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_name(cfg, precision):
+    solver = "mixed FP32 solver (FP64 set-up, FP64 glsc3 accumulation, FP64 final check)" \
+        if precision == "fp32" else "FP64 solver"
+    return (f"{cfg.name}: {cfg.ex}x{cfg.ey}x{cfg.ez} hex box, N={cfg.N} (p={cfg.N - 1}), "
+            f"jitter={cfg.jitter}, {cfg.niter} unpreconditioned CG iterations, {solver}")
+
+
+# ---------------------------------------------------------------- GPU arm
+def time_solves(ctx, torch, cfg, precision, steps, warmup, flush, profile):
+    """Per-step device time (CUDA events on the context stream), L2 flushed
+    between steps (outside the events)."""
+    import paper_2405_11065_b200 as nbk  # noqa: F401
+    ctx.set_profiling(profile)
+    for _ in range(warmup):
+        ctx.cg_solve(cfg.niter, precision, trace=False)
+    s = ctx.stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    kA = []
+    ctx.sync()
+    graph_ms = []
+    for i in range(steps):
+        flush.fill_(i & 0xFF)  # write 512 MiB > 126 MB L2, on the same stream
+        ev[i][0].record(s)
+        hist, _, res = ctx.cg_solve(cfg.niter, precision, trace=False)
+        ev[i][1].record(s)
+        kA.append(res["kA_ms"])
+        graph_ms.append(res["solve_ms"])
+    ctx.sync()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    return ms, kA, graph_ms, res, hist
+
+
+def run_gpu(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    import paper_2405_11065_b200 as nbk
+    cfg = nbk.CONFIGS[args.config]
+    spec = nbk.MeshSpec(**cfg.mesh_args(1))
+    stream = torch.cuda.Stream()
+    ctx = nbk.cg_setup(spec, "fp32", device=local, stream=stream)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    prec = args.precision
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region (headline precision) ----
+    barrier()
+    with torch.cuda.stream(stream), ClockSampler(local) as clk:
+        ms, kA, graph_ms, res, hist = time_solves(ctx, torch, cfg, prec, args.steps, args.warmup,
+                                                  flush, profile=True)
+    barrier()
+    tot_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ng = ctx.n_global
+    value = world * ng * cfg.niter * args.steps / (tot_ms / 1e3) / 1e9
+    launches = ctx.solve_launches(cfg.niter, prec) * args.steps
+
+    # ---- roofline of the dominant kernel (fused ax, K_A) ----
+    s = 4 if prec == "fp32" else 8
+    n = ctx.n_local
+    bytes_ka = 12 * s * n  # reads r, p, x, G (9s) + writes p, x, w (3s) per local point
+    ka_avg_ms = sum(kA) / (args.steps * cfg.niter)
+    peak, peak_src = measured_peak()
+    achieved = bytes_ka / (ka_avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(args.config, prec),
+                "kernel": "k_ax<fused> (p,x update + ax_e + mask + interior pap)",
+                "algorithmic_bytes_per_launch": bytes_ka, "avg_launch_ms": ka_avg_ms,
+                "share_of_step": sum(kA) / tot_ms * world if world == 1 else None,
+                "peak_source": peak_src}
+
+    # ---- FP64 solver beside it ----
+    extra = {}
+    if not args.no_fp64 and prec == "fp32":
+        barrier()
+        with torch.cuda.stream(stream):
+            ms64, kA64, _, res64, _ = time_solves(ctx, torch, cfg, "fp64", args.steps,
+                                                  args.warmup, flush, profile=True)
+        barrier()
+        v64 = ng * cfg.niter * args.steps / (sum(ms64) / 1e3) / 1e9
+        ka64 = sum(kA64) / (args.steps * cfg.niter)
+        extra["fp64"] = {"value": v64, "ms_per_step": sum(ms64) / args.steps,
+                         "k_ax_avg_ms": ka64,
+                         "k_ax_hbm_frac": 12 * 8 * n / (ka64 / 1e3) / 1e9 / peak,
+                         "true_res_rel": res64["true_res_rel"]}
+        extra["speedup_fp32_vs_fp64"] = value / v64
+
+    # ---- end to end through the C ABI with host buffers ----
+    import numpy as np
+    f_host = torch.empty(ctx.shape, dtype=torch.float64).pin_memory()
+    _, _, f0 = ctx.get_arrays()
+    f_host.numpy()[...] = f0
+    x_host = torch.empty(ctx.shape, dtype=torch.float64).pin_memory()
+    ctx.set_profiling(False)
+    for _ in range(args.warmup):
+        ctx.cg_solve_host(f_host.numpy(), cfg.niter, prec, x_host.numpy())
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.cg_solve_host(f_host.numpy(), cfg.niter, prec, x_host.numpy())
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_val = world * ng * cfg.niter * args.steps / (sum(e2e_ms) / 1e3) / 1e9
+    e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 8 * n + 8 * (cfg.niter + 1),
+           "path": "nbk_cg_solve_host (pinned host f -> solve -> host x)"}
+    del np
+
+    # ---- CPU baseline: the oracle on this host, bounded sample ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        iters = 40 if cfg.N <= 8 and cfg.ex * cfg.ey * cfg.ez <= 4096 else 2
+        v_cpu, dt = oracle_sample(cfg, prec, iters)
+        cpu = {"value": v_cpu, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": f"{args.config} {prec} oracle CG, {iters} of {cfg.niter} iterations "
+                         f"({dt:.1f} s; set-up untimed)"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg, prec), "n_global": ng, "n_local": n,
+                       "niter": cfg.niter,
+                       "parallelism": "1 GPU" if world == 1 else f"{world} replicas",
+                       "l2": "flushed between steps (512 MiB write, outside the events)"},
+            "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk.summary(), "true_res_rel": res["true_res_rel"],
+            "h_final_rel": float(hist[-1] / hist[0]) if hist[0] else 0.0,
+            "median_step_ms": statistics.median(ms), **extra}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

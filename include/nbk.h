@@ -1,0 +1,194 @@
+/*
+ * nbk.h -- C ABI of libnbk.so, the B200-native (sm_100a) implementation of the
+ * data-parallel hot path of Nekbone studied in arXiv 2405.11065: the
+ * unpreconditioned conjugate-gradient solve of the 3-D spectral-element
+ * Poisson problem, in FP64 and in the paper's mixed form (FP64 set-up, CG loop
+ * "exclusively in single precision", FP64 final residual check).
+ *
+ * Citations: P:n = PAPER.md line n (T1 = tab:cg-profiling);
+ * S:n = SPEC.md line n; R#/C# = readings / canonical-order rules in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *   - extern "C", plain pointers and sizes; no C++ exceptions cross the ABI.
+ *   - Every call returns nbk_status; on failure nbk_last_error(ctx) (or
+ *     nbk_last_error(NULL) for calls without a context) holds a message.
+ *   - Device pointers ("_dev") are CUDA device addresses in the context's
+ *     device; host pointers ("_host") are ordinary host memory.
+ *   - Local ("E-vector") storage: element-major, i fastest:
+ *       u[e][k][j][i], index L = ((e*N + k)*N + j)*N + i, e = ix + ex*(iy + ey*iz)
+ *     e is rank-local (the rank's slab starts at global element e_offset).
+ *   - Geometric factors: G[e][c][k][j][i], c = g1..g6 = rr, rs, rt, ss, st, tt (R3).
+ *   - Work is enqueued on the context's stream; calls that return host data
+ *     synchronise that stream.  A context is not re-entrant; use one per
+ *     (process, GPU).
+ *   - The CUDA path has no CPU fallback: if the device or kernels are not
+ *     available, nbk_cg_setup fails with NBK_ECUDA.
+ */
+#ifndef NBK_H
+#define NBK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NBK_OK = 0,
+    NBK_EINVAL = 2,  /* bad argument (S:567 exit code 2: config error)          */
+    NBK_EDEFECT = 3, /* pap <= 0 or non-finite scalar during CG (exit 3) */
+    NBK_ECUDA = 4,   /* CUDA runtime error (message in nbk_last_error)          */
+    NBK_ENCCL = 5,   /* NCCL error                                              */
+    NBK_ENOMEM = 6,  /* workspace too small                                     */
+    NBK_ESTATE = 7   /* call in the wrong state / order                         */
+} nbk_status;
+
+typedef enum {
+    NBK_FP64 = 0, /* FP64 CG solver (Nekbone's reference precision)                        */
+    NBK_FP32 = 1  /* mixed: FP64 set-up, FP32 CG loop with FP64 inner-product accumulation
+                     (north_star; reading R11), FP64 final residual check (C12)          */
+} nbk_precision;
+
+/* Box mesh (reading R5): cubic elements of edge h = 1/ex on
+ * [0,1] x [0,ey/ex] x [0,ez/ex]; homogeneous Dirichlet on all 6 faces (R6).
+ * jitter > 0 moves every interior vertex by jitter*h*(2U-1) per coordinate,
+ * U from SplitMix64(seed_geom, 3v+d); the element map is trilinear.
+ * RHS (R7): b_g = 2U-1 from SplitMix64(seed_rhs, g) on unmasked global nodes. */
+typedef struct {
+    int32_t ex, ey, ez; /* GLOBAL element counts, >= 1; ez % nranks == 0          */
+    int32_t N;          /* GLL points per direction, N = p + 1, 2 <= N <= 16     */
+    double jitter;      /* 0 = undeformed; must lie in [0, 0.25]                 */
+    uint64_t seed_geom;
+    uint64_t seed_rhs;
+} nbk_mesh;
+
+/* Process / device placement.  rank owns element layers
+ * iz in [rank*ez/nranks, (rank+1)*ez/nranks) (contiguous z-slabs, R21). */
+typedef struct {
+    int32_t rank, nranks; /* nranks == 1 in this build (multi-rank: see DESIGN.md) */
+    int32_t device;       /* CUDA device ordinal                                    */
+    void* stream;         /* cudaStream_t the library enqueues on (NULL = legacy)   */
+} nbk_dist;
+
+typedef struct {
+    int64_t n_local;  /* local points on this rank, e_local * N^3 (Nekbone's n)     */
+    int64_t n_global; /* unique global GLL nodes of the whole box (R19 DOF unit)    */
+    int64_t e_local;  /* elements on this rank                                      */
+    int64_t e_offset; /* global id of this rank's first element                     */
+    int64_t n_shared; /* unique shared nodes (multiplicity > 1) in the dssum plan   */
+    int64_t n_copies; /* local points belonging to shared nodes                     */
+    int32_t N;
+    int32_t has_fp32; /* FP32 arrays allocated                                      */
+} nbk_info;
+
+/* Outcome of a solve. */
+typedef struct {
+    double true_res;      /* sqrt(glsc3(f - A x, c, f - A x)) evaluated in FP64 (C12) */
+    double true_res_rel;  /* true_res / h_0                                           */
+    int32_t defect_iter;  /* first iteration with pap <= 0 or a non-finite scalar, 0   */
+    int32_t niter;
+    float solve_ms;       /* device time of the CG loop (CUDA events)                  */
+    float kA_ms;          /* summed device time of the fused ax kernel (if profiling)  */
+} nbk_result;
+
+typedef struct nbk_ctx nbk_ctx;
+
+/* Flags of nbk_ax_apply. */
+#define NBK_AX_LOCAL 0 /* w = ax_e(u) per element only (T1 line 5, F2 ax_e)             */
+#define NBK_AX_DSSUM 1 /* ... followed by direct-stiffness summation (dssum)      */
+#define NBK_AX_MASK 2  /* ... and the Dirichlet mask (masked points assigned +0, C5)     */
+
+/* Bytes of device workspace nbk_cg_setup needs for this mesh / precision
+ * (precision NBK_FP32 also allocates the FP64 arrays used by set-up and the
+ * final FP64 check).  Returns NBK_EINVAL for an invalid mesh. */
+nbk_status nbk_workspace_bytes(const nbk_mesh* mesh, nbk_precision precision, const nbk_dist* dist,
+                               size_t* bytes_out);
+
+/* cg_setup(mesh, N, precision) (north_star): FP64 set-up on the device:
+ * GLL nodes/weights/D, geometric factors g1..g6, RHS, dssum plan (sorted
+ * segments over unique global node ids), FP32 copies if precision == NBK_FP32
+ * (C11: RN32 of the FP64 values).  dev_workspace (>= nbk_workspace_bytes,
+ * 256-byte aligned) is caller-owned and must outlive the context; the library
+ * carves every device buffer from it and never frees it.  On success *out is
+ * a new context (free it with nbk_destroy). */
+nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk_dist* dist,
+                        void* dev_workspace, size_t ws_bytes, nbk_ctx** out);
+
+/* Parity path (C10): replace the set-up data with host FP64 arrays (e.g. the
+ * oracle's): D (N*N, row a = evaluation node), G (e_local*6*N^3), f
+ * (e_local*N^3, local storage).  Any pointer may be NULL (keep current).
+ * FP32 copies are re-derived.  Synchronous. */
+nbk_status nbk_load_arrays(nbk_ctx* ctx, const double* D_host, const double* G_host,
+                           const double* f_host);
+
+/* Export the context's FP64 set-up data (for independent-set-up comparison).
+ * Any pointer may be NULL.  Synchronous. */
+nbk_status nbk_get_arrays(nbk_ctx* ctx, double* D_host, double* G_host, double* f_host);
+
+/* ax_apply (north_star; T1 line 5): w = [mask o][dssum o] ax_e(u) for all local
+ * elements, ax_e = D^T G D u_e in the canonical order C1-C3.  u_dev / w_dev:
+ * e_local*N^3 values of the stated precision (double or float); u and w must
+ * not overlap.  Asynchronous on the context stream. */
+nbk_status nbk_ax_apply(nbk_ctx* ctx, const void* u_dev, void* w_dev, int32_t flags,
+                        nbk_precision precision);
+
+/* dssum (north_star; P:125 gather-scatter): every copy of every global node
+ * gets the sum of all its copies, summed in ascending local index (C4); then,
+ * if apply_mask, Dirichlet points are assigned +0 (C5).  In place on f_dev.
+ * Asynchronous. */
+nbk_status nbk_dssum(nbk_ctx* ctx, void* f_dev, int32_t apply_mask, nbk_precision precision);
+
+/* glsc3 (T1 lines 3, 6, 9): sum_L a_L b_L c_L with c = 1/multiplicity, FP64
+ * accumulation (double-double, deterministic tree) and one final rounding (C6).
+ * FP64 vectors: terms RN64(a b) c; FP32 vectors: (double)a (double)b c.
+ * Writes the result to *out_host; synchronous. */
+nbk_status nbk_glsc3(nbk_ctx* ctx, const void* a_dev, const void* b_dev, nbk_precision precision,
+                     double* out_host);
+
+/* cg_solve(niter) (north_star): fixed-iteration unpreconditioned CG (T1,
+ * solveM = identity so rtz1 = previous rtr), x0 = 0, r0 = f, all scalars on
+ * the device, the whole loop replayed as one CUDA graph.  precision selects the
+ * FP64 or the mixed FP32 solver (the context must have been set up with
+ * NBK_FP32 for the latter).  Outputs (host, caller-allocated, may be NULL):
+ *   hist_host  : niter+1 doubles, h_k = sqrt(rtr_k) (R13)
+ *   trace_host : niter*5 doubles, per iteration rtz1, beta, alpha, pap, rtr
+ *   result     : final FP64 true residual (C12), defect iteration, timings.
+ * The solution stays on the device (nbk_get_solution).  Returns NBK_EDEFECT
+ * if a defect was flagged (results are still written).  Synchronous.
+ * 1 <= niter <= 10000. */
+nbk_status nbk_cg_solve(nbk_ctx* ctx, int32_t niter, nbk_precision precision, double* hist_host,
+                        double* trace_host, nbk_result* result);
+
+/* End-to-end form of cg_solve for host data: copies f_host (e_local*N^3 FP64,
+ * NULL = keep the set-up RHS) to the device, solves, and copies the solution
+ * (as FP64, exact for the FP32 solver) to x_host (may be NULL).  Synchronous. */
+nbk_status nbk_cg_solve_host(nbk_ctx* ctx, const double* f_host, int32_t niter,
+                             nbk_precision precision, double* x_host, double* hist_host,
+                             nbk_result* result);
+
+/* Copy the last solution (FP64 view: exact upcast of the FP32 solver's x) to
+ * host memory, e_local*N^3 doubles.  Synchronous. */
+nbk_status nbk_get_solution(nbk_ctx* ctx, double* x_host);
+
+/* Device pointer of the last solution in its native precision (do not free). */
+nbk_status nbk_solution_ptr(nbk_ctx* ctx, nbk_precision precision, void** x_dev);
+
+/* Per-kernel timing inside the solve graph (CUDA events around the fused ax
+ * kernel each iteration).  Takes effect at the next graph build. */
+nbk_status nbk_set_profiling(nbk_ctx* ctx, int32_t enable);
+
+nbk_status nbk_query(const nbk_ctx* ctx, nbk_info* info);
+
+/* Number of kernel launches one nbk_cg_solve(niter, precision) performs. */
+nbk_status nbk_solve_launches(const nbk_ctx* ctx, int32_t niter, nbk_precision precision,
+                              int64_t* launches);
+
+const char* nbk_last_error(const nbk_ctx* ctx);
+const char* nbk_version(void);
+void nbk_destroy(nbk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBK_H */

@@ -1,0 +1,64 @@
+"""Build libnbk.so (the C-ABI CUDA library) in-tree for sm_100a with nvcc.
+
+    python -m paper_2405_11065_b200.build [--force]
+
+Flags: -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo, -fmad=false (no
+contraction except the explicit __fma_rn of the canonical order, DESIGN.md
+CEO-1), IEEE division / sqrt and no flush-to-zero (nvcc defaults, spelled out).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(CSRC, "libnbk.so")
+SOURCES = ["nbk_capi.cu", "nbk_setup.cu"]
+HEADERS = ["nbk_common.cuh", "nbk_kernels.cuh", "nbk_internal.h", "../../include/nbk.h"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-ftz=false", "-prec-div=true",
+         "-prec-sqrt=true", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = SOURCES + HEADERS + [os.path.basename(__file__)]
+    for f in deps:
+        p = os.path.join(CSRC, f) if not f.endswith(".py") else os.path.join(HERE, f)
+        if os.path.exists(p) and os.path.getmtime(p) > t:
+            return True
+    return False
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {src}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+        log = os.path.join(CSRC, src.replace(".cu", ".ptxas.log"))
+        with open(log, "w") as fh:
+            fh.write(r.stderr)
+        objs.append(obj)
+    tmp = LIB + ".tmp"
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    subprocess.check_call(cmd)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,255 @@
+// nbk_common.cuh -- device helpers shared by the libnbk kernels (sm_100a).
+//
+//  * double-double (dd) arithmetic for the FP64-accumulated inner products
+//    glsc3 (T1 lines 3, 6, 9; north_star "FP64 accumulation even in the FP32
+//    solver"; rule C6: one final rounding of a ~106-bit accurate sum);
+//  * structural per-point data of the box mesh: Dirichlet mask (R6) and the
+//    multiplicity m (c = 1/m, R8), computed from indices -- 0 bytes of HBM;
+//  * deterministic warp / block reductions of dd values (fixed trees, no
+//    atomics on values: bitwise reproducible for a fixed launch shape).
+//
+// The whole library is compiled with -fmad=false: no add/mul is contracted
+// into an FMA except the explicit __fma_rn / __fmaf_rn calls of the canonical
+// evaluation order (CEO-1).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nbk {
+
+// ------------------------------------------------------------------ dd
+struct dd {
+    double hi, lo;
+};
+
+// Knuth TwoSum: s + e == a + b exactly (no branch).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e)
+{
+    s = __dadd_rn(a, b);
+    double bb = __dsub_rn(s, a);
+    e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// Dekker Fast2Sum (|a| >= |b| or a == 0).
+__device__ __forceinline__ void fast_two_sum(double a, double b, double& s, double& e)
+{
+    s = __dadd_rn(a, b);
+    e = __dsub_rn(b, __dsub_rn(s, a));
+}
+
+__device__ __forceinline__ dd dd_add(dd a, dd b)
+{
+    double s, e, t, f;
+    two_sum(a.hi, b.hi, s, e);
+    two_sum(a.lo, b.lo, t, f);
+    e = __dadd_rn(e, t);
+    fast_two_sum(s, e, s, e);
+    e = __dadd_rn(e, f);
+    fast_two_sum(s, e, s, e);
+    return dd{s, e};
+}
+
+// Per-thread accumulator: running sum S plus the exact TwoSum errors in C.
+struct acc_t {
+    double s = 0.0, c = 0.0;
+    __device__ __forceinline__ void add(double t)
+    {
+        double s2, e;
+        two_sum(s, t, s2, e);
+        s = s2;
+        c = __dadd_rn(c, e);
+    }
+    __device__ __forceinline__ dd get() const
+    {
+        double h, l;
+        two_sum(s, c, h, l);
+        return dd{h, l};
+    }
+};
+
+__device__ __forceinline__ dd shfl_down_dd(dd v, int off)
+{
+    dd o;
+    o.hi = __shfl_down_sync(0xffffffffu, v.hi, off);
+    o.lo = __shfl_down_sync(0xffffffffu, v.lo, off);
+    return o;
+}
+
+// Fixed-tree block reduction; result valid in thread 0.  Must be called by
+// every thread of the block (blockDim.x a multiple of 32, <= 1024).
+__device__ __forceinline__ dd block_reduce_dd(dd v)
+{
+    __shared__ dd red_smem[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = dd_add(v, shfl_down_dd(v, off));
+    __syncthreads();  // red_smem may be reused by a previous call
+    if (lane == 0) red_smem[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        v = lane < nw ? red_smem[lane] : dd{0.0, 0.0};
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = dd_add(v, shfl_down_dd(v, off));
+    }
+    return v;
+}
+
+// Reduce n dd partials in a fixed order with one block (all threads call).
+__device__ __forceinline__ dd reduce_partials(const dd* parts, int n)
+{
+    dd v{0.0, 0.0};
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        dd p;
+        p.hi = __ldcg(&parts[q].hi);
+        p.lo = __ldcg(&parts[q].lo);
+        v = dd_add(v, p);
+    }
+    return block_reduce_dd(v);
+}
+
+// "Last block finalises": every block publishes its partial, then the block
+// that increments the counter last reduces all partials (order fixed by the
+// partial index, so the result does not depend on which block is last).
+// Returns true in the last block (all threads).
+__device__ __forceinline__ bool publish_and_check_last(dd* parts, int slot, dd v,
+                                                       unsigned int* counter, unsigned int total)
+{
+    __shared__ unsigned int last_flag;
+    if (threadIdx.x == 0) {
+        parts[slot] = v;
+        __threadfence();
+        unsigned int prev = atomicAdd(counter, 1u);
+        last_flag = (prev == total - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    bool last = last_flag != 0;
+    if (last) __threadfence();
+    return last;
+}
+
+// ------------------------------------------------------------------ mesh
+// Rank-local view of the global box mesh (contiguous z-slab, R21).
+struct MeshView {
+    int ex, ey;          // elements in x, y
+    int ez_local, z0;    // element layers on this rank and the first global layer
+    int ezg;             // global element layers
+    int N;
+    int64_t E;           // local elements
+    // magic numbers for division by ex and ex*ey (uint32 fast division)
+    uint32_t ex_mul, ex_shr, exy_mul, exy_shr;
+};
+
+// q = floor(n / d) with (mul, shr) from make_fast_div (round-up method of
+// Granlund & Montgomery; exact for every 32-bit n).
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t mul, uint32_t shr)
+{
+    return (uint32_t)(((uint64_t)__umulhi(n, mul) + n) >> shr);
+}
+
+struct ElemCoord {
+    int ax, ay, azg;
+};
+
+__device__ __forceinline__ ElemCoord elem_coord(const MeshView& m, uint32_t e)
+{
+    uint32_t az = fast_div(e, m.exy_mul, m.exy_shr);
+    uint32_t rem = e - az * (uint32_t)(m.ex * m.ey);
+    uint32_t ay = fast_div(rem, m.ex_mul, m.ex_shr);
+    uint32_t ax = rem - ay * (uint32_t)m.ex;
+    return ElemCoord{(int)ax, (int)ay, (int)az + m.z0};
+}
+
+// Dirichlet node (R6): on any face of the global box.
+__device__ __forceinline__ bool is_masked(const MeshView& m, const ElemCoord& c, int i, int j,
+                                          int k)
+{
+    const int n1 = m.N - 1;
+    return (i == 0 && c.ax == 0) || (i == n1 && c.ax == m.ex - 1) || (j == 0 && c.ay == 0) ||
+           (j == n1 && c.ay == m.ey - 1) || (k == 0 && c.azg == 0) ||
+           (k == n1 && c.azg == m.ezg - 1);
+}
+
+// Multiplicity of the node (number of elements sharing it, R8).
+__device__ __forceinline__ int multiplicity(const MeshView& m, const ElemCoord& c, int i, int j,
+                                            int k)
+{
+    const int n1 = m.N - 1;
+    int mx = ((i == 0 && c.ax > 0) || (i == n1 && c.ax < m.ex - 1)) ? 2 : 1;
+    int my = ((j == 0 && c.ay > 0) || (j == n1 && c.ay < m.ey - 1)) ? 2 : 1;
+    int mz = ((k == 0 && c.azg > 0) || (k == n1 && c.azg < m.ezg - 1)) ? 2 : 1;
+    return mx * my * mz;
+}
+
+// c = 1/m is exact (m in {1,2,4,8}).
+__device__ __forceinline__ double inv_mult(int m)
+{
+    return m == 1 ? 1.0 : (m == 2 ? 0.5 : (m == 4 ? 0.25 : 0.125));
+}
+
+// glsc3 term (C6): FP64 vectors -> RN64(a b) c ; FP32 vectors -> exact product.
+__device__ __forceinline__ double dot_term(double a, double b, double c)
+{
+    return __dmul_rn(__dmul_rn(a, b), c);
+}
+__device__ __forceinline__ double dot_term(float a, float b, double c)
+{
+    return __dmul_rn(__dmul_rn((double)a, (double)b), c);
+}
+
+template <typename T>
+__device__ __forceinline__ T fma_t(T a, T b, T c);
+template <>
+__device__ __forceinline__ double fma_t<double>(double a, double b, double c)
+{
+    return __fma_rn(a, b, c);
+}
+template <>
+__device__ __forceinline__ float fma_t<float>(float a, float b, float c)
+{
+    return __fmaf_rn(a, b, c);
+}
+template <typename T>
+__device__ __forceinline__ T mul_t(T a, T b);
+template <>
+__device__ __forceinline__ double mul_t<double>(double a, double b)
+{
+    return __dmul_rn(a, b);
+}
+template <>
+__device__ __forceinline__ float mul_t<float>(float a, float b)
+{
+    return __fmul_rn(a, b);
+}
+template <typename T>
+__device__ __forceinline__ T add_t(T a, T b);
+template <>
+__device__ __forceinline__ double add_t<double>(double a, double b)
+{
+    return __dadd_rn(a, b);
+}
+template <>
+__device__ __forceinline__ float add_t<float>(float a, float b)
+{
+    return __fadd_rn(a, b);
+}
+
+// ------------------------------------------------------------ CG state
+// Device-resident CG scalars (rule C7); alpha/beta never leave the device.
+struct CgState {
+    double rtr;        // rtr of the previous iteration = rtz1 of the current (z = r)
+    double rtz2;       // rtz1 of the previous iteration
+    double beta;       // beta of the current iteration (for the p update)
+    double alpha;      // alpha of the latest completed pap (x update, r update)
+    double alpham;     // -alpha
+    float beta32, alpha32, alpham32, pad0;
+    double true_rtr;   // glsc3(f - A x, c, f - A x) of the final FP64 check
+    double dot;        // result slot of the standalone glsc3
+    int it;            // current iteration k (1-based)
+    int zero;          // rtz1 == 0 reached (rule C9): alpha = beta = 0 from then on
+    int defect;        // first iteration with pap <= 0 or a non-finite scalar
+    int pad1;
+    unsigned int cnt[4];  // last-block counters (reset by the finaliser)
+};
+
+}  // namespace nbk

@@ -1,0 +1,71 @@
+// nbk_internal.h -- host-side context of libnbk (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/nbk.h"
+#include "nbk_common.cuh"
+
+#define NBK_MAX_NITER 10000
+#define NBK_VEC_GRID_MAX (148 * 8)
+
+struct nbk_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaEvent_t> prof_events;  // 2 per iteration when profiling
+    int64_t launches = 0;
+};
+
+struct nbk_ctx {
+    nbk_mesh mesh{};
+    nbk_dist dist{};
+    nbk_precision setup_precision = NBK_FP64;
+    cudaStream_t stream = nullptr;
+    int N = 0;
+    int64_t E = 0, n = 0, n_global = 0, e_offset = 0;
+    int64_t nseg = 0, ncopies = 0;
+    nbk::MeshView view{};
+    std::string err;
+
+    // device buffers (carved from the caller's workspace)
+    nbk::CgState* st = nullptr;
+    double *D64 = nullptr, *G64 = nullptr, *f64 = nullptr;
+    double *x64 = nullptr, *r64 = nullptr, *p64 = nullptr, *w64 = nullptr;
+    float *D32 = nullptr, *G32 = nullptr;
+    float *x32 = nullptr, *r32 = nullptr, *p32 = nullptr, *w32 = nullptr;
+    double *hist = nullptr, *trace = nullptr;
+    nbk::dd* parts = nullptr;
+    int64_t nparts = 0;
+    int32_t *seg_off = nullptr, *seg_idx = nullptr;
+    unsigned char* scratch = nullptr;  // set-up scratch (aliases the vector region)
+    size_t scratch_bytes = 0;
+
+    double h0_64 = 0.0;  // sqrt(glsc3(f64, c, f64)) (C12 denominator)
+    int profiling = 0;
+    std::map<std::tuple<int, int, int>, nbk_graph> graphs;  // (precision, niter, profiling)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int last_solved_precision = -1;
+};
+
+namespace nbk {
+
+struct Layout {
+    size_t off_state, off_D64, off_D32, off_hist, off_trace, off_parts, off_segoff, off_segidx,
+        off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
+    int64_t E, n, n_global, nseg, ncopies, nparts, e_offset;
+    size_t scratch_need;
+};
+
+// Host helpers implemented in nbk_setup.cu
+bool validate_mesh(const nbk_mesh* m, const nbk_dist* d, std::string& why);
+Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d);
+MeshView make_view(const nbk_mesh* m, const nbk_dist* d);
+void gll_host(int N, double* xi, double* rho, double* D);
+cudaError_t setup_device(nbk_ctx* ctx, const Layout& L);
+cudaError_t build_plan(nbk_ctx* ctx);
+
+}  // namespace nbk

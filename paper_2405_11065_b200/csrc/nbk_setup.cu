@@ -1,0 +1,407 @@
+// nbk_setup.cu -- cg_setup: the library's own FP64 set-up on the device
+// ("Maintain the initialisation part in double precision").
+//
+//  * GLL nodes / weights / derivative matrix on the host (tiny), by the
+//    Legendre-Vandermonde Newton iteration x <- x - (x P_p - P_{p-1}) / (N P_p)
+//    from Chebyshev-Gauss-Lobatto guesses (independent of the oracle, which
+//    runs Newton on P'_p); D closed form with the negative-sum diagonal (R17).
+//  * Geometric factors g1..g6 (R3, R5) with the ANALYTIC trilinear Jacobian
+//    (the oracle differentiates the GLL coordinates with D instead).
+//  * RHS b_g = 2U-1 from SplitMix64(seed_rhs, g) on unmasked nodes (R7).
+//  * dssum plan: local points sorted by (global node id, local index) with a
+//    stable radix sort; runs of length > 1 become segments (ascending local
+//    index inside a segment = the canonical chain order C4).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+#include <cstring>
+
+#include "nbk_internal.h"
+
+namespace nbk {
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+bool validate_mesh(const nbk_mesh* m, const nbk_dist* d, std::string& why)
+{
+    if (!m) { why = "mesh is NULL"; return false; }
+    if (m->ex < 1 || m->ey < 1 || m->ez < 1) { why = "element counts must be >= 1"; return false; }
+    if (m->N < 2 || m->N > 16) { why = "N must lie in [2, 16]"; return false; }
+    if (!(m->jitter >= 0.0 && m->jitter <= 0.25)) { why = "jitter must lie in [0, 0.25]"; return false; }
+    int nr = d ? d->nranks : 1, rk = d ? d->rank : 0;
+    if (nr < 1 || rk < 0 || rk >= nr) { why = "bad rank / nranks"; return false; }
+    if (m->ez % nr != 0) { why = "ez must be divisible by nranks"; return false; }
+    if (nr != 1) { why = "multi-rank slabs are not enabled in this build (nranks must be 1)"; return false; }
+    int64_t n = (int64_t)m->ex * m->ey * (m->ez / nr) * m->N * m->N * m->N;
+    if (n >= (int64_t)1 << 31) { why = "local point count must fit in int32"; return false; }
+    int64_t ng = ((int64_t)m->ex * (m->N - 1) + 1) * ((int64_t)m->ey * (m->N - 1) + 1) *
+                 ((int64_t)m->ez * (m->N - 1) + 1);
+    if (ng >= (int64_t)1 << 32) { why = "global node count must fit in uint32"; return false; }
+    return true;
+}
+
+// shared-node counts of an ex*ey*ez box (Appendix B)
+static void box_counts(int64_t ex, int64_t ey, int64_t ez, int64_t N, int64_t& nglob,
+                       int64_t& nshared)
+{
+    int64_t Gx = ex * (N - 1) + 1, Gy = ey * (N - 1) + 1, Gz = ez * (N - 1) + 1;
+    nglob = Gx * Gy * Gz;
+    nshared = nglob - (Gx - (ex - 1)) * (Gy - (ey - 1)) * (Gz - (ez - 1));
+}
+
+static void make_fast_div(uint32_t d, uint32_t& mul, uint32_t& shr)
+{
+    uint32_t l = 0;
+    while (((uint64_t)1 << l) < d) ++l;
+    mul = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << l) - d)) / d + 1);
+    shr = l;
+}
+
+MeshView make_view(const nbk_mesh* m, const nbk_dist* d)
+{
+    int nr = d ? d->nranks : 1, rk = d ? d->rank : 0;
+    MeshView v{};
+    v.ex = m->ex;
+    v.ey = m->ey;
+    v.ez_local = m->ez / nr;
+    v.z0 = rk * v.ez_local;
+    v.ezg = m->ez;
+    v.N = m->N;
+    v.E = (int64_t)v.ex * v.ey * v.ez_local;
+    make_fast_div((uint32_t)v.ex, v.ex_mul, v.ex_shr);
+    make_fast_div((uint32_t)(v.ex * v.ey), v.exy_mul, v.exy_shr);
+    return v;
+}
+
+static size_t plan_scratch_bytes(int64_t n)
+{
+    size_t sort_tmp = 0, scan_tmp = 0;
+    cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int)n);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+    return 6 * align256((size_t)n * 4) + align256(sort_tmp > scan_tmp ? sort_tmp : scan_tmp) + 256;
+}
+
+Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
+{
+    Layout L{};
+    MeshView v = make_view(m, d);
+    const int64_t N = m->N, N3 = N * N * N;
+    L.E = v.E;
+    L.n = L.E * N3;
+    L.e_offset = (int64_t)v.z0 * v.ex * v.ey;
+    int64_t ngl, nsh_dummy;
+    box_counts(m->ex, m->ey, m->ez, N, L.n_global, nsh_dummy);
+    box_counts(m->ex, m->ey, v.ez_local, N, ngl, L.nseg);
+    L.ncopies = L.n - (ngl - L.nseg);
+    const int epb = (256 / (N * N)) > 0 ? (int)(256 / (N * N)) : 1;
+    L.nparts = (L.E + epb - 1) / epb + 2 * NBK_VEC_GRID_MAX + 64;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
+    L.off_state = take(sizeof(CgState));
+    L.off_D64 = take(8 * N * N);
+    L.off_D32 = take(4 * N * N);
+    L.off_hist = take(8 * (NBK_MAX_NITER + 1));
+    L.off_trace = take(8 * 5 * (size_t)NBK_MAX_NITER);
+    L.off_parts = take(sizeof(dd) * (size_t)L.nparts);
+    L.off_segoff = take(4 * (size_t)(L.nseg + 1));
+    L.off_segidx = take(4 * (size_t)(L.ncopies > 0 ? L.ncopies : 1));
+    L.off_G64 = take(8 * 6 * (size_t)L.n);
+    L.off_f64 = take(8 * (size_t)L.n);
+    L.scratch_need = plan_scratch_bytes(L.n);
+    size_t vec64 = 4 * align256(8 * (size_t)L.n);
+    L.off_vec64 = take(vec64 > L.scratch_need ? vec64 : L.scratch_need);
+    if (prec == NBK_FP32) {
+        L.off_G32 = take(4 * 6 * (size_t)L.n);
+        L.off_vec32 = take(4 * align256(4 * (size_t)L.n));
+    } else {
+        L.off_G32 = L.off_vec32 = 0;
+    }
+    L.total = o;
+    return L;
+}
+
+// ------------------------------------------------------------------ GLL
+static void legendre_all(int p, double x, double* P)
+{
+    P[0] = 1.0;
+    if (p >= 1) P[1] = x;
+    for (int k = 2; k <= p; ++k) P[k] = ((2.0 * k - 1.0) * x * P[k - 1] - (k - 1.0) * P[k - 2]) / k;
+}
+
+void gll_host(int N, double* xi, double* rho, double* D)
+{
+    const int p = N - 1;
+    const double pi = 3.141592653589793238462643;
+    double x[32], P[33];
+    for (int j = 0; j < N; ++j) x[j] = std::cos(pi * j / p);  // descending
+    for (int it = 0; it < 200; ++it) {
+        double dmax = 0.0;
+        for (int j = 0; j < N; ++j) {
+            legendre_all(p, x[j], P);
+            double xn = x[j] - (x[j] * P[p] - P[p - 1]) / (N * P[p]);
+            dmax = std::fmax(dmax, std::fabs(xn - x[j]));
+            x[j] = xn;
+        }
+        if (dmax <= 2.2e-16) break;
+    }
+    for (int j = 0; j < N; ++j) xi[j] = -x[j];  // ascending
+    xi[0] = -1.0;
+    xi[p] = 1.0;
+    for (int j = 0; j < N / 2; ++j) {
+        double a = 0.5 * (xi[p - j] - xi[j]);
+        xi[j] = -a;
+        xi[p - j] = a;
+    }
+    if (N % 2) xi[p / 2] = 0.0;
+    double Pp[32];
+    for (int j = 0; j < N; ++j) {
+        legendre_all(p, xi[j], P);
+        Pp[j] = P[p];
+        rho[j] = 2.0 / (p * (double)N * P[p] * P[p]);
+    }
+    for (int a = 0; a < N; ++a) {
+        double s = 0.0;
+        for (int b = 0; b < N; ++b) {
+            if (a == b) continue;
+            double v = Pp[a] / (Pp[b] * (xi[a] - xi[b]));
+            D[a * N + b] = v;
+            s += v;
+        }
+        D[a * N + a] = -s;
+    }
+}
+
+// ------------------------------------------------------------ device setup
+struct GeoParams {
+    double xi[16], rho[16];
+    int N;
+    double jitter;
+    unsigned long long seed_geom, seed_rhs;
+    MeshView v;
+};
+
+__device__ __forceinline__ unsigned long long splitmix64_dev(unsigned long long seed,
+                                                             unsigned long long i)
+{
+    unsigned long long z = seed + (i + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ double pm1_dev(unsigned long long seed, unsigned long long i)
+{
+    const double u = __dmul_rn((double)(splitmix64_dev(seed, i) >> 11), 0x1.0p-53);
+    return __dsub_rn(__dmul_rn(2.0, u), 1.0);
+}
+
+// One block per element: 8 vertices in smem, then one thread per point.
+__global__ void __launch_bounds__(256) k_geom(GeoParams gp, double* G)
+{
+    __shared__ double V[8][3];
+    const MeshView& m = gp.v;
+    const int N = gp.N, N3 = N * N * N;
+    const int64_t e = blockIdx.x;
+    ElemCoord ec = elem_coord(m, (uint32_t)e);
+    const double h = 1.0 / m.ex;
+    if (threadIdx.x < 8) {
+        const int a = threadIdx.x & 1, b = (threadIdx.x >> 1) & 1, c = threadIdx.x >> 2;
+        const long long vx = ec.ax + a, vy = ec.ay + b, vz = ec.azg + c;
+        double pos[3] = {vx * h, vy * h, vz * h};
+        const bool interior = vx > 0 && vx < m.ex && vy > 0 && vy < m.ey && vz > 0 && vz < m.ezg;
+        if (gp.jitter > 0.0 && interior) {
+            const long long vid = vx + (long long)(m.ex + 1) * (vy + (long long)(m.ey + 1) * vz);
+            for (int d = 0; d < 3; ++d)
+                pos[d] += gp.jitter * h * pm1_dev(gp.seed_geom, (unsigned long long)(3 * vid + d));
+        }
+        for (int d = 0; d < 3; ++d) V[threadIdx.x][d] = pos[d];
+    }
+    __syncthreads();
+    for (int pt = threadIdx.x; pt < N3; pt += blockDim.x) {
+        const int i = pt % N, j = (pt / N) % N, k = pt / (N * N);
+        const double r = gp.xi[i], s = gp.xi[j], t = gp.xi[k];
+        const double fr[2] = {0.5 * (1.0 - r), 0.5 * (1.0 + r)};
+        const double fs[2] = {0.5 * (1.0 - s), 0.5 * (1.0 + s)};
+        const double ft[2] = {0.5 * (1.0 - t), 0.5 * (1.0 + t)};
+        const double dl[2] = {-0.5, 0.5};
+        double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // J[d][m] = dx_d/dr_m
+        for (int v = 0; v < 8; ++v) {
+            const int a = v & 1, b = (v >> 1) & 1, c = v >> 2;
+            const double wr = dl[a] * fs[b] * ft[c], ws = fr[a] * dl[b] * ft[c],
+                         wt = fr[a] * fs[b] * dl[c];
+            for (int d = 0; d < 3; ++d) {
+                J[d][0] += wr * V[v][d];
+                J[d][1] += ws * V[v][d];
+                J[d][2] += wt * V[v][d];
+            }
+        }
+        // adjugate A[m][d] = (J^-1)[m][d] * det
+        double A[3][3];
+        A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+        A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+        A[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+        A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+        A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+        A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+        A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        const double det = J[0][0] * A[0][0] + J[0][1] * A[1][0] + J[0][2] * A[2][0];
+        const double W = gp.rho[i] * gp.rho[j] * gp.rho[k];
+        const double sc = W / det;  // G = W det J^-1 J^-T = (W/det) A A^T
+        double g[6];
+        const int mm[6] = {0, 0, 0, 1, 1, 2}, nn[6] = {0, 1, 2, 1, 2, 2};
+        for (int q = 0; q < 6; ++q) {
+            const int a = mm[q], b = nn[q];
+            g[q] = sc * (A[a][0] * A[b][0] + A[a][1] * A[b][1] + A[a][2] * A[b][2]);
+        }
+        double* Ge = G + e * 6 * N3 + pt;
+        for (int q = 0; q < 6; ++q) Ge[q * N3] = g[q];
+    }
+}
+
+__device__ __forceinline__ uint32_t point_gid_dev(const MeshView& m, int64_t L, bool* masked)
+{
+    const int N = m.N, N3 = N * N * N;
+    const uint32_t e = (uint32_t)(L / N3);
+    const int rem = (int)(L - (int64_t)e * N3);
+    const int i = rem % N, j = (rem / N) % N, k = rem / (N * N);
+    ElemCoord ec = elem_coord(m, e);
+    const uint32_t Gx = (uint32_t)m.ex * (N - 1) + 1, Gy = (uint32_t)m.ey * (N - 1) + 1;
+    const uint32_t gx = ec.ax * (N - 1) + i, gy = ec.ay * (N - 1) + j, gz = ec.azg * (N - 1) + k;
+    if (masked) *masked = is_masked(m, ec, i, j, k);
+    return gx + Gx * (gy + Gy * gz);
+}
+
+__global__ void __launch_bounds__(256) k_rhs(MeshView m, unsigned long long seed, double* f)
+{
+    const int64_t n = m.E * m.N * m.N * m.N;
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
+         L += (int64_t)gridDim.x * blockDim.x) {
+        bool msk;
+        uint32_t g = point_gid_dev(m, L, &msk);
+        f[L] = msk ? 0.0 : pm1_dev(seed, g);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gid_keys(MeshView m, uint32_t* keys, uint32_t* vals)
+{
+    const int64_t n = m.E * m.N * m.N * m.N;
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
+         L += (int64_t)gridDim.x * blockDim.x) {
+        keys[L] = point_gid_dev(m, L, nullptr);
+        vals[L] = (uint32_t)L;
+    }
+}
+
+// flag_head[q] = 1 if q starts a run of length > 1; in_run[q] = 1 if q's run has length > 1
+__global__ void __launch_bounds__(256) k_run_flags(const uint32_t* keys, int64_t n, uint32_t* head,
+                                                   uint32_t* inrun)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = keys[q];
+        const bool same_prev = q > 0 && keys[q - 1] == k;
+        const bool same_next = q + 1 < n && keys[q + 1] == k;
+        head[q] = (!same_prev && same_next) ? 1u : 0u;
+        inrun[q] = (same_prev || same_next) ? 1u : 0u;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scatter_plan(const uint32_t* vals, const uint32_t* head,
+                                                      const uint32_t* inrun,
+                                                      const uint32_t* head_pos,
+                                                      const uint32_t* run_pos, int64_t n,
+                                                      int32_t* seg_off, int32_t* seg_idx,
+                                                      int64_t ncopies, int64_t nseg)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        if (inrun[q]) seg_idx[run_pos[q]] = (int32_t)vals[q];
+        if (head[q]) seg_off[head_pos[q]] = (int32_t)run_pos[q];
+        if (q == 0) seg_off[nseg] = (int32_t)ncopies;
+    }
+}
+
+static int grid_for(int64_t n, int cap = 148 * 16)
+{
+    int64_t g = (n + 255) / 256;
+    if (g < 1) g = 1;
+    return (int)(g > cap ? cap : g);
+}
+
+cudaError_t build_plan(nbk_ctx* ctx)
+{
+    const int64_t n = ctx->n;
+    cudaStream_t s = ctx->stream;
+    unsigned char* base = ctx->scratch;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { unsigned char* r = base + o; o += align256(bytes); return r; };
+    uint32_t* k0 = (uint32_t*)take(4 * n);
+    uint32_t* k1 = (uint32_t*)take(4 * n);
+    uint32_t* v0 = (uint32_t*)take(4 * n);
+    uint32_t* v1 = (uint32_t*)take(4 * n);
+    uint32_t* head = (uint32_t*)take(4 * n);
+    uint32_t* inrun = (uint32_t*)take(4 * n);
+    void* tmp = base + o;
+    size_t tmp_bytes = ctx->scratch_bytes - o;
+    k_gid_keys<<<grid_for(n), 256, 0, s>>>(ctx->view, k0, v0);
+    cub::DoubleBuffer<uint32_t> kb(k0, k1), vb(v0, v1);
+    int end_bit = 1;
+    while (end_bit < 32 && ((uint64_t)1 << end_bit) < (uint64_t)ctx->n_global) ++end_bit;
+    size_t need = 0;
+    cudaError_t err = cub::DeviceRadixSort::SortPairs(nullptr, need, kb, vb, (int)n, 0, end_bit, s);
+    if (err != cudaSuccess) return err;
+    if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+    err = cub::DeviceRadixSort::SortPairs(tmp, need, kb, vb, (int)n, 0, end_bit, s);
+    if (err != cudaSuccess) return err;
+    uint32_t* keys = kb.Current();
+    uint32_t* vals = vb.Current();
+    uint32_t* kalt = kb.Alternate();  // reuse as head_pos
+    uint32_t* valt = vb.Alternate();  // reuse as run_pos
+    k_run_flags<<<grid_for(n), 256, 0, s>>>(keys, n, head, inrun);
+    err = cub::DeviceScan::ExclusiveSum(nullptr, need, head, kalt, (int)n, s);
+    if (err != cudaSuccess) return err;
+    if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+    err = cub::DeviceScan::ExclusiveSum(tmp, need, head, kalt, (int)n, s);
+    if (err != cudaSuccess) return err;
+    err = cub::DeviceScan::ExclusiveSum(tmp, need, inrun, valt, (int)n, s);
+    if (err != cudaSuccess) return err;
+    k_scatter_plan<<<grid_for(n), 256, 0, s>>>(vals, head, inrun, kalt, valt, n, ctx->seg_off,
+                                              ctx->seg_idx, ctx->ncopies, ctx->nseg);
+    // check the counts match the analytic plan size
+    uint32_t last_head, last_run, h_last, r_last;
+    cudaMemcpyAsync(&last_head, kalt + n - 1, 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&last_run, valt + n - 1, 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&h_last, head + n - 1, 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&r_last, inrun + n - 1, 4, cudaMemcpyDeviceToHost, s);
+    err = cudaStreamSynchronize(s);
+    if (err != cudaSuccess) return err;
+    if ((int64_t)(last_head + h_last) != ctx->nseg || (int64_t)(last_run + r_last) != ctx->ncopies)
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t setup_device(nbk_ctx* ctx, const Layout& L)
+{
+    (void)L;
+    GeoParams gp{};
+    double D[256];
+    gll_host(ctx->N, gp.xi, gp.rho, D);
+    gp.N = ctx->N;
+    gp.jitter = ctx->mesh.jitter;
+    gp.seed_geom = ctx->mesh.seed_geom;
+    gp.seed_rhs = ctx->mesh.seed_rhs;
+    gp.v = ctx->view;
+    cudaStream_t s = ctx->stream;
+    cudaError_t err = cudaMemcpyAsync(ctx->D64, D, 8 * ctx->N * ctx->N, cudaMemcpyHostToDevice, s);
+    if (err != cudaSuccess) return err;
+    err = build_plan(ctx);  // uses the vector region as scratch: before f / vectors
+    if (err != cudaSuccess) return err;
+    k_geom<<<(unsigned)ctx->E, 256, 0, s>>>(gp, ctx->G64);
+    k_rhs<<<grid_for(ctx->n), 256, 0, s>>>(ctx->view, gp.seed_rhs, ctx->f64);
+    return cudaGetLastError();
+}
+
+}  // namespace nbk

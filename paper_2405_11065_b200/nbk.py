@@ -1,0 +1,279 @@
+"""Thin Python binding of libnbk.so (include/nbk.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels.  PyTorch is used
+for device memory (the caller-owned workspace and field tensors) and streams.
+There is no CPU fallback: if ``csrc/libnbk.so`` is missing or no CUDA device is
+present, the calls raise.
+
+Names follow the north_star boundary: ``cg_setup``, ``ax_apply``, ``dssum``,
+``glsc3``, ``cg_solve``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "csrc", "libnbk.so")
+
+NBK_OK, NBK_EINVAL, NBK_EDEFECT, NBK_ECUDA, NBK_ENCCL, NBK_ENOMEM, NBK_ESTATE = 0, 2, 3, 4, 5, 6, 7
+NBK_FP64, NBK_FP32 = 0, 1
+AX_LOCAL, AX_DSSUM, AX_MASK = 0, 1, 2
+PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32}
+
+# every symbol include/nbk.h declares
+SYMBOLS = ["nbk_workspace_bytes", "nbk_cg_setup", "nbk_load_arrays", "nbk_get_arrays",
+           "nbk_ax_apply", "nbk_dssum", "nbk_glsc3", "nbk_cg_solve", "nbk_cg_solve_host",
+           "nbk_get_solution", "nbk_solution_ptr", "nbk_set_profiling", "nbk_query",
+           "nbk_solve_launches", "nbk_last_error", "nbk_version", "nbk_destroy"]
+
+
+class NbkError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libnbk status {status}: {msg}")
+        self.status = status
+
+
+class CMesh(ctypes.Structure):
+    _fields_ = [("ex", ctypes.c_int32), ("ey", ctypes.c_int32), ("ez", ctypes.c_int32),
+                ("N", ctypes.c_int32), ("jitter", ctypes.c_double),
+                ("seed_geom", ctypes.c_uint64), ("seed_rhs", ctypes.c_uint64)]
+
+
+class CDist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("stream", ctypes.c_void_p)]
+
+
+class CInfo(ctypes.Structure):
+    _fields_ = [("n_local", ctypes.c_int64), ("n_global", ctypes.c_int64),
+                ("e_local", ctypes.c_int64), ("e_offset", ctypes.c_int64),
+                ("n_shared", ctypes.c_int64), ("n_copies", ctypes.c_int64),
+                ("N", ctypes.c_int32), ("has_fp32", ctypes.c_int32)]
+
+
+class CResult(ctypes.Structure):
+    _fields_ = [("true_res", ctypes.c_double), ("true_res_rel", ctypes.c_double),
+                ("defect_iter", ctypes.c_int32), ("niter", ctypes.c_int32),
+                ("solve_ms", ctypes.c_float), ("kA_ms", ctypes.c_float)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libnbk.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -m paper_2405_11065_b200.build` (no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    P = ctypes.POINTER
+    sig = {
+        "nbk_workspace_bytes": [P(CMesh), ctypes.c_int, P(CDist), P(ctypes.c_size_t)],
+        "nbk_cg_setup": [P(CMesh), ctypes.c_int, P(CDist), vp, ctypes.c_size_t, P(vp)],
+        "nbk_load_arrays": [vp, vp, vp, vp],
+        "nbk_get_arrays": [vp, vp, vp, vp],
+        "nbk_ax_apply": [vp, vp, vp, i32, ctypes.c_int],
+        "nbk_dssum": [vp, vp, i32, ctypes.c_int],
+        "nbk_glsc3": [vp, vp, vp, ctypes.c_int, P(ctypes.c_double)],
+        "nbk_cg_solve": [vp, i32, ctypes.c_int, vp, vp, P(CResult)],
+        "nbk_cg_solve_host": [vp, vp, i32, ctypes.c_int, vp, vp, P(CResult)],
+        "nbk_get_solution": [vp, vp],
+        "nbk_solution_ptr": [vp, ctypes.c_int, P(vp)],
+        "nbk_set_profiling": [vp, i32],
+        "nbk_query": [vp, P(CInfo)],
+        "nbk_solve_launches": [vp, i32, ctypes.c_int, P(i64)],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    L.nbk_last_error.argtypes = [vp]
+    L.nbk_last_error.restype = ctypes.c_char_p
+    L.nbk_version.argtypes = []
+    L.nbk_version.restype = ctypes.c_char_p
+    L.nbk_destroy.argtypes = [vp]
+    L.nbk_destroy.restype = None
+    _lib = L
+    return L
+
+
+def _check(st: int, ctx=None, ok=(NBK_OK,)):
+    if st not in ok:
+        msg = load().nbk_last_error(ctx).decode()
+        raise NbkError(st, msg)
+    return st
+
+
+def _ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"] and a.dtype == np.float64
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+@dataclass(frozen=True)
+class MeshSpec:
+    ex: int
+    ey: int
+    ez: int
+    N: int
+    jitter: float = 0.0
+    seed_geom: int = 0
+    seed_rhs: int = 0
+
+    def c(self) -> CMesh:
+        return CMesh(self.ex, self.ey, self.ez, self.N, float(self.jitter),
+                     self.seed_geom & (2**64 - 1), self.seed_rhs & (2**64 - 1))
+
+    @property
+    def E(self) -> int:
+        return self.ex * self.ey * self.ez
+
+
+def workspace_bytes(mesh: MeshSpec, precision: str = "fp32", nranks: int = 1, rank: int = 0) -> int:
+    out = ctypes.c_size_t(0)
+    d = CDist(rank, nranks, 0, None)
+    _check(load().nbk_workspace_bytes(ctypes.byref(mesh.c()), PREC[precision], ctypes.byref(d),
+                                      ctypes.byref(out)))
+    return int(out.value)
+
+
+class Context:
+    """cg_setup(mesh, N, precision): a device-resident problem (one per GPU)."""
+
+    def __init__(self, mesh: MeshSpec, precision: str = "fp32", device: int = 0, stream=None):
+        import torch
+        self.torch = torch
+        if not torch.cuda.is_available():
+            raise NbkError(NBK_ECUDA, "no CUDA device: libnbk has no CPU fallback")
+        self.lib = load()
+        self.mesh = mesh
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        nbytes = workspace_bytes(mesh, precision)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self._ctx = ctypes.c_void_p(None)
+        d = CDist(0, 1, device, ctypes.c_void_p(self.stream.cuda_stream))
+        _check(self.lib.nbk_cg_setup(ctypes.byref(mesh.c()), PREC[precision], ctypes.byref(d),
+                                     ctypes.c_void_p(self.workspace.data_ptr()), nbytes,
+                                     ctypes.byref(self._ctx)))
+        info = CInfo()
+        _check(self.lib.nbk_query(self._ctx, ctypes.byref(info)), self._ctx)
+        self.info = {k: getattr(info, k) for k, _ in CInfo._fields_}
+        self.n_local = info.n_local
+        self.n_global = info.n_global
+        self.N = mesh.N
+        self.shape = (info.e_local, mesh.N, mesh.N, mesh.N)
+
+    # ------------------------------------------------------------------
+    def close(self):
+        if self._ctx:
+            self.lib.nbk_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        self.stream.synchronize()
+
+    def _dev(self, t, dtype):
+        assert t.is_cuda and t.is_contiguous() and t.dtype == dtype and t.numel() == self.n_local
+        return ctypes.c_void_p(t.data_ptr())
+
+    @staticmethod
+    def _prec_of(t):
+        import torch
+        return "fp64" if t.dtype == torch.float64 else "fp32"
+
+    # ---------------------------------------------------------------- ABI
+    def load_arrays(self, D=None, G=None, f=None):
+        """Parity path (C10): ingest host FP64 arrays (e.g. the oracle's)."""
+        arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in (D, G, f)]
+        _check(self.lib.nbk_load_arrays(self._ctx, *[_ptr(a) for a in arrs]), self._ctx)
+
+    def get_arrays(self):
+        N, n = self.N, self.n_local
+        D = np.zeros((N, N))
+        G = np.zeros((self.shape[0], 6, N, N, N))
+        f = np.zeros(self.shape)
+        _check(self.lib.nbk_get_arrays(self._ctx, _ptr(D), _ptr(G), _ptr(f)), self._ctx)
+        del n
+        return D, G, f
+
+    def ax_apply(self, u, w, flags: int = AX_DSSUM | AX_MASK):
+        prec = self._prec_of(u)
+        with self.torch.cuda.stream(self.stream):
+            _check(self.lib.nbk_ax_apply(self._ctx, self._dev(u, u.dtype), self._dev(w, u.dtype),
+                                         flags, PREC[prec]), self._ctx)
+        return w
+
+    def dssum(self, f, apply_mask: bool = False):
+        prec = self._prec_of(f)
+        _check(self.lib.nbk_dssum(self._ctx, self._dev(f, f.dtype), int(apply_mask), PREC[prec]),
+               self._ctx)
+        return f
+
+    def glsc3(self, a, b) -> float:
+        prec = self._prec_of(a)
+        out = ctypes.c_double(0.0)
+        _check(self.lib.nbk_glsc3(self._ctx, self._dev(a, a.dtype), self._dev(b, a.dtype),
+                                  PREC[prec], ctypes.byref(out)), self._ctx)
+        return float(out.value)
+
+    def set_profiling(self, on: bool):
+        _check(self.lib.nbk_set_profiling(self._ctx, int(on)), self._ctx)
+
+    def cg_solve(self, niter: int, precision: str = "fp32", trace: bool = True):
+        hist = np.zeros(niter + 1)
+        tr = np.zeros((niter, 5)) if trace else None
+        res = CResult()
+        st = self.lib.nbk_cg_solve(self._ctx, niter, PREC[precision], _ptr(hist),
+                                   _ptr(tr) if trace else None, ctypes.byref(res))
+        _check(st, self._ctx, ok=(NBK_OK, NBK_EDEFECT))
+        out = {k: getattr(res, k) for k, _ in CResult._fields_}
+        return hist, tr, out
+
+    def cg_solve_host(self, f_host, niter: int, precision: str = "fp32", x_host=None):
+        hist = np.zeros(niter + 1)
+        res = CResult()
+        fh = None if f_host is None else np.ascontiguousarray(f_host, dtype=np.float64)
+        st = self.lib.nbk_cg_solve_host(self._ctx, _ptr(fh), niter, PREC[precision],
+                                        _ptr(x_host), _ptr(hist), ctypes.byref(res))
+        _check(st, self._ctx, ok=(NBK_OK, NBK_EDEFECT))
+        return hist, {k: getattr(res, k) for k, _ in CResult._fields_}
+
+    def solution(self) -> np.ndarray:
+        x = np.zeros(self.shape)
+        _check(self.lib.nbk_get_solution(self._ctx, _ptr(x)), self._ctx)
+        return x
+
+    def solution_ptr(self, precision: str) -> int:
+        p = ctypes.c_void_p(None)
+        _check(self.lib.nbk_solution_ptr(self._ctx, PREC[precision], ctypes.byref(p)), self._ctx)
+        return int(p.value)
+
+    def solve_launches(self, niter: int, precision: str) -> int:
+        n = ctypes.c_int64(0)
+        _check(self.lib.nbk_solve_launches(self._ctx, niter, PREC[precision], ctypes.byref(n)),
+               self._ctx)
+        return int(n.value)
+
+
+def cg_setup(mesh: MeshSpec, precision: str = "fp32", device: int = 0, stream=None) -> Context:
+    return Context(mesh, precision, device, stream)
+
+
+def version() -> str:
+    return load().nbk_version().decode()

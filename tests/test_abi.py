@@ -1,0 +1,60 @@
+"""CPU checks of the C-ABI library: it loads and exports every symbol that
+include/nbk.h declares (no compute calls: no GPU here), and the build flags
+that the canonical evaluation order depends on are present in the binary."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "nbk.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(nbk_[a-z0-9_]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2405_11065_b200 import build
+    build.build()
+    return ctypes.CDLL(build.LIB)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    from paper_2405_11065_b200 import nbk
+    assert sorted(nbk.SYMBOLS) == syms
+
+
+def test_binding_loads_and_reports_version(lib):
+    from paper_2405_11065_b200 import nbk
+    L = nbk.load()
+    assert L.nbk_version().decode().startswith("nbk")
+
+
+def test_kernels_are_sm100a_and_use_no_contraction(lib):
+    from paper_2405_11065_b200 import build
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", build.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
+                           "_ZN3nbk4k_axIdLi8ELb1EEEvNS_6AxArgsIT_EE", build.LIB],
+                          capture_output=True, text=True).stdout
+    assert "DFMA" in sass
+
+
+def test_workspace_size_query_without_gpu_is_rejected_cleanly(lib):
+    """Without a device the library must not fall back to CPU compute."""
+    from paper_2405_11065_b200 import nbk
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(nbk.NbkError):
+        nbk.Context(nbk.MeshSpec(2, 2, 2, 4), "fp64")
