@@ -4,6 +4,7 @@
 // scalars, one D2H copy of the history per solve.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -39,19 +40,44 @@ static int vec_grid(int64_t n)
 
 
 // ------------------------------------------------------------ dispatchers
+// Launch with the programmatic-stream-serialization attribute (PDL) when pdl:
+// the kernel may start while its predecessor drains; it calls griddepcontrol.wait
+// before touching the predecessor's results.
+static bool g_pdl_enabled = [] {
+    const char* e = getenv("NBK_PDL");  // opt-in: measured no gain on C2
+    return e && e[0] == '1';
+}();
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                            cudaStream_t s, bool pdl, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    const bool on = pdl && g_pdl_enabled;
+    cfg.attrs = on ? attr : nullptr;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 // attr_only: set the dynamic shared-memory limit (done once at set-up, never
 // under stream capture).
 template <typename T, int N, bool FUSED>
-static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false)
+static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
+                               bool pdl = false)
 {
-    constexpr int EPB = ax_epb(N);
-    const size_t smem = (size_t)EPB * 3 * N * N * N * sizeof(T);
+    constexpr int EPB = ax_epb<T>(N);
+    const size_t smem = (size_t)ax_smem_bytes<T>(N);
     if (attr_only)
         return cudaFuncSetAttribute(k_ax<T, N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem);
     const unsigned grid = (unsigned)((a.mesh.E + EPB - 1) / EPB);
-    k_ax<T, N, FUSED><<<grid, ax_threads(N), smem, s>>>(a);
-    return cudaGetLastError();
+    return launch_k(k_ax<T, N, FUSED>, grid, ax_threads<T>(N), smem, s, pdl, a);
 }
 
 #define NBK_SWITCH_N(N, CALL)                 \
@@ -75,28 +101,28 @@ static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_onl
     }
 
 template <typename T, bool FUSED>
-static cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false)
+static cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
+                             bool pdl = false)
 {
-#define AXN(n) launch_ax_n<T, n, FUSED>(a, s, attr_only)
+#define AXN(n) launch_ax_n<T, n, FUSED>(a, s, attr_only, pdl)
     NBK_SWITCH_N(a.mesh.N, AXN)
 #undef AXN
 }
 
 template <typename T, int MODE>
-static cudaError_t launch_vec(const VecArgs<T>& a, cudaStream_t s)
+static cudaError_t launch_vec(const VecArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
     const int g = vec_grid(a.n);
-#define VECN(n) (k_vec<T, n, MODE><<<g, 256, 0, s>>>(a), cudaGetLastError())
+#define VECN(n) launch_k(k_vec<T, n, MODE>, g, 256, 0, s, pdl, a)
     NBK_SWITCH_N(a.mesh.N, VECN)
 #undef VECN
 }
 
 template <typename T, bool FUSED>
-static cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s)
+static cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
-    const int g = vec_grid(a.nseg);
-    k_dssum<T, FUSED><<<g, 256, 0, s>>>(a);
-    return cudaGetLastError();
+    const int g = vec_grid((a.n2 + a.n4 + a.n8 + a.nother + 1) / 2);
+    return launch_k(k_dssum<T, FUSED>, g, 256, 0, s, pdl, a);
 }
 
 // ------------------------------------------------------------ helpers
@@ -112,7 +138,25 @@ static AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
     return a;
 }
 
-static int ax_blocks(const nbk_ctx* c) { return (int)((c->E + ax_epb(c->N) - 1) / ax_epb(c->N)); }
+template <typename T>
+static int ax_blocks_n(int64_t E, int N)
+{
+#define EPBN(n) (int)((E + ax_epb<T>(n) - 1) / ax_epb<T>(n))
+    NBK_SWITCH_N(N, EPBN)
+#undef EPBN
+}
+
+template <typename T>
+static DssumArgs<T> dssum_args(nbk_ctx* c, T* w)
+{
+    DssumArgs<T> d{};
+    d.w = w;
+    d.g2 = c->g2; d.g4 = c->g4; d.g8 = c->g8;
+    d.n2 = c->n2; d.n4 = c->n4; d.n8 = c->n8;
+    d.seg_off = c->seg_off; d.seg_idx = c->seg_idx; d.nother = c->nother;
+    d.st = c->st; d.trace = c->trace; d.mesh = c->view; d.mask = 0;
+    return d;
+}
 
 // Enqueue one CG solve (T1 loop, fixed niter) on the stream; used under capture.
 template <typename T>
@@ -136,18 +180,17 @@ static cudaError_t enqueue_solve(nbk_ctx* c, int niter, nbk_graph* g, bool fp32)
 
     AxArgs<T> aa = ax_args<T>(c, D, G);
     aa.u = nullptr; aa.w = w; aa.p = p; aa.r = r; aa.x = x; aa.mask = 1;
-    DssumArgs<T> da{};
-    da.w = w; da.p = p; da.seg_off = c->seg_off; da.seg_idx = c->seg_idx; da.nseg = c->nseg;
-    da.parts = c->parts; da.nA = ax_blocks(c); da.st = c->st; da.trace = c->trace; da.mask = 0;
-    da.mesh = c->view;
+    DssumArgs<T> da = dssum_args<T>(c, w);
+    da.p = p; da.parts = c->parts; da.nA = ax_blocks_n<T>(c->E, c->N);
     VecArgs<T> vr = vi;
     vr.w = w;
     for (int k = 1; k <= niter; ++k) {
         if (g && c->profiling) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1)], s, cudaEventRecordExternal);
-        if ((e = launch_ax<T, true>(aa, s)) != cudaSuccess) return e;
+        const bool pdl = !(g && c->profiling);  // events between kernels break PDL edges
+        if ((e = launch_ax<T, true>(aa, s, false, pdl)) != cudaSuccess) return e;
         if (g && c->profiling) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = launch_dssum<T, true>(da, s)) != cudaSuccess) return e;
-        if ((e = launch_vec<T, VEC_RUPD>(vr, s)) != cudaSuccess) return e;
+        if ((e = launch_dssum<T, true>(da, s, pdl)) != cudaSuccess) return e;
+        if ((e = launch_vec<T, VEC_RUPD>(vr, s, pdl)) != cudaSuccess) return e;
         launches += 3;
     }
     k_tail_x<T><<<vec_grid(c->n), 256, 0, s>>>(x, p, c->st, c->n);
@@ -161,9 +204,7 @@ static cudaError_t enqueue_solve(nbk_ctx* c, int niter, nbk_graph* g, bool fp32)
     AxArgs<double> a64 = ax_args<double>(c, c->D64, c->G64);
     a64.u = c->x64; a64.w = c->w64; a64.mask = 1;
     if ((e = launch_ax<double, false>(a64, s)) != cudaSuccess) return e;
-    DssumArgs<double> d64{};
-    d64.w = c->w64; d64.seg_off = c->seg_off; d64.seg_idx = c->seg_idx; d64.nseg = c->nseg;
-    d64.st = c->st; d64.mesh = c->view; d64.mask = 0;
+    DssumArgs<double> d64 = dssum_args<double>(c, c->w64);
     if ((e = launch_dssum<double, false>(d64, s)) != cudaSuccess) return e;
     VecArgs<double> vt{};
     vt.r = c->r64; vt.w = c->w64; vt.f = c->f64; vt.n = c->n; vt.parts = vi.parts; vt.st = c->st;
@@ -303,6 +344,7 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     c->parts = (dd*)(b + L.off_parts);
     c->seg_off = (int32_t*)(b + L.off_segoff);
     c->seg_idx = (int32_t*)(b + L.off_segidx);
+    c->grp = (int32_t*)(b + L.off_grp);
     c->G64 = (double*)(b + L.off_G64);
     c->f64 = (double*)(b + L.off_f64);
     const size_t v64 = ((size_t)8 * c->n + 255) & ~(size_t)255;
@@ -374,9 +416,7 @@ nbk_status nbk_ax_apply(nbk_ctx* c, const void* u_dev, void* w_dev, int32_t flag
         a.u = (const double*)u_dev; a.w = (double*)w_dev; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
         NBK_CUDA(c, launch_ax<double, false>(a, s));
         if (flags & NBK_AX_DSSUM) {
-            DssumArgs<double> d{};
-            d.w = (double*)w_dev; d.seg_off = c->seg_off; d.seg_idx = c->seg_idx; d.nseg = c->nseg;
-            d.st = c->st; d.mesh = c->view;
+            DssumArgs<double> d = dssum_args<double>(c, (double*)w_dev);
             NBK_CUDA(c, launch_dssum<double, false>(d, s));
         }
     } else if (prec == NBK_FP32) {
@@ -384,9 +424,7 @@ nbk_status nbk_ax_apply(nbk_ctx* c, const void* u_dev, void* w_dev, int32_t flag
         a.u = (const float*)u_dev; a.w = (float*)w_dev; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
         NBK_CUDA(c, launch_ax<float, false>(a, s));
         if (flags & NBK_AX_DSSUM) {
-            DssumArgs<float> d{};
-            d.w = (float*)w_dev; d.seg_off = c->seg_off; d.seg_idx = c->seg_idx; d.nseg = c->nseg;
-            d.st = c->st; d.mesh = c->view;
+            DssumArgs<float> d = dssum_args<float>(c, (float*)w_dev);
             NBK_CUDA(c, launch_dssum<float, false>(d, s));
         }
     } else {
@@ -401,15 +439,11 @@ nbk_status nbk_dssum(nbk_ctx* c, void* f_dev, int32_t apply_mask, nbk_precision 
     if (!f_dev) return fail(c, NBK_EINVAL, "f is NULL");
     cudaStream_t s = c->stream;
     if (prec == NBK_FP64) {
-        DssumArgs<double> d{};
-        d.w = (double*)f_dev; d.seg_off = c->seg_off; d.seg_idx = c->seg_idx; d.nseg = c->nseg;
-        d.st = c->st; d.mesh = c->view; d.mask = 0;
+        DssumArgs<double> d = dssum_args<double>(c, (double*)f_dev);
         NBK_CUDA(c, launch_dssum<double, false>(d, s));
         if (apply_mask) { k_mask<double><<<vec_grid(c->n), 256, 0, s>>>((double*)f_dev, c->view); NBK_CUDA(c, cudaGetLastError()); }
     } else if (prec == NBK_FP32) {
-        DssumArgs<float> d{};
-        d.w = (float*)f_dev; d.seg_off = c->seg_off; d.seg_idx = c->seg_idx; d.nseg = c->nseg;
-        d.st = c->st; d.mesh = c->view; d.mask = 0;
+        DssumArgs<float> d = dssum_args<float>(c, (float*)f_dev);
         NBK_CUDA(c, launch_dssum<float, false>(d, s));
         if (apply_mask) { k_mask<float><<<vec_grid(c->n), 256, 0, s>>>((float*)f_dev, c->view); NBK_CUDA(c, cudaGetLastError()); }
     } else {

@@ -96,14 +96,26 @@ __device__ __forceinline__ dd block_reduce_dd(dd v)
 }
 
 // Reduce n dd partials in a fixed order with one block (all threads call).
+// Thread t owns partials t, t+T, t+2T, ... (combined in that order); the loads
+// of a batch are issued together so the tail costs ~one L2 round trip.
 __device__ __forceinline__ dd reduce_partials(const dd* parts, int n)
 {
+    constexpr int B = 8;
     dd v{0.0, 0.0};
-    for (int q = threadIdx.x; q < n; q += blockDim.x) {
-        dd p;
-        p.hi = __ldcg(&parts[q].hi);
-        p.lo = __ldcg(&parts[q].lo);
-        v = dd_add(v, p);
+    for (int q0 = threadIdx.x; q0 < n; q0 += B * blockDim.x) {
+        dd p[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int q = q0 + b * blockDim.x;
+            if (q < n) {
+                p[b].hi = __ldcg(&parts[q].hi);
+                p[b].lo = __ldcg(&parts[q].lo);
+            } else {
+                p[b] = dd{0.0, 0.0};
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) v = dd_add(v, p[b]);
     }
     return block_reduce_dd(v);
 }
@@ -111,21 +123,35 @@ __device__ __forceinline__ dd reduce_partials(const dd* parts, int n)
 // "Last block finalises": every block publishes its partial, then the block
 // that increments the counter last reduces all partials (order fixed by the
 // partial index, so the result does not depend on which block is last).
+// Release/acquire through the counter (atom.acq_rel), no SC fence.
 // Returns true in the last block (all threads).
 __device__ __forceinline__ bool publish_and_check_last(dd* parts, int slot, dd v,
                                                        unsigned int* counter, unsigned int total)
 {
     __shared__ unsigned int last_flag;
     if (threadIdx.x == 0) {
-        parts[slot] = v;
-        __threadfence();
-        unsigned int prev = atomicAdd(counter, 1u);
+        __stcg(&parts[slot].hi, v.hi);
+        __stcg(&parts[slot].lo, v.lo);
+        unsigned int prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;"
+                     : "=r"(prev)
+                     : "l"(counter)
+                     : "memory");
         last_flag = (prev == total - 1) ? 1u : 0u;
     }
     __syncthreads();
-    bool last = last_flag != 0;
-    if (last) __threadfence();
-    return last;
+    return last_flag != 0;
+}
+
+// Programmatic dependent launch (PDL): let the next kernel in the stream be
+// scheduled early / wait for the previous kernel's results.
+__device__ __forceinline__ void pdl_launch_dependents()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ mesh
@@ -232,6 +258,49 @@ template <>
 __device__ __forceinline__ float add_t<float>(float a, float b)
 {
     return __fadd_rn(a, b);
+}
+
+// ------------------------------------------------------------ TMA / mbarrier
+// 1-D bulk copies global -> shared through the tensor memory accelerator
+// (cp.async.bulk, SASS UBLKCP) completing on an mbarrier (transaction bytes).
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                            uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 // ------------------------------------------------------------ CG state

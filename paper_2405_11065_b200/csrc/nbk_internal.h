@@ -41,6 +41,9 @@ struct nbk_ctx {
     nbk::dd* parts = nullptr;
     int64_t nparts = 0;
     int32_t *seg_off = nullptr, *seg_idx = nullptr;
+    int32_t *grp = nullptr;                               // group index storage
+    int32_t *g2 = nullptr, *g4 = nullptr, *g8 = nullptr;  // segments grouped by multiplicity
+    int64_t n2 = 0, n4 = 0, n8 = 0, nother = 0;
     unsigned char* scratch = nullptr;  // set-up scratch (aliases the vector region)
     size_t scratch_bytes = 0;
 
@@ -54,7 +57,7 @@ struct nbk_ctx {
 namespace nbk {
 
 struct Layout {
-    size_t off_state, off_D64, off_D32, off_hist, off_trace, off_parts, off_segoff, off_segidx,
+    size_t off_state, off_D64, off_D32, off_hist, off_trace, off_parts, off_segoff, off_segidx, off_grp,
         off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
     int64_t E, n, n_global, nseg, ncopies, nparts, e_offset;
     size_t scratch_need;

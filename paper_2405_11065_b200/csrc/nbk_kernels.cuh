@@ -22,16 +22,54 @@
 
 namespace nbk {
 
-// Elements per CTA of k_ax: about 256 threads (N^2 per element).
-__host__ __device__ constexpr int ax_epb(int N) { return (256 / (N * N)) > 0 ? 256 / (N * N) : 1; }
+// ------------------------------------------------------------ K_A config
+// Per CTA: EPB elements, one thread per (i, j) of each element (k-loop in
+// registers).  STAGE_G: the CTA's G block (EPB*6*N^3 values) and its p/u block
+// (EPB*N^3) are staged in shared memory by TMA 1-D bulk copies (even N: 16-byte
+// granularity) or a cooperative copy (odd N); wr/ws are written into the G
+// slots of g1/g2 once consumed, so smem = 7*EPB*N^3 values.  Without STAGE_G
+// (only N=16 FP64, > 227 KB) G is read from global memory per k-slice.
+template <typename T>
+__host__ __device__ constexpr int ax_epb(int N)
+{
+    if (N == 8) return sizeof(T) == 4 ? 3 : 2;
+    if (N == 10) return sizeof(T) == 4 ? 2 : 1;
+    if (N == 12) return 1;
+    int by_thr = 256 / (N * N) > 0 ? 256 / (N * N) : 1;
+    int by_smem = (int)(57344 / (7 * N * N * N * (int)sizeof(T)));
+    if (by_smem < 1) by_smem = 1;
+    return by_thr < by_smem ? by_thr : by_smem;
+}
+template <typename T>
+__host__ __device__ constexpr bool ax_stage_g(int N)
+{
+    return 7 * N * N * N * (int)sizeof(T) * ax_epb<T>(N) <= 200 * 1024;
+}
 // CTA size: N^2 * EPB rounded up to whole warps (the extra lanes idle).
-__host__ __device__ constexpr int ax_threads(int N) { return (N * N * ax_epb(N) + 31) / 32 * 32; }
+template <typename T>
+__host__ __device__ constexpr int ax_threads(int N)
+{
+    return (N * N * ax_epb<T>(N) + 31) / 32 * 32;
+}
+template <typename T>
+__host__ __device__ constexpr int ax_smem_bytes(int N)
+{
+    return (ax_stage_g<T>(N) ? 7 : 3) * ax_epb<T>(N) * N * N * N * (int)sizeof(T);
+}
+template <typename T>
+__host__ __device__ constexpr int ax_min_blocks(int N)
+{
+    int by_smem = (232448 - 1024) / (ax_smem_bytes<T>(N) + 1024 + 2 * N * N * (int)sizeof(T) + 64);
+    int by_thr = 2048 / ax_threads<T>(N);
+    int m = by_smem < by_thr ? by_smem : by_thr;
+    return m < 1 ? 1 : m;
+}
 
 template <typename T>
 struct AxArgs {
     const T* D;        // N*N, D[a*N+b] = l_b'(xi_a)
     const T* G;        // E*6*N^3
-    const T* u;        // input field (plain mode) or p_{k-1} (fused mode)
+    const T* u;        // input field (plain mode)
     T* w;              // output
     T* p;              // fused: p (in/out)
     const T* r;        // fused: r
@@ -43,33 +81,60 @@ struct AxArgs {
 };
 
 // ---------------------------------------------------------------- K_A
-// Thread layout: (i, j) of one of EPB elements; the k-loop runs in registers.
-// smem: D, D^T and per element u_e, wr, ws (3 N^3 values).
 template <typename T, int N, bool FUSED>
-__global__ void __launch_bounds__(ax_threads(N))
+__global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     k_ax(AxArgs<T> a)
 {
-    constexpr int N2 = N * N, N3 = N * N * N, EPB = ax_epb(N);
+    constexpr int N2 = N * N, N3 = N * N * N, EPB = ax_epb<T>(N);
+    constexpr bool STAGE = ax_stage_g<T>(N);
+    constexpr bool TMA = STAGE && (N % 2 == 0);
     __shared__ T sD[N2], sDt[N2];
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* su = reinterpret_cast<T*>(smem_raw);
+    __shared__ __align__(8) uint64_t bar;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* sG = reinterpret_cast<T*>(smem_raw);                  // STAGE: EPB*6*N3
+    T* sU = STAGE ? sG + EPB * 6 * N3 : sG;                  // EPB*N3
+    T* sW = sU + EPB * N3;                                   // !STAGE: wr, ws (2*EPB*N3)
 
     const int tid = threadIdx.x;
     const int el = tid / N2, ij = tid - el * N2;
     const int i = ij % N, j = ij / N;
-    const int64_t e = (int64_t)blockIdx.x * EPB + el;
-    const bool valid = el < EPB && e < a.mesh.E;
-    T* ue = su + el * 3 * N3;
-    T* wre = ue + N3;
-    T* wse = wre + N3;
+    const int64_t e0 = (int64_t)blockIdx.x * EPB;
+    const int64_t e = e0 + el;
+    const int nel = (int)((a.mesh.E - e0) < EPB ? (a.mesh.E - e0) : EPB);
+    const bool valid = el < nel;
+    const T* src_u = FUSED ? a.p : a.u;
 
+    // ---- stage G and u/p of the CTA's elements in shared memory.  G does not
+    // depend on the previous kernel: its bulk copy is issued before the PDL
+    // wait and overlaps the previous kernel's tail.
+    if constexpr (TMA) {
+        if (tid == 0) {
+            mbar_init(&bar, 1);
+            const uint32_t gbytes = (uint32_t)(nel * 6 * N3 * sizeof(T));
+            const uint32_t ubytes = (uint32_t)(nel * N3 * sizeof(T));
+            mbar_arrive_expect_tx(&bar, gbytes + ubytes);
+            tma_load_1d(sG, a.G + e0 * 6 * N3, gbytes, &bar);
+            pdl_wait();
+            tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar);
+        }
+        pdl_wait();
+    } else if constexpr (STAGE) {
+        pdl_wait();
+        for (int q = tid; q < nel * 6 * N3; q += blockDim.x) sG[q] = a.G[e0 * 6 * N3 + q];
+        for (int q = tid; q < nel * N3; q += blockDim.x) sU[q] = src_u[e0 * N3 + q];
+    } else {
+        pdl_wait();
+        for (int q = tid; q < nel * N3; q += blockDim.x) sU[q] = src_u[e0 * N3 + q];
+    }
     for (int q = tid; q < N2; q += blockDim.x) {
         T d = a.D[q];
         sD[q] = d;
         sDt[(q % N) * N + q / N] = d;
     }
 
+    const int64_t base = e * N3 + ij;
     T betaT = 0, alphaT = 0;
+    T rreg[FUSED ? N : 1], xreg[FUSED ? N : 1];
     if constexpr (FUSED) {
         if constexpr (sizeof(T) == 8) {
             betaT = (T)a.st->beta;
@@ -78,38 +143,45 @@ __global__ void __launch_bounds__(ax_threads(N))
             betaT = (T)a.st->beta32;
             alphaT = (T)a.st->alpha32;
         }
+        if (valid) {  // issued before the TMA wait: overlaps with the bulk copies
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                rreg[k] = a.r[base + k * N2];
+                xreg[k] = a.x[base + k * N2];
+            }
+        }
     }
+    __syncthreads();  // barrier init, sD, cooperative copies visible
+    if constexpr (TMA) mbar_wait(&bar, 0);
 
-    // ---- load p (fused: p = fma(beta, p, r), x = fma(alpha_prev, p_prev, x))
+    T* ue = sU + el * N3;
+    T* wre = STAGE ? sG + el * 6 * N3 : sW + el * N3;            // aliases g1 (STAGE)
+    T* wse = STAGE ? sG + el * 6 * N3 + N3 : sW + (EPB + el) * N3;  // aliases g2
+
+    // ---- p = fma(beta, p, r), x = fma(alpha_prev, p_prev, x)  (C8, fused)
     T ureg[N];
-    const int64_t base = e * N3 + ij;
     if (valid) {
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            const int64_t L = base + k * N2;
-            T v;
+            T v = ue[k * N2 + ij];
             if constexpr (FUSED) {
-                T po = a.p[L];
-                T rr = a.r[L];
-                T xx = a.x[L];
-                v = fma_t<T>(betaT, po, rr);         // C8: p = fma(betaT, p, r)
-                a.x[L] = fma_t<T>(alphaT, po, xx);   // C8: x = fma(alphaT, p, x)
-                a.p[L] = v;
-            } else {
-                v = a.u[L];
+                const T po = v;
+                v = fma_t<T>(betaT, po, rreg[k]);
+                a.x[base + k * N2] = fma_t<T>(alphaT, po, xreg[k]);
+                a.p[base + k * N2] = v;
+                ue[k * N2 + ij] = v;
             }
             ureg[k] = v;
-            ue[k * N2 + ij] = v;
         }
     }
-    __syncthreads();
+    if constexpr (FUSED) __syncthreads();
 
     // ---- gradient (C1), metric (C2), t-part of the transpose (C3: b chain)
     T b[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) b[k] = 0;
     if (valid) {
-        const T* Ge = a.G + e * 6 * N3 + ij;
+        const T* Ge = STAGE ? sG + el * 6 * N3 + ij : a.G + e * 6 * N3 + ij;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             T ur = 0, us = 0, ut = 0;
@@ -130,6 +202,7 @@ __global__ void __launch_bounds__(ax_threads(N))
             T wt = mul_t<T>(g3, ur);
             wt = fma_t<T>(g5, us, wt);
             wt = fma_t<T>(g6, ut, wt);
+            // own (i,j,k) slot of g1/g2 is dead after the reads above
             wre[k * N2 + ij] = wr;
             wse[k * N2 + ij] = ws;
 #pragma unroll
@@ -159,6 +232,7 @@ __global__ void __launch_bounds__(ax_threads(N))
             }
         }
     }
+    pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
         if (threadIdx.x == 0) a.parts[blockIdx.x] = v;
@@ -166,13 +240,21 @@ __global__ void __launch_bounds__(ax_threads(N))
 }
 
 // ---------------------------------------------------------------- K_B
+// The dssum plan groups the segments (unique shared nodes) by multiplicity
+// m in {2, 4, 8}: group m is a dense int32 array of m ascending local indices
+// per node, read with one vector load.  Segments of any other length (none
+// on a single-rank box) use the generic offset list.
 template <typename T>
 struct DssumArgs {
     T* w;
     const T* p;               // fused: p (shared-node pap term)
-    const int32_t* seg_off;   // nseg+1 offsets into seg_idx
-    const int32_t* seg_idx;   // local indices, ascending within a segment
-    int64_t nseg;
+    const int32_t* g2;        // n2 x 2
+    const int32_t* g4;        // n4 x 4
+    const int32_t* g8;        // n8 x 8
+    int64_t n2, n4, n8;
+    const int32_t* seg_off;   // generic segments (nother)
+    const int32_t* seg_idx;
+    int64_t nother;
     dd* parts;                // fused: partials [0, nA) from K_A, [nA, nA+gridDim) here
     int nA;
     CgState* st;
@@ -181,26 +263,103 @@ struct DssumArgs {
     MeshView mesh;
 };
 
+template <typename T>
+__device__ __forceinline__ bool masked_local(const MeshView& m, int32_t L)
+{
+    const int N = m.N, N3 = N * N * N;
+    const uint32_t e = (uint32_t)(L / N3);
+    const int rem = L - (int)e * N3;
+    ElemCoord ec = elem_coord(m, e);
+    return is_masked(m, ec, rem % N, (rem / N) % N, rem / (N * N));
+}
+
+// Sum the M copies (C4: ascending local index), write back, pap term.
+template <typename T, int M, bool FUSED>
+__device__ __forceinline__ void dssum_node(const DssumArgs<T>& a, const int32_t (&ix)[M], acc_t& acc)
+{
+    T v[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) v[q] = a.w[ix[q]];
+    T p0 = 0;
+    if constexpr (FUSED) p0 = a.p[ix[0]];
+    T sum = v[0];
+#pragma unroll
+    for (int q = 1; q < M; ++q) sum = add_t<T>(sum, v[q]);
+    if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[0])) sum = 0;
+#pragma unroll
+    for (int q = 0; q < M; ++q) a.w[ix[q]] = sum;
+    if constexpr (FUSED) acc.add(dot_term(sum, p0, 1.0));  // one term per node (m c = 1)
+}
+
+// Load the (ascending) local indices of segment s; returns its length m.
+template <typename T>
+__device__ __forceinline__ int seg_load(const DssumArgs<T>& a, int64_t s, int32_t (&ix)[8])
+{
+    const int64_t n24 = a.n2 + a.n4;
+    if (s < a.n2) {
+        const int2 q = reinterpret_cast<const int2*>(a.g2)[s];
+        ix[0] = q.x; ix[1] = q.y;
+        return 2;
+    } else if (s < n24) {
+        const int4 q = reinterpret_cast<const int4*>(a.g4)[s - a.n2];
+        ix[0] = q.x; ix[1] = q.y; ix[2] = q.z; ix[3] = q.w;
+        return 4;
+    }
+    const int4* g = reinterpret_cast<const int4*>(a.g8) + 2 * (s - n24);
+    const int4 q0 = g[0], q1 = g[1];
+    ix[0] = q0.x; ix[1] = q0.y; ix[2] = q0.z; ix[3] = q0.w;
+    ix[4] = q1.x; ix[5] = q1.y; ix[6] = q1.z; ix[7] = q1.w;
+    return 8;
+}
+
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nseg;
-         s += (int64_t)gridDim.x * blockDim.x) {
+    pdl_wait();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tot = a.n2 + a.n4 + a.n8;
+    // two segments per thread per step, all loads of both issued before use
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < tot; s += 2 * stride) {
+        const int64_t s2 = s + stride;
+        int32_t ix[2][8];
+        int m[2];
+        m[0] = seg_load(a, s, ix[0]);
+        m[1] = s2 < tot ? seg_load(a, s2, ix[1]) : 0;
+        T v[2][8];
+        T p0[2] = {0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < m[h]) v[h][q] = a.w[ix[h][q]];
+            if constexpr (FUSED)
+                if (m[h]) p0[h] = a.p[ix[h][0]];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!m[h]) continue;
+            T sum = v[h][0];                          // C4: ascending local index
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                if (q < m[h]) sum = add_t<T>(sum, v[h][q]);
+            if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[h][0])) sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < m[h]) a.w[ix[h][q]] = sum;
+            if constexpr (FUSED) acc.add(dot_term(sum, p0[h], 1.0));  // one term per node
+        }
+    }
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nother; s += stride) {
         const int32_t o0 = a.seg_off[s], o1 = a.seg_off[s + 1];
         const int32_t L0 = a.seg_idx[o0];
-        T sum = a.w[L0];                              // C4: s = w[L1]
+        T sum = a.w[L0];
         for (int32_t q = o0 + 1; q < o1; ++q) sum = add_t<T>(sum, a.w[a.seg_idx[q]]);
-        if (!FUSED && a.mask) {
-            const int N = a.mesh.N;
-            const uint32_t e = (uint32_t)(L0 / (N * N * N));
-            const int rem = L0 - (int)e * N * N * N;
-            ElemCoord ec = elem_coord(a.mesh, e);
-            if (is_masked(a.mesh, ec, rem % N, (rem / N) % N, rem / (N * N))) sum = 0;
-        }
+        if (!FUSED && a.mask && masked_local<T>(a.mesh, L0)) sum = 0;
         for (int32_t q = o0; q < o1; ++q) a.w[a.seg_idx[q]] = sum;
-        if constexpr (FUSED) acc.add(dot_term(sum, a.p[L0], 1.0));  // one term per node
+        if constexpr (FUSED) acc.add(dot_term(sum, a.p[L0], 1.0));
     }
+    pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
         const unsigned int total = gridDim.x;
@@ -250,45 +409,116 @@ struct VecArgs {
     MeshView mesh;
 };
 
+// V consecutive values, 16-byte vector memory operations when V*sizeof(T) >= 16.
+template <typename T, int V>
+struct VecT {
+    T v[V];
+    __device__ __forceinline__ void load(const T* p)
+    {
+        if constexpr (V * sizeof(T) % 16 == 0) {
+#pragma unroll
+            for (int q = 0; q < V * (int)sizeof(T) / 16; ++q)
+                reinterpret_cast<float4*>(v)[q] = reinterpret_cast<const float4*>(p)[q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q) v[q] = p[q];
+        }
+    }
+    __device__ __forceinline__ void store(T* p) const
+    {
+        if constexpr (V * sizeof(T) % 16 == 0) {
+#pragma unroll
+            for (int q = 0; q < V * (int)sizeof(T) / 16; ++q)
+                reinterpret_cast<float4*>(p)[q] = reinterpret_cast<const float4*>(v)[q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q) p[q] = v[q];
+        }
+    }
+};
+
+// Vector kernel over all local points: chunks of V = 4 consecutive points
+// (N^3 % 4 == 0) in one element, 16-byte loads/stores; structural c = 1/m.
 template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 {
     constexpr int N2 = N * N, N3 = N * N * N;
+    constexpr int V = (N3 % 4 == 0) ? 4 : 1;
     acc_t acc;
     T am = 0;
+    pdl_wait();
     if constexpr (MODE == VEC_RUPD) {
         if constexpr (sizeof(T) == 8) am = (T)a.st->alpham; else am = (T)a.st->alpham32;
     }
-    uint32_t e_cached = 0xffffffffu;
-    ElemCoord ec{0, 0, 0};
-    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < a.n;
-         L += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nch = a.n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nch; q += stride) {
+        const int64_t L = q * V;
         const uint32_t e = (uint32_t)(L / N3);
         const int rem = (int)(L - (int64_t)e * N3);
-        if (e != e_cached) {
-            ec = elem_coord(a.mesh, e);
-            e_cached = e;
-        }
-        const double c = inv_mult(multiplicity(a.mesh, ec, rem % N, (rem / N) % N, rem / N2));
-        T v;
-        if constexpr (MODE == VEC_INIT) {
-            v = (T)a.f[L];                 // C11: f32 = RN32(f64)
-            a.r[L] = v;
-            a.x[L] = 0;
-            a.p[L] = 0;
-            acc.add(dot_term(v, v, c));
-        } else if constexpr (MODE == VEC_RUPD) {
-            v = fma_t<T>(am, a.w[L], a.r[L]);  // C8: r = fma(-alphaT, w, r)
-            a.r[L] = v;
-            acc.add(dot_term(v, v, c));
-        } else if constexpr (MODE == VEC_TRUE) {
-            v = fma_t<T>((T)-1, a.w[L], (T)a.f[L]);  // C12: r_true = f - w (one rounding)
-            a.r[L] = v;
-            acc.add(dot_term(v, v, c));
+        const ElemCoord ec = elem_coord(a.mesh, e);
+        double c[V];
+        if constexpr (N % V == 0) {
+            // the chunk lies in one (j, k) row: c = c_yz * c_x(i)
+            const int i0 = rem % N, j = (rem / N) % N, k = rem / N2;
+            const int n1 = N - 1;
+            const int myz = (((j == 0 && ec.ay > 0) || (j == n1 && ec.ay < a.mesh.ey - 1)) ? 2 : 1) *
+                            (((k == 0 && ec.azg > 0) || (k == n1 && ec.azg < a.mesh.ezg - 1)) ? 2 : 1);
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                const int i = i0 + t;
+                const int mx = ((i == 0 && ec.ax > 0) || (i == n1 && ec.ax < a.mesh.ex - 1)) ? 2 : 1;
+                c[t] = inv_mult(mx * myz);
+            }
         } else {
-            acc.add(dot_term(a.a[L], a.b[L], c));
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                const int pt = rem + t;
+                c[t] = inv_mult(multiplicity(a.mesh, ec, pt % N, (pt / N) % N, pt / N2));
+            }
+        }
+        if constexpr (MODE == VEC_INIT) {
+            VecT<double, V> f;
+            f.load(a.f + L);
+            VecT<T, V> r, z;
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                r.v[t] = (T)f.v[t];  // C11: f32 = RN32(f64)
+                z.v[t] = 0;
+            }
+            r.store(a.r + L);
+            z.store(a.x + L);
+            z.store(a.p + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+        } else if constexpr (MODE == VEC_RUPD) {
+            VecT<T, V> w, r;
+            w.load(a.w + L);
+            r.load(a.r + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, w.v[t], r.v[t]);  // C8
+            r.store(a.r + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+        } else if constexpr (MODE == VEC_TRUE) {
+            VecT<T, V> w, r;
+            VecT<double, V> f;
+            w.load(a.w + L);
+            f.load(a.f + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, w.v[t], (T)f.v[t]);  // C12
+            r.store(a.r + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+        } else {
+            VecT<T, V> x, y;
+            x.load(a.a + L);
+            y.load(a.b + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(x.v[t], y.v[t], c[t]));
         }
     }
+    pdl_launch_dependents();
     dd v = block_reduce_dd(acc.get());
     if (publish_and_check_last(a.parts, blockIdx.x, v, &a.st->cnt[1], gridDim.x)) {
         dd tot = reduce_partials(a.parts, (int)gridDim.x);

@@ -74,13 +74,14 @@ MeshView make_view(const nbk_mesh* m, const nbk_dist* d)
     return v;
 }
 
-static size_t plan_scratch_bytes(int64_t n)
+static size_t plan_scratch_bytes(int64_t n, int64_t nseg)
 {
     size_t sort_tmp = 0, scan_tmp = 0;
     cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
     cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int)n);
     cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
-    return 6 * align256((size_t)n * 4) + align256(sort_tmp > scan_tmp ? sort_tmp : scan_tmp) + 256;
+    const size_t a = 6 * align256((size_t)n * 4), b = 10 * align256((size_t)nseg * 4);
+    return (a > b ? a : b) + align256(sort_tmp > scan_tmp ? sort_tmp : scan_tmp) + 256;
 }
 
 Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
@@ -95,8 +96,7 @@ Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
     box_counts(m->ex, m->ey, m->ez, N, L.n_global, nsh_dummy);
     box_counts(m->ex, m->ey, v.ez_local, N, ngl, L.nseg);
     L.ncopies = L.n - (ngl - L.nseg);
-    const int epb = (256 / (N * N)) > 0 ? (int)(256 / (N * N)) : 1;
-    L.nparts = (L.E + epb - 1) / epb + 2 * NBK_VEC_GRID_MAX + 64;
+    L.nparts = L.E + 2 * NBK_VEC_GRID_MAX + 64;  // >= K_A CTAs for every EPB
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
     L.off_state = take(sizeof(CgState));
@@ -107,9 +107,10 @@ Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
     L.off_parts = take(sizeof(dd) * (size_t)L.nparts);
     L.off_segoff = take(4 * (size_t)(L.nseg + 1));
     L.off_segidx = take(4 * (size_t)(L.ncopies > 0 ? L.ncopies : 1));
+    L.off_grp = take(4 * (size_t)L.ncopies + 64);
     L.off_G64 = take(8 * 6 * (size_t)L.n);
     L.off_f64 = take(8 * (size_t)L.n);
-    L.scratch_need = plan_scratch_bytes(L.n);
+    L.scratch_need = plan_scratch_bytes(L.n, L.nseg);
     size_t vec64 = 4 * align256(8 * (size_t)L.n);
     L.off_vec64 = take(vec64 > L.scratch_need ? vec64 : L.scratch_need);
     if (prec == NBK_FP32) {
@@ -324,6 +325,49 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint32_t* vals, cons
     }
 }
 
+// Group the segments by length m in {2, 4, 8} (dense m-wide index rows).
+// Segments are visited in the order of their first (smallest) local index so
+// that consecutive threads of k_dssum touch neighbouring addresses.
+__global__ void __launch_bounds__(256) k_seg_first(const int32_t* off, const int32_t* idx,
+                                                   int64_t nseg, uint32_t* first, uint32_t* id)
+{
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        first[s] = (uint32_t)idx[off[s]];
+        id[s] = (uint32_t)s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_seg_flags(const int32_t* off, const uint32_t* order,
+                                                   int64_t nseg, uint32_t* f2, uint32_t* f4,
+                                                   uint32_t* f8)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nseg;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = order[t];
+        const int m = off[s + 1] - off[s];
+        f2[t] = m == 2;
+        f4[t] = m == 4;
+        f8[t] = m == 8;
+    }
+}
+__global__ void __launch_bounds__(256) k_group_scatter(const int32_t* off, const int32_t* idx,
+                                                       const uint32_t* order,
+                                                       int64_t nseg, const uint32_t* f2,
+                                                       const uint32_t* f4, const uint32_t* f8,
+                                                       const uint32_t* p2, const uint32_t* p4,
+                                                       const uint32_t* p8, int32_t* g2, int32_t* g4,
+                                                       int32_t* g8)
+{
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nseg;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t o = off[order[t]];
+        if (f2[t]) for (int q = 0; q < 2; ++q) g2[2 * (int64_t)p2[t] + q] = idx[o + q];
+        if (f4[t]) for (int q = 0; q < 4; ++q) g4[4 * (int64_t)p4[t] + q] = idx[o + q];
+        if (f8[t]) for (int q = 0; q < 8; ++q) g8[8 * (int64_t)p8[t] + q] = idx[o + q];
+    }
+}
+
 static int grid_for(int64_t n, int cap = 148 * 16)
 {
     int64_t g = (n + 255) / 256;
@@ -380,6 +424,66 @@ cudaError_t build_plan(nbk_ctx* ctx)
     if (err != cudaSuccess) return err;
     if ((int64_t)(last_head + h_last) != ctx->nseg || (int64_t)(last_run + r_last) != ctx->ncopies)
         return cudaErrorInvalidValue;
+
+    // ---- group the segments by multiplicity (scratch is free again)
+    const int64_t ns = ctx->nseg;
+    ctx->n2 = ctx->n4 = ctx->n8 = ctx->nother = 0;
+    ctx->g2 = ctx->g4 = ctx->g8 = ctx->grp;
+    if (ns == 0) return cudaGetLastError();
+    o = 0;
+    uint32_t* f2 = (uint32_t*)take(4 * ns);
+    uint32_t* f4 = (uint32_t*)take(4 * ns);
+    uint32_t* f8 = (uint32_t*)take(4 * ns);
+    uint32_t* q2 = (uint32_t*)take(4 * ns);
+    uint32_t* q4 = (uint32_t*)take(4 * ns);
+    uint32_t* q8 = (uint32_t*)take(4 * ns);
+    uint32_t* fk0 = (uint32_t*)take(4 * ns);
+    uint32_t* fk1 = (uint32_t*)take(4 * ns);
+    uint32_t* od0 = (uint32_t*)take(4 * ns);
+    uint32_t* od1 = (uint32_t*)take(4 * ns);
+    tmp = base + o;
+    tmp_bytes = ctx->scratch_bytes - o;
+    // order segments by their first local index
+    k_seg_first<<<grid_for(ns), 256, 0, s>>>(ctx->seg_off, ctx->seg_idx, ns, fk0, od0);
+    {
+        cub::DoubleBuffer<uint32_t> fb(fk0, fk1), ob(od0, od1);
+        int eb = 1;
+        while (eb < 32 && ((uint64_t)1 << eb) < (uint64_t)n) ++eb;
+        err = cub::DeviceRadixSort::SortPairs(nullptr, need, fb, ob, (int)ns, 0, eb, s);
+        if (err != cudaSuccess) return err;
+        if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+        err = cub::DeviceRadixSort::SortPairs(tmp, need, fb, ob, (int)ns, 0, eb, s);
+        if (err != cudaSuccess) return err;
+        od0 = ob.Current();
+    }
+    const uint32_t* order = od0;
+    k_seg_flags<<<grid_for(ns), 256, 0, s>>>(ctx->seg_off, order, ns, f2, f4, f8);
+    err = cub::DeviceScan::ExclusiveSum(nullptr, need, f2, q2, (int)ns, s);
+    if (err != cudaSuccess) return err;
+    if (need > tmp_bytes) return cudaErrorMemoryAllocation;
+    uint32_t* fl[3] = {f2, f4, f8};
+    uint32_t* ql[3] = {q2, q4, q8};
+    uint32_t cnt[3], lastf[3];
+    for (int g = 0; g < 3; ++g) {
+        err = cub::DeviceScan::ExclusiveSum(tmp, need, fl[g], ql[g], (int)ns, s);
+        if (err != cudaSuccess) return err;
+        cudaMemcpyAsync(&cnt[g], ql[g] + ns - 1, 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&lastf[g], fl[g] + ns - 1, 4, cudaMemcpyDeviceToHost, s);
+    }
+    err = cudaStreamSynchronize(s);
+    if (err != cudaSuccess) return err;
+    ctx->n2 = cnt[0] + lastf[0];
+    ctx->n4 = cnt[1] + lastf[1];
+    ctx->n8 = cnt[2] + lastf[2];
+    ctx->nother = ns - ctx->n2 - ctx->n4 - ctx->n8;
+    if (ctx->nother != 0) return cudaErrorInvalidValue;  // single-rank box: m in {2, 4, 8}
+    ctx->g2 = ctx->grp;
+    ctx->g4 = ctx->g2 + ((2 * ctx->n2 + 3) & ~(int64_t)3);   // 16-byte aligned rows
+    ctx->g8 = ctx->g4 + 4 * ctx->n4;
+    k_group_scatter<<<grid_for(ns), 256, 0, s>>>(ctx->seg_off, ctx->seg_idx, order, ns, f2, f4, f8, q2,
+                                                 q4, q8, ctx->g2, ctx->g4, ctx->g8);
+    err = cudaStreamSynchronize(s);
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 

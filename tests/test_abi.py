@@ -44,10 +44,21 @@ def test_kernels_are_sm100a_and_use_no_contraction(lib):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", build.LIB],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                           "_ZN3nbk4k_axIdLi8ELb1EEEvNS_6AxArgsIT_EE", build.LIB],
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", build.LIB],
                           capture_output=True, text=True).stdout
-    assert "DFMA" in sass
+    funcs = {}
+    cur = None
+    for line in sass.splitlines():
+        if "Function : " in line:
+            cur = line.split("Function : ")[1].strip()
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    fused64 = "\n".join(funcs["_ZN3nbk4k_axIdLi8ELb1EEEvNS_6AxArgsIT_EE"])
+    fused32 = "\n".join(funcs["_ZN3nbk4k_axIfLi8ELb1EEEvNS_6AxArgsIT_EE"])
+    assert "DFMA" in fused64 and "FFMA" in fused32
+    # TMA 1-D bulk copies (cp.async.bulk -> UBLKCP) stage G and p in shared memory
+    assert "UBLKCP" in fused64 and "UBLKCP" in fused32
 
 
 def test_workspace_size_query_without_gpu_is_rejected_cleanly(lib):
