@@ -22,6 +22,61 @@
 
 namespace nbk {
 
+// Load N consecutive values of shared memory into registers with the widest
+// vector loads the row alignment allows (rows are N*sizeof(T) bytes, and every
+// row start used below is a multiple of that).
+template <typename T, int N>
+__device__ __forceinline__ void lds_row(T (&dst)[N], const T* src)
+{
+    constexpr int RB = N * (int)sizeof(T);
+    if constexpr (RB % 16 == 0) {
+#pragma unroll
+        for (int q = 0; q < RB / 16; ++q) {
+            if constexpr (sizeof(T) == 4) {
+                const float4 v = reinterpret_cast<const float4*>(src)[q];
+                dst[4 * q] = v.x;
+                dst[4 * q + 1] = v.y;
+                dst[4 * q + 2] = v.z;
+                dst[4 * q + 3] = v.w;
+            } else {
+                const double2 d = reinterpret_cast<const double2*>(src)[q];
+                dst[2 * q] = d.x;
+                dst[2 * q + 1] = d.y;
+            }
+        }
+    } else if constexpr (RB % 8 == 0 && sizeof(T) == 4) {
+#pragma unroll
+        for (int q = 0; q < N / 2; ++q) {
+            const float2 v = reinterpret_cast<const float2*>(src)[q];
+            dst[2 * q] = v.x;
+            dst[2 * q + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; ++q) dst[q] = src[q];
+    }
+}
+
+// b[kk] = fma(d[kk], t, b[kk]) for kk = 0..N-1 (packed FFMA2 for FP32: per-lane
+// numerics identical to __fmaf_rn, so the canonical order is unchanged).
+template <typename T, int N>
+__device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t)
+{
+    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+        const float2 tt = make_float2(t, t);
+#pragma unroll
+        for (int q = 0; q < N / 2; ++q) {
+            float2 r = __ffma2_rn(make_float2(d[2 * q], d[2 * q + 1]), tt,
+                                  make_float2(b[2 * q], b[2 * q + 1]));
+            b[2 * q] = r.x;
+            b[2 * q + 1] = r.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; ++q) b[q] = fma_t<T>(d[q], t, b[q]);
+    }
+}
+
 // ------------------------------------------------------------ K_A config
 // Per CTA: EPB elements, one thread per (i, j) of each element (k-loop in
 // registers).  STAGE_G: the CTA's G block (EPB*6*N^3 values) and its p/u block
@@ -88,7 +143,8 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     constexpr int N2 = N * N, N3 = N * N * N, EPB = ax_epb<T>(N);
     constexpr bool STAGE = ax_stage_g<T>(N);
     constexpr bool TMA = STAGE && (N % 2 == 0);
-    __shared__ T sD[N2], sDt[N2];
+    __shared__ __align__(16) T sD[N2];
+    __shared__ __align__(16) T sDt[N2];
     __shared__ __align__(8) uint64_t bar;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* sG = reinterpret_cast<T*>(smem_raw);                  // STAGE: EPB*6*N3
@@ -176,21 +232,37 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     }
     if constexpr (FUSED) __syncthreads();
 
+    // D rows / columns of this thread: D[i][l], D[j][l] (gradient) and
+    // D[l][i], D[l][j] (transpose), in registers when they fit.
+    constexpr bool DREG = N * sizeof(T) <= 48;
+
     // ---- gradient (C1), metric (C2), t-part of the transpose (C3: b chain)
     T b[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) b[k] = 0;
     if (valid) {
         const T* Ge = STAGE ? sG + el * 6 * N3 + ij : a.G + e * 6 * N3 + ij;
+        T Dri[N], Drj[N];
+        if constexpr (DREG) {
+            lds_row<T, N>(Dri, sD + i * N);
+            lds_row<T, N>(Drj, sD + j * N);
+        }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
+            if constexpr (!DREG) {
+                lds_row<T, N>(Dri, sD + i * N);
+                lds_row<T, N>(Drj, sD + j * N);
+            }
+            T urow[N], Dk[N];
+            lds_row<T, N>(urow, ue + k * N2 + j * N);   // u[k][j][:]
+            lds_row<T, N>(Dk, sD + k * N);              // D[k][:] (broadcast)
             T ur = 0, us = 0, ut = 0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) ur = fma_t<T>(sDt[l * N + i], ue[k * N2 + j * N + l], ur);
+            for (int l = 0; l < N; ++l) ur = fma_t<T>(Dri[l], urow[l], ur);
 #pragma unroll
-            for (int l = 0; l < N; ++l) us = fma_t<T>(sDt[l * N + j], ue[k * N2 + l * N + i], us);
+            for (int l = 0; l < N; ++l) us = fma_t<T>(Drj[l], ue[k * N2 + l * N + i], us);
 #pragma unroll
-            for (int l = 0; l < N; ++l) ut = fma_t<T>(sD[k * N + l], ureg[l], ut);
+            for (int l = 0; l < N; ++l) ut = fma_t<T>(Dk[l], ureg[l], ut);
             const T g1 = Ge[0 * N3 + k * N2], g2 = Ge[1 * N3 + k * N2], g3 = Ge[2 * N3 + k * N2];
             const T g4 = Ge[3 * N3 + k * N2], g5 = Ge[4 * N3 + k * N2], g6 = Ge[5 * N3 + k * N2];
             T wr = mul_t<T>(g1, ur);
@@ -205,8 +277,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             // own (i,j,k) slot of g1/g2 is dead after the reads above
             wre[k * N2 + ij] = wr;
             wse[k * N2 + ij] = ws;
-#pragma unroll
-            for (int kk = 0; kk < N; ++kk) b[kk] = fma_t<T>(sD[k * N + kk], wt, b[kk]);
+            fma_row<T, N>(b, Dk, wt);   // b[kk] = fma(D[k][kk], wt, b[kk])
         }
     }
     __syncthreads();
@@ -214,21 +285,40 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     // ---- r/s part of the transpose (C3: a chain), w = a + b, mask, pap
     acc_t acc;
     if (valid) {
-        ElemCoord ec = elem_coord(a.mesh, (uint32_t)e);
+        const ElemCoord ec = elem_coord(a.mesh, (uint32_t)e);
+        const int n1 = N - 1;
+        const bool mxy = (i == 0 && ec.ax == 0) || (i == n1 && ec.ax == a.mesh.ex - 1) ||
+                         (j == 0 && ec.ay == 0) || (j == n1 && ec.ay == a.mesh.ey - 1);
+        const bool sxy = (i == 0 && ec.ax > 0) || (i == n1 && ec.ax < a.mesh.ex - 1) ||
+                         (j == 0 && ec.ay > 0) || (j == n1 && ec.ay < a.mesh.ey - 1);
+        const bool mz0 = ec.azg == 0, mz1 = ec.azg == a.mesh.ezg - 1;
+        T Dci[N], Dcj[N];
+        if constexpr (DREG) {
+            lds_row<T, N>(Dci, sDt + i * N);   // D[:][i]
+            lds_row<T, N>(Dcj, sDt + j * N);   // D[:][j]
+        }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
+            if constexpr (!DREG) {
+                lds_row<T, N>(Dci, sDt + i * N);
+                lds_row<T, N>(Dcj, sDt + j * N);
+            }
+            T wrow[N];
+            lds_row<T, N>(wrow, wre + k * N2 + j * N);  // wr[k][j][:]
             T s = 0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) s = fma_t<T>(sD[l * N + i], wre[k * N2 + j * N + l], s);
+            for (int l = 0; l < N; ++l) s = fma_t<T>(Dci[l], wrow[l], s);
 #pragma unroll
-            for (int l = 0; l < N; ++l) s = fma_t<T>(sD[l * N + j], wse[k * N2 + l * N + i], s);
+            for (int l = 0; l < N; ++l) s = fma_t<T>(Dcj[l], wse[k * N2 + l * N + i], s);
             T wv = add_t<T>(s, b[k]);
-            if (a.mask && is_masked(a.mesh, ec, i, j, k)) wv = 0;   // C5: assign +0
+            const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
+            if (a.mask && masked) wv = 0;   // C5: assign +0
             a.w[base + k * N2] = wv;
             if constexpr (FUSED) {
                 // element-interior points (m == 1) contribute w p c here; shared
                 // nodes contribute once per node in K_B (bitwise-equal exact sum).
-                if (multiplicity(a.mesh, ec, i, j, k) == 1) acc.add(dot_term(wv, ureg[k], 1.0));
+                const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
+                if (!sxy && !sz) acc.add(dot_term(wv, ureg[k], 1.0));
             }
         }
     }
