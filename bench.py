@@ -100,6 +100,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def max_over_ranks(value: float, world: int, device="cuda") -> float:
+    """Max of a per-rank number over all ranks (timings: the slowest rank)."""
+    if world <= 1:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -170,10 +180,11 @@ def run_reference(args):
     return 0
 
 
-def workload_name(cfg, precision):
+def workload_name(cfg, precision, world=1):
     solver = "mixed FP32 solver (FP64 set-up, FP64 glsc3 accumulation, FP64 final check)" \
         if precision == "fp32" else "FP64 solver"
-    return (f"{cfg.name}: {cfg.ex}x{cfg.ey}x{cfg.ez} hex box, N={cfg.N} (p={cfg.N - 1}), "
+    ez = cfg.mesh_args(world)["ez"]
+    return (f"{cfg.name}: {cfg.ex}x{cfg.ey}x{ez} hex box, N={cfg.N} (p={cfg.N - 1}), "
             f"jitter={cfg.jitter}, {cfg.niter} unpreconditioned CG iterations, {solver}")
 
 
@@ -212,9 +223,18 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     import paper_2405_11065_b200 as nbk
     cfg = nbk.CONFIGS[args.config]
-    spec = nbk.MeshSpec(**cfg.mesh_args(1))
+    # z-slabs over the ranks: weak configs grow the box with N
+    spec = nbk.MeshSpec(**cfg.mesh_args(world))
     stream = torch.cuda.Stream()
-    ctx = nbk.cg_setup(spec, "fp32", device=local, stream=stream)
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nbk.nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy())
+    ctx = nbk.cg_setup(spec, "fp32", device=local, stream=stream, rank=rank, nranks=world,
+                       nccl_id=nccl_id)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     prec = args.precision
 
@@ -235,13 +255,9 @@ def run_gpu(args):
         ms_prof, kA, _, _, _ = time_solves(ctx, torch, cfg, prec, args.steps, args.warmup, flush,
                                            profile=True)
     barrier()
-    tot_ms = sum(ms)
-    if world > 1:
-        t = torch.tensor([tot_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
-    ng = ctx.n_global
-    value = world * ng * cfg.niter * args.steps / (tot_ms / 1e3) / 1e9
+    tot_ms = max_over_ranks(sum(ms), world)
+    ng = ctx.n_global  # global unique nodes of the whole (all-rank) box
+    value = ng * cfg.niter * args.steps / (tot_ms / 1e3) / 1e9
     launches = ctx.solve_launches(cfg.niter, prec) * args.steps
 
     # ---- roofline of the dominant kernel (fused ax, K_A) ----
@@ -270,7 +286,7 @@ def run_gpu(args):
             _, kA64, _, _, _ = time_solves(ctx, torch, cfg, "fp64", args.steps, args.warmup,
                                            flush, profile=True)
         barrier()
-        v64 = ng * cfg.niter * args.steps / (sum(ms64) / 1e3) / 1e9
+        v64 = ng * cfg.niter * args.steps / (max_over_ranks(sum(ms64), world) / 1e3) / 1e9
         ka64 = sum(kA64) / (args.steps * cfg.niter)
         extra["fp64"] = {"value": v64, "ms_per_step": sum(ms64) / args.steps,
                          "k_ax_avg_ms": ka64,
@@ -296,7 +312,7 @@ def run_gpu(args):
         b.record(stream)
         b.synchronize()
         e2e_ms.append(a.elapsed_time(b))
-    e2e_val = world * ng * cfg.niter * args.steps / (sum(e2e_ms) / 1e3) / 1e9
+    e2e_val = ng * cfg.niter * args.steps / (max_over_ranks(sum(e2e_ms), world) / 1e3) / 1e9
     e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
            "d2h_bytes_per_step": 8 * n + 8 * (cfg.niter + 1),
            "path": "nbk_cg_solve_host (pinned host f -> solve -> host x)"}
@@ -314,11 +330,12 @@ def run_gpu(args):
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "weak" if cfg.weak else "strong", "vs_baseline": None,
             "dtype": "f32" if prec == "fp32" else "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, prec), "n_global": ng, "n_local": n,
+            "config": {"workload": workload_name(cfg, prec, world), "n_global": ng, "n_local": n,
                        "niter": cfg.niter,
-                       "parallelism": "1 GPU" if world == 1 else f"{world} replicas",
+                       "parallelism": "1 GPU" if world == 1 else
+                       f"{world} z-slabs (NCCL face exchange + all-gather)",
                        "l2": "flushed between steps (512 MiB write, outside the events)"},
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "true_res_rel": res["true_res_rel"],

@@ -64,11 +64,24 @@ typedef struct {
 } nbk_mesh;
 
 /* Process / device placement.  rank owns element layers
- * iz in [rank*ez/nranks, (rank+1)*ez/nranks) (contiguous z-slabs, R21). */
+ * iz in [rank*ez/nranks, (rank+1)*ez/nranks) (contiguous z-slabs, R21; SURVEY
+ * 8(e)); 1 <= nranks <= 64.  Two ways to run nranks > 1:
+ *   - NCCL mode (one process per GPU, "nearest-neighbor communications
+ *     ... and Allreduce"): nccl_id points at the 128-byte id rank 0 obtained
+ *     from nbk_nccl_unique_id and broadcast to every rank; nbk_cg_setup is then
+ *     collective (ncclCommInitRank) and so are nbk_ax_apply (with DSSUM),
+ *     nbk_dssum, nbk_glsc3, nbk_cg_solve(_host): each exchanges the slab-face
+ *     layers with ncclSend/ncclRecv and all-gathers the per-rank inner-product
+ *     partials (combined in rank order, identical on every rank).
+ *   - virtual slabs (nccl_id == NULL): P contexts in one process on one device
+ *     and stream, linked with nbk_group_link and driven by the nbk_group_*
+ *     calls; the same kernels run with faces and partials shared by pointer.
+ * Either way results are bitwise independent of nranks. */
 typedef struct {
-    int32_t rank, nranks; /* nranks == 1 in this build (multi-rank: see DESIGN.md) */
+    int32_t rank, nranks; /* this context's slab and the number of slabs            */
     int32_t device;       /* CUDA device ordinal                                    */
     void* stream;         /* cudaStream_t the library enqueues on (NULL = legacy)   */
+    const void* nccl_id;  /* NCCL mode: 128-byte ncclUniqueId; NULL otherwise       */
 } nbk_dist;
 
 typedef struct {
@@ -80,6 +93,8 @@ typedef struct {
     int64_t n_copies; /* local points belonging to shared nodes                     */
     int32_t N;
     int32_t has_fp32; /* FP32 arrays allocated                                      */
+    int64_t face_layer; /* values per exchanged face layer (ex*ey*N^2), 0 if 1 rank   */
+    int64_t face_nodes; /* global nodes on this rank's slab-boundary planes           */
 } nbk_info;
 
 /* Outcome of a solve. */
@@ -104,6 +119,15 @@ typedef struct nbk_ctx nbk_ctx;
  * final FP64 check).  Returns NBK_EINVAL for an invalid mesh. */
 nbk_status nbk_workspace_bytes(const nbk_mesh* mesh, nbk_precision precision, const nbk_dist* dist,
                                size_t* bytes_out);
+
+/* Slab partition of the mesh for dist (host only, no device needed): local
+ * sizes, element offset, local dssum plan size and face sizes.  has_fp32 = 0. */
+nbk_status nbk_partition(const nbk_mesh* mesh, const nbk_dist* dist, nbk_info* info);
+
+/* NCCL mode bootstrap: writes a fresh 128-byte ncclUniqueId to out128 (call on
+ * rank 0, broadcast it, pass it in nbk_dist.nccl_id).  NBK_ENCCL if
+ * libnccl.so.2 cannot be loaded. */
+nbk_status nbk_nccl_unique_id(void* out128);
 
 /* cg_setup(mesh, N, precision) (north_star): FP64 set-up on the device:
  * GLL nodes/weights/D, geometric factors g1..g6, RHS, dssum plan (sorted
@@ -183,6 +207,26 @@ nbk_status nbk_query(const nbk_ctx* ctx, nbk_info* info);
 /* Number of kernel launches one nbk_cg_solve(niter, precision) performs. */
 nbk_status nbk_solve_launches(const nbk_ctx* ctx, int32_t niter, nbk_precision precision,
                               int64_t* launches);
+
+/* Virtual slabs (nranks > 1 without NCCL; SURVEY 8(e) "virtual-slab mode on
+ * one GPU"): link the P contexts ctxs[r] = rank r of P (same mesh, device,
+ * stream and set-up precision) so that their face buffers and reduction
+ * partials are shared.  The contexts then accept only the nbk_group_* calls
+ * below, which take the P contexts in rank order and per-rank arrays of device
+ * pointers (u_devs[r] etc., rank r's local storage).  Semantics equal the
+ * single-context calls on the whole mesh.  Destroying one member unlinks the
+ * group. */
+nbk_status nbk_group_link(nbk_ctx* const* ctxs, int32_t P);
+nbk_status nbk_group_ax_apply(nbk_ctx* const* ctxs, int32_t P, const void* const* u_devs,
+                              void* const* w_devs, int32_t flags, nbk_precision precision);
+nbk_status nbk_group_dssum(nbk_ctx* const* ctxs, int32_t P, void* const* f_devs, int32_t apply_mask,
+                           nbk_precision precision);
+nbk_status nbk_group_glsc3(nbk_ctx* const* ctxs, int32_t P, const void* const* a_devs,
+                           const void* const* b_devs, nbk_precision precision, double* out_host);
+/* hist/trace/result as nbk_cg_solve (identical on every rank); each member
+ * keeps its slab of the solution (nbk_get_solution per context). */
+nbk_status nbk_group_cg_solve(nbk_ctx* const* ctxs, int32_t P, int32_t niter, nbk_precision precision,
+                              double* hist_host, double* trace_host, nbk_result* result);
 
 const char* nbk_last_error(const nbk_ctx* ctx);
 const char* nbk_version(void);

@@ -19,6 +19,14 @@ SOURCES = ["nbk_capi.cu", "nbk_setup.cu"]
 HEADERS = ["nbk_common.cuh", "nbk_kernels.cuh", "nbk_internal.h", "../../include/nbk.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NCCL_DIR = None
+try:
+    import nvidia.nccl as _nccl  # the pip NCCL torch links (one libnccl.so.2 per process)
+    NCCL_DIR = os.path.dirname(_nccl.__file__) if _nccl.__file__ else list(_nccl.__path__)[0]
+except Exception:  # pragma: no cover
+    pass
+NCCL_INC = [f"-I{os.path.join(NCCL_DIR, 'include')}"] if NCCL_DIR else []
+NCCL_DEF = [f"-DNBK_NCCL_LIB=\"{os.path.join(NCCL_DIR, 'lib', 'libnccl.so.2')}\""] if NCCL_DIR else []
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-ftz=false", "-prec-div=true",
          "-prec-sqrt=true", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
@@ -41,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, *NCCL_DEF, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -53,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             fh.write(r.stderr)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

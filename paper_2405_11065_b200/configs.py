@@ -14,7 +14,7 @@ class Config:
     name: str
     ex: int
     ey: int
-    ez: int            # per GPU for the weak-scaling config C4 (global ez = ez * P)
+    ez: int            # per GPU for the weak-scaling configs (global ez = ez * P)
     N: int
     jitter: float
     seed_geom: int
@@ -32,10 +32,10 @@ class Config:
 CONFIGS = {
     "C1": Config("C1", 2, 2, 2, 8, 0.0, 0, 1001, 100,
                  note="tiny oracle case: undeformed 2x2x2, p=7"),
-    "C2": Config("C2", 16, 16, 16, 8, 0.0, 0, 1002, 100,
-                 note="undeformed 16^3, p=7, 100 CG iterations"),
-    "C3": Config("C3", 32, 32, 32, 12, 0.1, 2003, 1003, 100,
-                 note="deformed 32^3, p=11, +-10% vertex jitter"),
+    "C2": Config("C2", 16, 16, 16, 8, 0.0, 0, 1002, 100, weak=True,
+                 note="undeformed 16^3 (per GPU), p=7, 100 CG iterations"),
+    "C3": Config("C3", 32, 32, 32, 12, 0.1, 2003, 1003, 100, weak=True,
+                 note="deformed 32^3 (per GPU), p=11, +-10% vertex jitter"),
     "C4": Config("C4", 64, 64, 32, 8, 0.0, 0, 1004, 100, weak=True,
                  note="weak scaling 64x64x32 per GPU, p=7"),
     "C5": Config("C5", 64, 64, 64, 10, 0.1, 2005, 1005, 200,

@@ -1,12 +1,18 @@
 // nbk_capi.cu -- the extern "C" boundary of libnbk.so (include/nbk.h) and the
 // host orchestration of the hot path: kernel dispatch over N, the CG loop
 // captured once into a CUDA graph per (precision, niter), device-resident
-// scalars, one D2H copy of the history per solve.
+// scalars, one D2H copy of the history per solve; multi-rank z-slabs (NCCL
+// face exchange + all-gather of per-rank partials, or in-process virtual
+// slabs on one device).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <vector>
+
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "nbk_internal.h"
 #include "nbk_kernels.cuh"
@@ -125,6 +131,131 @@ static cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl 
     return launch_k(k_dssum<T, FUSED>, g, 256, 0, s, pdl, a);
 }
 
+// ------------------------------------------------------------ NCCL (dlopen)
+// NCCL is loaded at run time only when a context has nranks > 1 and a unique
+// id, so that the process uses the one libnccl.so.2 torch has already loaded
+// (dlopen by soname returns the loaded copy) and 1-rank use needs no NCCL.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclAllGather) allGather = nullptr;
+    decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+static const NcclApi* nccl_api(std::string& why)
+{
+    static NcclApi api;
+    static int state = 0;  // 0 untried, 1 ok, -1 failed
+    static std::string err;
+    if (state == 0) {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+#ifdef NBK_NCCL_LIB
+        if (!h) h = dlopen(NBK_NCCL_LIB, RTLD_NOW | RTLD_GLOBAL);
+#endif
+        if (!h) {
+            err = std::string("cannot load libnccl.so.2: ") + dlerror();
+            state = -1;
+        } else {
+#define NBK_SYM(f, n) api.f = (decltype(api.f))dlsym(h, n)
+            NBK_SYM(getUniqueId, "ncclGetUniqueId");
+            NBK_SYM(commInitRank, "ncclCommInitRank");
+            NBK_SYM(commDestroy, "ncclCommDestroy");
+            NBK_SYM(groupStart, "ncclGroupStart");
+            NBK_SYM(groupEnd, "ncclGroupEnd");
+            NBK_SYM(send, "ncclSend");
+            NBK_SYM(recv, "ncclRecv");
+            NBK_SYM(allGather, "ncclAllGather");
+            NBK_SYM(errorString, "ncclGetErrorString");
+#undef NBK_SYM
+            const bool ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.groupStart &&
+                            api.groupEnd && api.send && api.recv && api.allGather && api.errorString;
+            state = ok ? 1 : -1;
+            if (!ok) err = "libnccl.so.2 lacks a required symbol";
+        }
+    }
+    if (state < 0) { why = err; return nullptr; }
+    return &api;
+}
+
+// ------------------------------------------------------------ teams
+// The contexts whose work one call enqueues: {self} for a 1-rank or an NCCL
+// rank context, or all P contexts of an in-process virtual-slab group (every
+// slab on this device; faces and partials are shared by pointer aliasing and
+// the phases of all slabs are enqueued in order on the first member's stream).
+struct Team {
+    std::vector<nbk_ctx*> m;
+    bool multi = false;   // nranks > 1: face exchange + rank-ordered reductions
+    cudaStream_t s = nullptr;
+};
+
+static Team team_self(nbk_ctx* c)
+{
+    Team t;
+    t.m.push_back(c);
+    t.multi = c->nranks > 1;
+    t.s = c->stream;
+    return t;
+}
+
+template <typename T>
+static T* fld(nbk_ctx* c, int which, bool fp32)
+{
+    // which: 0 x, 1 r, 2 p, 3 w
+    void* v64[4] = {c->x64, c->r64, c->p64, c->w64};
+    void* v32[4] = {c->x32, c->r32, c->p32, c->w32};
+    return (T*)(fp32 ? v32[which] : v64[which]);
+}
+
+// Exchange the packed face layers with the neighbour ranks (NCCL mode).  In a
+// virtual group the receive buffers alias the neighbours' send buffers.
+template <typename T>
+static cudaError_t xchg_faces(const Team& t, cudaStream_t s, std::string& err)
+{
+    for (nbk_ctx* c : t.m) {
+        if (!c->comm) continue;
+        std::string why;
+        const NcclApi* A = nccl_api(why);
+        if (!A) { err = why; return cudaErrorUnknown; }
+        ncclComm_t comm = (ncclComm_t)c->comm;
+        const ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+        const size_t cnt = (size_t)c->nlayer;
+        ncclResult_t r = A->groupStart();
+        if (c->has_lo && r == ncclSuccess) r = A->send(c->send_lo, cnt, ty, c->rank - 1, comm, s);
+        if (c->has_lo && r == ncclSuccess) r = A->recv(c->recv_lo, cnt, ty, c->rank - 1, comm, s);
+        if (c->has_hi && r == ncclSuccess) r = A->send(c->send_hi, cnt, ty, c->rank + 1, comm, s);
+        if (c->has_hi && r == ncclSuccess) r = A->recv(c->recv_hi, cnt, ty, c->rank + 1, comm, s);
+        ncclResult_t r2 = A->groupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess) {
+            err = std::string("NCCL face exchange: ") + A->errorString(r != ncclSuccess ? r : r2);
+            return cudaErrorUnknown;
+        }
+    }
+    return cudaSuccess;
+}
+
+// All-gather of the per-rank dd partials, in place (slot = gather + rank).
+static cudaError_t xchg_gather(const Team& t, cudaStream_t s, std::string& err)
+{
+    for (nbk_ctx* c : t.m) {
+        if (!c->comm) continue;
+        std::string why;
+        const NcclApi* A = nccl_api(why);
+        if (!A) { err = why; return cudaErrorUnknown; }
+        ncclResult_t r = A->allGather(c->gather + c->rank, c->gather, 2, ncclFloat64,
+                                      (ncclComm_t)c->comm, s);
+        if (r != ncclSuccess) {
+            err = std::string("NCCL allgather: ") + A->errorString(r);
+            return cudaErrorUnknown;
+        }
+    }
+    return cudaSuccess;
+}
+
 // ------------------------------------------------------------ helpers
 template <typename T>
 static AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
@@ -154,83 +285,218 @@ static DssumArgs<T> dssum_args(nbk_ctx* c, T* w)
     d.g2 = c->g2; d.g4 = c->g4; d.g8 = c->g8;
     d.n2 = c->n2; d.n4 = c->n4; d.n8 = c->n8;
     d.seg_off = c->seg_off; d.seg_idx = c->seg_idx; d.nother = c->nother;
-    d.st = c->st; d.trace = c->trace; d.mesh = c->view; d.mask = 0;
+    d.st = c->st; d.trace = c->trace; d.mesh = c->view; d.mask = 0; d.fin = 1;
     return d;
 }
 
-// Enqueue one CG solve (T1 loop, fixed niter) on the stream; used under capture.
 template <typename T>
-static cudaError_t enqueue_solve(nbk_ctx* c, int niter, nbk_graph* g, bool fp32)
+static FaceArgs<T> face_args(nbk_ctx* c, T* w)
 {
-    cudaStream_t s = c->stream;
-    const T* D = fp32 ? (const T*)c->D32 : (const T*)c->D64;
-    const T* G = fp32 ? (const T*)c->G32 : (const T*)c->G64;
-    T* x = fp32 ? (T*)c->x32 : (T*)c->x64;
-    T* r = fp32 ? (T*)c->r32 : (T*)c->r64;
-    T* p = fp32 ? (T*)c->p32 : (T*)c->p64;
-    T* w = fp32 ? (T*)c->w32 : (T*)c->w64;
+    FaceArgs<T> f{};
+    f.w = w;
+    f.send_lo = (T*)c->send_lo; f.send_hi = (T*)c->send_hi;
+    f.recv_lo = (const T*)c->recv_lo; f.recv_hi = (const T*)c->recv_hi;
+    f.has_lo = c->has_lo; f.has_hi = c->has_hi;
+    f.parts = c->parts; f.st = c->st; f.slot = c->gather + c->rank; f.mesh = c->view;
+    return f;
+}
+
+static dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - NBK_VEC_GRID_MAX; }
+
+// dssum (+ mask) of w over a team.  fused: shared-node pap terms, alpha.
+// One rank: K_B (its last block forms alpha).  Several: K_B (publish only) and
+// the face pack, exchange, face merge (reduces this rank's pap), all-gather,
+// k_fin (rank-ordered combination, alpha).
+template <typename T, bool FUSED>
+static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std::vector<const T*>& p,
+                              int mask, bool pdl, std::string& err)
+{
+    cudaError_t e;
+    const cudaStream_t s = t.s;
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        nbk_ctx* c = t.m[q];
+        DssumArgs<T> d = dssum_args<T>(c, w[q]);
+        d.mask = mask;
+        if (FUSED) {
+            d.p = p[q];
+            d.parts = c->parts;
+            d.nA = ax_blocks_n<T>(c->E, c->N);
+            d.fin = t.multi ? 0 : 1;
+        }
+        if ((e = launch_dssum<T, FUSED>(d, s, pdl && !t.multi)) != cudaSuccess) return e;
+        if (t.multi) {
+            FaceArgs<T> f = face_args<T>(c, w[q]);
+            k_face_pack<T><<<vec_grid(2 * c->nlayer), 256, 0, s>>>(f);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+    }
+    if (!t.multi) return cudaSuccess;
+    if ((e = xchg_faces<T>(t, s, err)) != cudaSuccess) return e;
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        nbk_ctx* c = t.m[q];
+        FaceArgs<T> f = face_args<T>(c, w[q]);
+        f.mask = mask;
+        if (FUSED) {
+            f.p = p[q];
+            f.nprev = ax_blocks_n<T>(c->E, c->N) +
+                      vec_grid((c->n2 + c->n4 + c->n8 + c->nother + 1) / 2);
+        }
+        const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
+        k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (FUSED) {
+        if ((e = xchg_gather(t, s, err)) != cudaSuccess) return e;
+        for (nbk_ctx* c : t.m) {
+            k_fin<0><<<1, 32, 0, s>>>(c->gather, c->nranks, c->st, c->hist, c->trace);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+// Vector kernel (K_C and the other modes) over a team: one rank finalises in
+// its last block; several publish per-rank partials, all-gather, k_fin.
+template <typename T, int MODE>
+static cudaError_t vec_team(const Team& t, const std::vector<VecArgs<T>>& args, bool pdl,
+                            std::string& err)
+{
+    cudaError_t e;
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        VecArgs<T> a = args[q];
+        a.slot = t.multi ? t.m[q]->gather + t.m[q]->rank : nullptr;
+        if ((e = launch_vec<T, MODE>(a, t.s, pdl && !t.multi)) != cudaSuccess) return e;
+    }
+    if (!t.multi) return cudaSuccess;
+    if ((e = xchg_gather(t, t.s, err)) != cudaSuccess) return e;
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        nbk_ctx* c = t.m[q];
+        k_fin<1 + MODE><<<1, 32, 0, t.s>>>(c->gather, c->nranks, c->st, c->hist, c->trace);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+template <typename T>
+static VecArgs<T> vec_args(nbk_ctx* c)
+{
+    VecArgs<T> v{};
+    v.n = c->n; v.parts = vec_parts(c); v.st = c->st; v.hist = c->hist; v.trace = c->trace;
+    v.mesh = c->view;
+    return v;
+}
+
+// ax (+ dssum + mask) of per-member fields over a team (standalone / final check).
+template <typename T>
+static cudaError_t ax_team(const Team& t, const std::vector<const T*>& u, const std::vector<T*>& w,
+                           int flags, bool fp32, std::string& err)
+{
+    cudaError_t e;
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        nbk_ctx* c = t.m[q];
+        AxArgs<T> a = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
+                           : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
+        a.u = u[q]; a.w = w[q]; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
+        if ((e = launch_ax<T, false>(a, t.s)) != cudaSuccess) return e;
+    }
+    if (flags & NBK_AX_DSSUM) return dssum_team<T, false>(t, w, {}, 0, false, err);
+    return cudaSuccess;
+}
+
+// Enqueue one CG solve (T1 loop, fixed niter) for the team; used under capture.
+template <typename T>
+static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp32, bool profiling,
+                                 std::string& err)
+{
+    const cudaStream_t s = t.s;
+    const size_t P = t.m.size();
     cudaError_t e;
     int64_t launches = 0;
+    std::vector<T*> x(P), r(P), p(P), w(P);
+    std::vector<const T*> pc(P);
+    for (size_t q = 0; q < P; ++q) {
+        x[q] = fld<T>(t.m[q], 0, fp32); r[q] = fld<T>(t.m[q], 1, fp32);
+        p[q] = fld<T>(t.m[q], 2, fp32); w[q] = fld<T>(t.m[q], 3, fp32);
+        pc[q] = p[q];
+    }
+    const int64_t per_fin = t.multi ? 1 : 0;  // k_fin launches per reduction and member
+    const int64_t nface = t.multi ? 2 : 0;    // pack + merge per dssum and member
 
-    VecArgs<T> vi{};
-    vi.r = r; vi.x = x; vi.p = p; vi.f = c->f64; vi.n = c->n; vi.parts = c->parts + c->nparts - NBK_VEC_GRID_MAX;
-    vi.st = c->st; vi.hist = c->hist; vi.trace = c->trace; vi.mesh = c->view;
-    if ((e = launch_vec<T, VEC_INIT>(vi, s)) != cudaSuccess) return e;
-    ++launches;
+    std::vector<VecArgs<T>> vi(P), vr(P);
+    for (size_t q = 0; q < P; ++q) {
+        vi[q] = vec_args<T>(t.m[q]);
+        vi[q].r = r[q]; vi[q].x = x[q]; vi[q].p = p[q]; vi[q].f = t.m[q]->f64;
+        vr[q] = vi[q];
+        vr[q].w = w[q];
+    }
+    if ((e = vec_team<T, VEC_INIT>(t, vi, false, err)) != cudaSuccess) return e;
+    launches += (int64_t)P * (1 + per_fin);
 
-    AxArgs<T> aa = ax_args<T>(c, D, G);
-    aa.u = nullptr; aa.w = w; aa.p = p; aa.r = r; aa.x = x; aa.mask = 1;
-    DssumArgs<T> da = dssum_args<T>(c, w);
-    da.p = p; da.parts = c->parts; da.nA = ax_blocks_n<T>(c->E, c->N);
-    VecArgs<T> vr = vi;
-    vr.w = w;
     for (int k = 1; k <= niter; ++k) {
-        if (g && c->profiling) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1)], s, cudaEventRecordExternal);
-        const bool pdl = !(g && c->profiling);  // events between kernels break PDL edges
-        if ((e = launch_ax<T, true>(aa, s, false, pdl)) != cudaSuccess) return e;
-        if (g && c->profiling) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = launch_dssum<T, true>(da, s, pdl)) != cudaSuccess) return e;
-        if ((e = launch_vec<T, VEC_RUPD>(vr, s, pdl)) != cudaSuccess) return e;
-        launches += 3;
+        const bool prof = g && profiling && P == 1;
+        if (prof) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1)], s, cudaEventRecordExternal);
+        const bool pdl = !prof;  // events between kernels break PDL edges
+        for (size_t q = 0; q < P; ++q) {
+            nbk_ctx* c = t.m[q];
+            AxArgs<T> aa = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
+                                : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
+            aa.u = nullptr; aa.w = w[q]; aa.p = p[q]; aa.r = r[q]; aa.x = x[q]; aa.mask = 1;
+            if ((e = launch_ax<T, true>(aa, s, false, pdl)) != cudaSuccess) return e;
+        }
+        if (prof) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1) + 1], s, cudaEventRecordExternal);
+        if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err)) != cudaSuccess) return e;
+        if ((e = vec_team<T, VEC_RUPD>(t, vr, pdl, err)) != cudaSuccess) return e;
+        launches += (int64_t)P * (3 + nface + 2 * per_fin);
     }
-    k_tail_x<T><<<vec_grid(c->n), 256, 0, s>>>(x, p, c->st, c->n);
-    ++launches;
-
-    // final FP64 residual check (C12): x64 = (double)x ; r_true = f - A x64
-    if (fp32) {
-        k_upcast<<<vec_grid(c->n), 256, 0, s>>>(c->x64, (const float*)x, c->n);
+    for (size_t q = 0; q < P; ++q) {
+        nbk_ctx* c = t.m[q];
+        k_tail_x<T><<<vec_grid(c->n), 256, 0, s>>>(x[q], p[q], c->st, c->n);
         ++launches;
+        // final FP64 residual check (C12): x64 = (double)x ; r_true = f - A x64
+        if (fp32) {
+            k_upcast<<<vec_grid(c->n), 256, 0, s>>>(c->x64, (const float*)x[q], c->n);
+            ++launches;
+        }
     }
-    AxArgs<double> a64 = ax_args<double>(c, c->D64, c->G64);
-    a64.u = c->x64; a64.w = c->w64; a64.mask = 1;
-    if ((e = launch_ax<double, false>(a64, s)) != cudaSuccess) return e;
-    DssumArgs<double> d64 = dssum_args<double>(c, c->w64);
-    if ((e = launch_dssum<double, false>(d64, s)) != cudaSuccess) return e;
-    VecArgs<double> vt{};
-    vt.r = c->r64; vt.w = c->w64; vt.f = c->f64; vt.n = c->n; vt.parts = vi.parts; vt.st = c->st;
-    vt.hist = c->hist; vt.trace = c->trace; vt.mesh = c->view;
-    if ((e = launch_vec<double, VEC_TRUE>(vt, s)) != cudaSuccess) return e;
-    launches += 3;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    std::vector<const double*> x64(P);
+    std::vector<double*> w64(P);
+    std::vector<VecArgs<double>> vt(P);
+    for (size_t q = 0; q < P; ++q) {
+        nbk_ctx* c = t.m[q];
+        x64[q] = c->x64; w64[q] = c->w64;
+        vt[q] = vec_args<double>(c);
+        vt[q].r = c->r64; vt[q].w = c->w64; vt[q].f = c->f64;
+    }
+    if ((e = ax_team<double>(t, x64, w64, NBK_AX_DSSUM | NBK_AX_MASK, false, err)) != cudaSuccess) return e;
+    if ((e = vec_team<double, VEC_TRUE>(t, vt, false, err)) != cudaSuccess) return e;
+    launches += (int64_t)P * (3 + nface + per_fin);
     if (g) g->launches = launches;
     return cudaSuccess;
 }
 
-static nbk_status get_graph(nbk_ctx* c, int niter, nbk_precision prec, nbk_graph** out)
+static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_graph** out)
 {
+    nbk_ctx* c = t.m[0];
     auto key = std::make_tuple((int)prec, niter, c->profiling);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) { *out = &it->second; return NBK_OK; }
     nbk_graph g;
-    if (c->profiling) {
+    if (c->profiling && t.m.size() == 1) {
         g.prof_events.resize(2 * niter);
         for (auto& ev : g.prof_events) NBK_CUDA(c, cudaEventCreate(&ev));
     }
-    NBK_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    cudaError_t e = prec == NBK_FP32 ? enqueue_solve<float>(c, niter, &g, true)
-                                     : enqueue_solve<double>(c, niter, &g, false);
+    NBK_CUDA(c, cudaStreamBeginCapture(t.s, cudaStreamCaptureModeThreadLocal));
+    std::string err;
+    cudaError_t e = prec == NBK_FP32 ? enqueue_solve<float>(t, niter, &g, true, c->profiling, err)
+                                     : enqueue_solve<double>(t, niter, &g, false, c->profiling, err);
     cudaGraph_t graph = nullptr;
-    cudaError_t e2 = cudaStreamEndCapture(c->stream, &graph);
-    if (e != cudaSuccess) return fail(c, NBK_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+    cudaError_t e2 = cudaStreamEndCapture(t.s, &graph);
+    if (e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        return fail(c, err.empty() ? NBK_ECUDA : NBK_ENCCL,
+                    std::string("capture: ") + (err.empty() ? cudaGetErrorString(e) : err));
+    }
     if (e2 != cudaSuccess) return fail(c, NBK_ECUDA, std::string("end capture: ") + cudaGetErrorString(e2));
     g.graph = graph;
     NBK_CUDA(c, cudaGraphInstantiate(&g.exec, graph, 0));
@@ -262,7 +528,26 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
     return launch_ax<float, true>(a32, c->stream, true);
 }
 
-static nbk_status refresh_fp32_and_h0(nbk_ctx* c)
+// glsc3 over a team (synchronous); result identical on every member.
+template <typename T>
+static nbk_status glsc3_team(const Team& t, const std::vector<const T*>& a, const std::vector<const T*>& b,
+                             double* out)
+{
+    nbk_ctx* c0 = t.m[0];
+    std::vector<VecArgs<T>> v(t.m.size());
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        v[q] = vec_args<T>(t.m[q]);
+        v[q].a = a[q]; v[q].b = b[q];
+    }
+    std::string err;
+    cudaError_t e = vec_team<T, VEC_DOT>(t, v, false, err);
+    if (e != cudaSuccess) return fail(c0, err.empty() ? NBK_ECUDA : NBK_ENCCL, err.empty() ? cudaGetErrorString(e) : err);
+    NBK_CUDA(c0, cudaMemcpyAsync(out, &c0->st->dot, 8, cudaMemcpyDeviceToHost, t.s));
+    NBK_CUDA(c0, cudaStreamSynchronize(t.s));
+    return NBK_OK;
+}
+
+static nbk_status refresh_fp32(nbk_ctx* c)
 {
     cudaStream_t s = c->stream;
     if (c->G32) {
@@ -270,22 +555,85 @@ static nbk_status refresh_fp32_and_h0(nbk_ctx* c)
         k_downcast<<<1, 256, 0, s>>>(c->D32, c->D64, (int64_t)c->N * c->N);
         NBK_CUDA(c, cudaGetLastError());
     }
-    // h0 (FP64) = sqrt(glsc3(f, c, f)) for the relative true residual
-    VecArgs<double> v{};
-    v.a = c->f64; v.b = c->f64; v.n = c->n; v.parts = c->parts + c->nparts - NBK_VEC_GRID_MAX;
-    v.st = c->st; v.mesh = c->view;
-    NBK_CUDA(c, launch_vec<double, VEC_DOT>(v, s));
-    double dot = 0.0;
-    NBK_CUDA(c, cudaMemcpyAsync(&dot, &c->st->dot, 8, cudaMemcpyDeviceToHost, s));
-    NBK_CUDA(c, cudaStreamSynchronize(s));
-    c->h0_64 = std::sqrt(dot);
+    c->h0_dirty = 1;
     return NBK_OK;
+}
+
+// h0 (FP64) = sqrt(glsc3(f, c, f)) for the relative true residual (C12).
+static nbk_status refresh_h0(const Team& t)
+{
+    bool dirty = false;
+    for (nbk_ctx* c : t.m) dirty = dirty || c->h0_dirty;
+    if (!dirty) return NBK_OK;
+    std::vector<const double*> f(t.m.size());
+    for (size_t q = 0; q < t.m.size(); ++q) f[q] = t.m[q]->f64;
+    double dot = 0.0;
+    nbk_status st = glsc3_team<double>(t, f, f, &dot);
+    if (st != NBK_OK) return st;
+    for (nbk_ctx* c : t.m) {
+        c->h0_64 = std::sqrt(dot);
+        c->h0_dirty = 0;
+    }
+    return NBK_OK;
+}
+
+// Team of a call made on one context: errors for virtual-group members.
+static nbk_status self_team(nbk_ctx* c, Team& t)
+{
+    if (c->nranks > 1 && !c->comm)
+        return fail(c, NBK_ESTATE, "virtual-slab context: use the nbk_group_* calls");
+    t = team_self(c);
+    return NBK_OK;
+}
+
+static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, double* hist_host,
+                             double* trace_host, nbk_result* result)
+{
+    nbk_ctx* c = t.m[0];
+    if (niter < 1 || niter > NBK_MAX_NITER) return fail(c, NBK_EINVAL, "niter out of range");
+    if (prec != NBK_FP64 && prec != NBK_FP32) return fail(c, NBK_EINVAL, "bad precision");
+    for (nbk_ctx* m : t.m)
+        if (prec == NBK_FP32 && !m->G32) return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
+    nbk_status st = refresh_h0(t);
+    if (st != NBK_OK) return st;
+    nbk_graph* g = nullptr;
+    st = get_graph(t, niter, prec, &g);
+    if (st != NBK_OK) return st;
+    cudaStream_t s = t.s;
+    NBK_CUDA(c, cudaEventRecord(c->ev0, s));
+    NBK_CUDA(c, cudaGraphLaunch(g->exec, s));
+    NBK_CUDA(c, cudaEventRecord(c->ev1, s));
+    CgState hs;
+    NBK_CUDA(c, cudaMemcpyAsync(&hs, c->st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    if (hist_host) NBK_CUDA(c, cudaMemcpyAsync(hist_host, c->hist, 8 * (size_t)(niter + 1), cudaMemcpyDeviceToHost, s));
+    if (trace_host) NBK_CUDA(c, cudaMemcpyAsync(trace_host, c->trace, 8 * 5 * (size_t)niter, cudaMemcpyDeviceToHost, s));
+    NBK_CUDA(c, cudaStreamSynchronize(s));
+    for (nbk_ctx* m : t.m) m->last_solved_precision = (int)prec;
+    if (result) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+        result->solve_ms = ms;
+        result->true_res = std::sqrt(hs.true_rtr);
+        result->true_res_rel = c->h0_64 > 0 ? result->true_res / c->h0_64 : 0.0;
+        result->defect_iter = hs.defect;
+        result->niter = niter;
+        float ka = 0.f;
+        if (c->profiling && !g->prof_events.empty()) {
+            for (int k = 0; k < niter; ++k) {
+                float tk = 0.f;
+                cudaEventElapsedTime(&tk, g->prof_events[2 * k], g->prof_events[2 * k + 1]);
+                ka += tk;
+            }
+        }
+        result->kA_ms = ka;
+    }
+    return hs.defect ? fail(c, NBK_EDEFECT, "CG defect: pap <= 0 or non-finite scalar") : NBK_OK;
 }
 
 // ================================================================== ABI
 extern "C" {
 
-const char* nbk_version(void) { return "nbk 0.1 (sm_100a)"; }
+const char* nbk_version(void) { return "nbk 0.2 (sm_100a; z-slab multi-rank)"; }
 
 const char* nbk_last_error(const nbk_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
@@ -298,6 +646,38 @@ nbk_status nbk_workspace_bytes(const nbk_mesh* mesh, nbk_precision precision, co
     if (precision != NBK_FP64 && precision != NBK_FP32) return fail(nullptr, NBK_EINVAL, "bad precision");
     Layout L = compute_layout(mesh, precision, dist);
     *bytes_out = L.total;
+    return NBK_OK;
+}
+
+nbk_status nbk_partition(const nbk_mesh* mesh, const nbk_dist* dist, nbk_info* info)
+{
+    std::string why;
+    if (!info) return fail(nullptr, NBK_EINVAL, "info is NULL");
+    if (!validate_mesh(mesh, dist, why)) return fail(nullptr, NBK_EINVAL, why);
+    Layout L = compute_layout(mesh, NBK_FP64, dist);
+    info->n_local = L.n;
+    info->n_global = L.n_global;
+    info->e_local = L.E;
+    info->e_offset = L.e_offset;
+    info->n_shared = L.nseg;
+    info->n_copies = L.ncopies;
+    info->N = mesh->N;
+    info->has_fp32 = 0;
+    info->face_layer = (L.has_lo + L.has_hi) ? L.nlayer : 0;
+    info->face_nodes = (L.has_lo + L.has_hi) * L.nplane;
+    return NBK_OK;
+}
+
+nbk_status nbk_nccl_unique_id(void* out128)
+{
+    if (!out128) return fail(nullptr, NBK_EINVAL, "out is NULL");
+    std::string why;
+    const NcclApi* A = nccl_api(why);
+    if (!A) return fail(nullptr, NBK_ENCCL, why);
+    ncclUniqueId id;
+    ncclResult_t r = A->getUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, NBK_ENCCL, A->errorString(r));
+    std::memcpy(out128, &id, sizeof(id));
     return NBK_OK;
 }
 
@@ -314,7 +694,7 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(nullptr, NBK_ECUDA, "no CUDA device (libnbk has no CPU fallback)");
-    nbk_dist d1{0, 1, 0, nullptr};
+    nbk_dist d1{0, 1, 0, nullptr, nullptr};
     const nbk_dist* d = dist ? dist : &d1;
     if (cudaSetDevice(d->device) != cudaSuccess) return fail(nullptr, NBK_ECUDA, "cudaSetDevice failed");
     Layout L = compute_layout(mesh, precision, d);
@@ -335,6 +715,12 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     c->ncopies = L.ncopies;
     c->nparts = L.nparts;
     c->view = make_view(mesh, d);
+    c->rank = d->rank;
+    c->nranks = d->nranks;
+    c->has_lo = L.has_lo;
+    c->has_hi = L.has_hi;
+    c->nlayer = L.nlayer;
+    c->nplane = L.nplane;
     unsigned char* b = (unsigned char*)dev_workspace;
     c->st = (CgState*)(b + L.off_state);
     c->D64 = (double*)(b + L.off_D64);
@@ -345,6 +731,15 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     c->seg_off = (int32_t*)(b + L.off_segoff);
     c->seg_idx = (int32_t*)(b + L.off_segidx);
     c->grp = (int32_t*)(b + L.off_grp);
+    if (c->has_lo || c->has_hi) {
+        const size_t fb = 8 * (size_t)L.nlayer;
+        c->send_lo = b + L.off_face;
+        c->send_hi = b + L.off_face + fb;
+        c->recv_lo = b + L.off_face + 2 * fb;
+        c->recv_hi = b + L.off_face + 3 * fb;
+    }
+    c->gather_own = (dd*)(b + L.off_gather);
+    c->gather = c->gather_own;
     c->G64 = (double*)(b + L.off_G64);
     c->f64 = (double*)(b + L.off_f64);
     const size_t v64 = ((size_t)8 * c->n + 255) & ~(size_t)255;
@@ -362,21 +757,34 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
         c->p32 = (float*)(b + L.off_vec32 + 2 * v32);
         c->w32 = (float*)(b + L.off_vec32 + 3 * v32);
     }
+    // NCCL communicator (collective over the ranks) when an id is given
+    if (c->nranks > 1 && d->nccl_id) {
+        const NcclApi* A = nccl_api(why);
+        if (!A) { delete c; return fail(nullptr, NBK_ENCCL, why); }
+        ncclUniqueId id;
+        std::memcpy(&id, d->nccl_id, sizeof(id));
+        ncclComm_t comm = nullptr;
+        ncclResult_t r = A->commInitRank(&comm, c->nranks, id, c->rank);
+        if (r != ncclSuccess) { delete c; return fail(nullptr, NBK_ENCCL, std::string("ncclCommInitRank: ") + A->errorString(r)); }
+        c->comm = comm;
+    }
     nbk_status st = NBK_OK;
     cudaError_t e = set_ax_attrs(c);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->st, 0, sizeof(CgState), c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->gather_own, 0, sizeof(dd) * NBK_MAX_RANKS, c->stream);
     if (e == cudaSuccess) e = setup_device(c, L);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
         std::string m = std::string("set-up: ") + cudaGetErrorString(e);
-        delete c;
+        nbk_destroy(c);
         return fail(nullptr, NBK_ECUDA, m);
     }
     // vectors start at zero (the plan used their space as scratch)
     e = cudaMemsetAsync(c->x64, 0, 4 * v64, c->stream);
-    if (e != cudaSuccess) { delete c; return fail(nullptr, NBK_ECUDA, cudaGetErrorString(e)); }
-    st = refresh_fp32_and_h0(c);
-    if (st != NBK_OK) { std::string m = c->err; delete c; return fail(nullptr, st, m); }
+    if (e != cudaSuccess) { nbk_destroy(c); return fail(nullptr, NBK_ECUDA, cudaGetErrorString(e)); }
+    st = refresh_fp32(c);
+    if (st == NBK_OK && !(c->nranks > 1 && !c->comm)) st = refresh_h0(team_self(c));
+    if (st != NBK_OK) { std::string m = c->err; nbk_destroy(c); return fail(nullptr, st, m); }
     cudaEventCreate(&c->ev0);
     cudaEventCreate(&c->ev1);
     *out = c;
@@ -390,7 +798,10 @@ nbk_status nbk_load_arrays(nbk_ctx* c, const double* D_host, const double* G_hos
     if (D_host) NBK_CUDA(c, cudaMemcpyAsync(c->D64, D_host, 8 * c->N * c->N, cudaMemcpyHostToDevice, s));
     if (G_host) NBK_CUDA(c, cudaMemcpyAsync(c->G64, G_host, 8 * 6 * c->n, cudaMemcpyHostToDevice, s));
     if (f_host) NBK_CUDA(c, cudaMemcpyAsync(c->f64, f_host, 8 * c->n, cudaMemcpyHostToDevice, s));
-    return refresh_fp32_and_h0(c);
+    nbk_status st = refresh_fp32(c);
+    if (st != NBK_OK) return st;
+    NBK_CUDA(c, cudaStreamSynchronize(s));
+    return NBK_OK;
 }
 
 nbk_status nbk_get_arrays(nbk_ctx* c, double* D_host, double* G_host, double* f_host)
@@ -404,76 +815,112 @@ nbk_status nbk_get_arrays(nbk_ctx* c, double* D_host, double* G_host, double* f_
     return NBK_OK;
 }
 
+static nbk_status ax_apply_team(const Team& t, const void* const* u_dev, void* const* w_dev, int32_t flags,
+                                nbk_precision prec)
+{
+    nbk_ctx* c = t.m[0];
+    if (flags & ~(NBK_AX_DSSUM | NBK_AX_MASK)) return fail(c, NBK_EINVAL, "bad flags");
+    if (prec != NBK_FP64 && prec != NBK_FP32) return fail(c, NBK_EINVAL, "bad precision");
+    const size_t P = t.m.size();
+    for (size_t q = 0; q < P; ++q) {
+        if (!u_dev[q] || !w_dev[q] || u_dev[q] == w_dev[q]) return fail(c, NBK_EINVAL, "u/w must be distinct non-NULL");
+        if (prec == NBK_FP32 && !t.m[q]->G32) return fail(c, NBK_ESTATE, "context has no FP32 arrays");
+    }
+    std::string err;
+    cudaError_t e;
+    if (prec == NBK_FP64) {
+        std::vector<const double*> u(P);
+        std::vector<double*> w(P);
+        for (size_t q = 0; q < P; ++q) { u[q] = (const double*)u_dev[q]; w[q] = (double*)w_dev[q]; }
+        e = ax_team<double>(t, u, w, flags, false, err);
+    } else {
+        std::vector<const float*> u(P);
+        std::vector<float*> w(P);
+        for (size_t q = 0; q < P; ++q) { u[q] = (const float*)u_dev[q]; w[q] = (float*)w_dev[q]; }
+        e = ax_team<float>(t, u, w, flags, true, err);
+    }
+    if (e != cudaSuccess)
+        return fail(c, err.empty() ? NBK_ECUDA : NBK_ENCCL, err.empty() ? cudaGetErrorString(e) : err);
+    return NBK_OK;
+}
+
 nbk_status nbk_ax_apply(nbk_ctx* c, const void* u_dev, void* w_dev, int32_t flags, nbk_precision prec)
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
-    if (!u_dev || !w_dev || u_dev == w_dev) return fail(c, NBK_EINVAL, "u/w must be distinct non-NULL");
-    if (flags & ~(NBK_AX_DSSUM | NBK_AX_MASK)) return fail(c, NBK_EINVAL, "bad flags");
-    if (prec == NBK_FP32 && !c->G32) return fail(c, NBK_ESTATE, "context has no FP32 arrays");
-    cudaStream_t s = c->stream;
+    Team t;
+    nbk_status st = self_team(c, t);
+    if (st != NBK_OK) return st;
+    return ax_apply_team(t, &u_dev, &w_dev, flags, prec);
+}
+
+static nbk_status dssum_team_abi(const Team& t, void* const* f_dev, int32_t apply_mask, nbk_precision prec)
+{
+    nbk_ctx* c = t.m[0];
+    const size_t P = t.m.size();
+    for (size_t q = 0; q < P; ++q)
+        if (!f_dev[q]) return fail(c, NBK_EINVAL, "f is NULL");
+    std::string err;
+    cudaError_t e;
     if (prec == NBK_FP64) {
-        AxArgs<double> a = ax_args<double>(c, c->D64, c->G64);
-        a.u = (const double*)u_dev; a.w = (double*)w_dev; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
-        NBK_CUDA(c, launch_ax<double, false>(a, s));
-        if (flags & NBK_AX_DSSUM) {
-            DssumArgs<double> d = dssum_args<double>(c, (double*)w_dev);
-            NBK_CUDA(c, launch_dssum<double, false>(d, s));
+        std::vector<double*> w(P);
+        for (size_t q = 0; q < P; ++q) w[q] = (double*)f_dev[q];
+        e = dssum_team<double, false>(t, w, {}, apply_mask ? 1 : 0, false, err);
+        for (size_t q = 0; e == cudaSuccess && apply_mask && q < P; ++q) {
+            k_mask<double><<<vec_grid(t.m[q]->n), 256, 0, t.s>>>(w[q], t.m[q]->view);
+            e = cudaGetLastError();
         }
     } else if (prec == NBK_FP32) {
-        AxArgs<float> a = ax_args<float>(c, c->D32, c->G32);
-        a.u = (const float*)u_dev; a.w = (float*)w_dev; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
-        NBK_CUDA(c, launch_ax<float, false>(a, s));
-        if (flags & NBK_AX_DSSUM) {
-            DssumArgs<float> d = dssum_args<float>(c, (float*)w_dev);
-            NBK_CUDA(c, launch_dssum<float, false>(d, s));
+        std::vector<float*> w(P);
+        for (size_t q = 0; q < P; ++q) w[q] = (float*)f_dev[q];
+        e = dssum_team<float, false>(t, w, {}, apply_mask ? 1 : 0, false, err);
+        for (size_t q = 0; e == cudaSuccess && apply_mask && q < P; ++q) {
+            k_mask<float><<<vec_grid(t.m[q]->n), 256, 0, t.s>>>(w[q], t.m[q]->view);
+            e = cudaGetLastError();
         }
     } else {
         return fail(c, NBK_EINVAL, "bad precision");
     }
+    if (e != cudaSuccess)
+        return fail(c, err.empty() ? NBK_ECUDA : NBK_ENCCL, err.empty() ? cudaGetErrorString(e) : err);
     return NBK_OK;
 }
 
 nbk_status nbk_dssum(nbk_ctx* c, void* f_dev, int32_t apply_mask, nbk_precision prec)
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
-    if (!f_dev) return fail(c, NBK_EINVAL, "f is NULL");
-    cudaStream_t s = c->stream;
+    Team t;
+    nbk_status st = self_team(c, t);
+    if (st != NBK_OK) return st;
+    return dssum_team_abi(t, &f_dev, apply_mask, prec);
+}
+
+static nbk_status glsc3_team_abi(const Team& t, const void* const* a_dev, const void* const* b_dev,
+                                 nbk_precision prec, double* out)
+{
+    nbk_ctx* c = t.m[0];
+    const size_t P = t.m.size();
+    if (!out) return fail(c, NBK_EINVAL, "NULL argument");
+    for (size_t q = 0; q < P; ++q)
+        if (!a_dev[q] || !b_dev[q]) return fail(c, NBK_EINVAL, "NULL argument");
     if (prec == NBK_FP64) {
-        DssumArgs<double> d = dssum_args<double>(c, (double*)f_dev);
-        NBK_CUDA(c, launch_dssum<double, false>(d, s));
-        if (apply_mask) { k_mask<double><<<vec_grid(c->n), 256, 0, s>>>((double*)f_dev, c->view); NBK_CUDA(c, cudaGetLastError()); }
+        std::vector<const double*> a(P), b(P);
+        for (size_t q = 0; q < P; ++q) { a[q] = (const double*)a_dev[q]; b[q] = (const double*)b_dev[q]; }
+        return glsc3_team<double>(t, a, b, out);
     } else if (prec == NBK_FP32) {
-        DssumArgs<float> d = dssum_args<float>(c, (float*)f_dev);
-        NBK_CUDA(c, launch_dssum<float, false>(d, s));
-        if (apply_mask) { k_mask<float><<<vec_grid(c->n), 256, 0, s>>>((float*)f_dev, c->view); NBK_CUDA(c, cudaGetLastError()); }
-    } else {
-        return fail(c, NBK_EINVAL, "bad precision");
+        std::vector<const float*> a(P), b(P);
+        for (size_t q = 0; q < P; ++q) { a[q] = (const float*)a_dev[q]; b[q] = (const float*)b_dev[q]; }
+        return glsc3_team<float>(t, a, b, out);
     }
-    return NBK_OK;
+    return fail(c, NBK_EINVAL, "bad precision");
 }
 
 nbk_status nbk_glsc3(nbk_ctx* c, const void* a_dev, const void* b_dev, nbk_precision prec, double* out)
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
-    if (!a_dev || !b_dev || !out) return fail(c, NBK_EINVAL, "NULL argument");
-    cudaStream_t s = c->stream;
-    dd* parts = c->parts + c->nparts - NBK_VEC_GRID_MAX;
-    if (prec == NBK_FP64) {
-        VecArgs<double> v{};
-        v.a = (const double*)a_dev; v.b = (const double*)b_dev; v.n = c->n; v.parts = parts;
-        v.st = c->st; v.mesh = c->view;
-        NBK_CUDA(c, launch_vec<double, VEC_DOT>(v, s));
-    } else if (prec == NBK_FP32) {
-        VecArgs<float> v{};
-        v.a = (const float*)a_dev; v.b = (const float*)b_dev; v.n = c->n; v.parts = parts;
-        v.st = c->st; v.mesh = c->view;
-        NBK_CUDA(c, launch_vec<float, VEC_DOT>(v, s));
-    } else {
-        return fail(c, NBK_EINVAL, "bad precision");
-    }
-    NBK_CUDA(c, cudaMemcpyAsync(out, &c->st->dot, 8, cudaMemcpyDeviceToHost, s));
-    NBK_CUDA(c, cudaStreamSynchronize(s));
-    return NBK_OK;
+    Team t;
+    nbk_status st = self_team(c, t);
+    if (st != NBK_OK) return st;
+    return glsc3_team_abi(t, &a_dev, &b_dev, prec, out);
 }
 
 nbk_status nbk_set_profiling(nbk_ctx* c, int32_t enable)
@@ -487,41 +934,10 @@ nbk_status nbk_cg_solve(nbk_ctx* c, int32_t niter, nbk_precision prec, double* h
                         double* trace_host, nbk_result* result)
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
-    if (niter < 1 || niter > NBK_MAX_NITER) return fail(c, NBK_EINVAL, "niter out of range");
-    if (prec != NBK_FP64 && prec != NBK_FP32) return fail(c, NBK_EINVAL, "bad precision");
-    if (prec == NBK_FP32 && !c->G32) return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
-    nbk_graph* g = nullptr;
-    nbk_status st = get_graph(c, niter, prec, &g);
+    Team t;
+    nbk_status st = self_team(c, t);
     if (st != NBK_OK) return st;
-    cudaStream_t s = c->stream;
-    NBK_CUDA(c, cudaEventRecord(c->ev0, s));
-    NBK_CUDA(c, cudaGraphLaunch(g->exec, s));
-    NBK_CUDA(c, cudaEventRecord(c->ev1, s));
-    CgState hs;
-    NBK_CUDA(c, cudaMemcpyAsync(&hs, c->st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
-    if (hist_host) NBK_CUDA(c, cudaMemcpyAsync(hist_host, c->hist, 8 * (size_t)(niter + 1), cudaMemcpyDeviceToHost, s));
-    if (trace_host) NBK_CUDA(c, cudaMemcpyAsync(trace_host, c->trace, 8 * 5 * (size_t)niter, cudaMemcpyDeviceToHost, s));
-    NBK_CUDA(c, cudaStreamSynchronize(s));
-    c->last_solved_precision = (int)prec;
-    if (result) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->ev0, c->ev1);
-        result->solve_ms = ms;
-        result->true_res = std::sqrt(hs.true_rtr);
-        result->true_res_rel = c->h0_64 > 0 ? result->true_res / c->h0_64 : 0.0;
-        result->defect_iter = hs.defect;
-        result->niter = niter;
-        float ka = 0.f;
-        if (c->profiling) {
-            for (int k = 0; k < niter; ++k) {
-                float t = 0.f;
-                cudaEventElapsedTime(&t, g->prof_events[2 * k], g->prof_events[2 * k + 1]);
-                ka += t;
-            }
-        }
-        result->kA_ms = ka;
-    }
-    return hs.defect ? fail(c, NBK_EDEFECT, "CG defect: pap <= 0 or non-finite scalar") : NBK_OK;
+    return solve_team(t, niter, prec, hist_host, trace_host, result);
 }
 
 nbk_status nbk_cg_solve_host(nbk_ctx* c, const double* f_host, int32_t niter, nbk_precision prec,
@@ -530,8 +946,9 @@ nbk_status nbk_cg_solve_host(nbk_ctx* c, const double* f_host, int32_t niter, nb
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
     if (f_host) {
         NBK_CUDA(c, cudaMemcpyAsync(c->f64, f_host, 8 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
-        nbk_status st0 = refresh_fp32_and_h0(c);  // new RHS: new h0 for the relative residual
+        nbk_status st0 = refresh_fp32(c);  // new RHS: new h0 for the relative residual
         if (st0 != NBK_OK) return st0;
+        c->h0_dirty = 1;
     }
     nbk_status st = nbk_cg_solve(c, niter, prec, hist_host, nullptr, result);
     if (st != NBK_OK && st != NBK_EDEFECT) return st;
@@ -570,14 +987,101 @@ nbk_status nbk_query(const nbk_ctx* c, nbk_info* info)
     info->n_copies = c->ncopies;
     info->N = c->N;
     info->has_fp32 = c->G32 ? 1 : 0;
+    info->face_layer = (c->has_lo + c->has_hi) ? c->nlayer : 0;
+    info->face_nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
     return NBK_OK;
 }
 
 nbk_status nbk_solve_launches(const nbk_ctx* c, int32_t niter, nbk_precision prec, int64_t* launches)
 {
     if (!c || !launches) return fail(nullptr, NBK_EINVAL, "NULL argument");
-    *launches = 1 + 3 * (int64_t)niter + 1 + (prec == NBK_FP32 ? 1 : 0) + 3;
+    const int64_t multi = c->nranks > 1 ? 1 : 0;
+    // init (+fin), per iteration K_A, K_B, K_C (+ pack, merge, 2 fin), tail_x, [upcast],
+    // final check K_A, K_B, K_C (+ pack, merge, fin)
+    *launches = (1 + multi) + (3 + 4 * multi) * (int64_t)niter + 1 + (prec == NBK_FP32 ? 1 : 0) +
+                (3 + 3 * multi);
     return NBK_OK;
+}
+
+// ------------------------------------------------------------ virtual slabs
+static nbk_status group_team(nbk_ctx* const* ctxs, int32_t P, Team& t)
+{
+    if (!ctxs || P < 1 || P > NBK_MAX_RANKS) return fail(nullptr, NBK_EINVAL, "bad context array");
+    for (int r = 0; r < P; ++r)
+        if (!ctxs[r]) return fail(nullptr, NBK_EINVAL, "NULL context");
+    nbk_ctx* c0 = ctxs[0];
+    if ((int)c0->group.size() != P) return fail(c0, NBK_ESTATE, "contexts are not linked (nbk_group_link)");
+    for (int r = 0; r < P; ++r)
+        if (c0->group[r] != ctxs[r]) return fail(c0, NBK_EINVAL, "context order differs from the linked group");
+    t.m.assign(ctxs, ctxs + P);
+    t.multi = P > 1;
+    t.s = c0->stream;
+    return NBK_OK;
+}
+
+nbk_status nbk_group_link(nbk_ctx* const* ctxs, int32_t P)
+{
+    if (!ctxs || P < 1 || P > NBK_MAX_RANKS) return fail(nullptr, NBK_EINVAL, "bad context array");
+    for (int r = 0; r < P; ++r) {
+        nbk_ctx* c = ctxs[r];
+        if (!c) return fail(nullptr, NBK_EINVAL, "NULL context");
+        if (c->rank != r || c->nranks != P) return fail(c, NBK_EINVAL, "context r must be rank r of P");
+        if (c->comm) return fail(c, NBK_ESTATE, "NCCL context cannot join a virtual group");
+        if (std::memcmp(&c->mesh, &ctxs[0]->mesh, sizeof(nbk_mesh)) != 0)
+            return fail(c, NBK_EINVAL, "contexts of a group must share the mesh");
+        if (c->stream != ctxs[0]->stream) return fail(c, NBK_EINVAL, "contexts of a group must share the stream");
+        if (c->dist.device != ctxs[0]->dist.device) return fail(c, NBK_EINVAL, "contexts of a group must share the device");
+        if ((c->G32 != nullptr) != (ctxs[0]->G32 != nullptr)) return fail(c, NBK_EINVAL, "mixed set-up precisions");
+    }
+    for (int r = 0; r < P; ++r) {
+        nbk_ctx* c = ctxs[r];
+        c->group.assign(ctxs, ctxs + P);
+        c->gather = ctxs[0]->gather_own;      // one shared partial array
+        if (c->has_lo) c->recv_lo = ctxs[r - 1]->send_hi;
+        if (c->has_hi) c->recv_hi = ctxs[r + 1]->send_lo;
+        c->h0_dirty = 1;
+        destroy_graphs(c);
+    }
+    return NBK_OK;
+}
+
+nbk_status nbk_group_ax_apply(nbk_ctx* const* ctxs, int32_t P, const void* const* u_devs,
+                              void* const* w_devs, int32_t flags, nbk_precision prec)
+{
+    Team t;
+    nbk_status st = group_team(ctxs, P, t);
+    if (st != NBK_OK) return st;
+    if (!u_devs || !w_devs) return fail(ctxs[0], NBK_EINVAL, "NULL pointer array");
+    return ax_apply_team(t, u_devs, w_devs, flags, prec);
+}
+
+nbk_status nbk_group_dssum(nbk_ctx* const* ctxs, int32_t P, void* const* f_devs, int32_t apply_mask,
+                           nbk_precision prec)
+{
+    Team t;
+    nbk_status st = group_team(ctxs, P, t);
+    if (st != NBK_OK) return st;
+    if (!f_devs) return fail(ctxs[0], NBK_EINVAL, "NULL pointer array");
+    return dssum_team_abi(t, f_devs, apply_mask, prec);
+}
+
+nbk_status nbk_group_glsc3(nbk_ctx* const* ctxs, int32_t P, const void* const* a_devs,
+                           const void* const* b_devs, nbk_precision prec, double* out_host)
+{
+    Team t;
+    nbk_status st = group_team(ctxs, P, t);
+    if (st != NBK_OK) return st;
+    if (!a_devs || !b_devs) return fail(ctxs[0], NBK_EINVAL, "NULL pointer array");
+    return glsc3_team_abi(t, a_devs, b_devs, prec, out_host);
+}
+
+nbk_status nbk_group_cg_solve(nbk_ctx* const* ctxs, int32_t P, int32_t niter, nbk_precision prec,
+                              double* hist_host, double* trace_host, nbk_result* result)
+{
+    Team t;
+    nbk_status st = group_team(ctxs, P, t);
+    if (st != NBK_OK) return st;
+    return solve_team(t, niter, prec, hist_host, trace_host, result);
 }
 
 void nbk_destroy(nbk_ctx* c)
@@ -586,6 +1090,17 @@ void nbk_destroy(nbk_ctx* c)
     destroy_graphs(c);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->comm) {
+        std::string why;
+        const NcclApi* A = nccl_api(why);
+        if (A) A->commDestroy((ncclComm_t)c->comm);
+    }
+    // unlink from a virtual group: the others must not alias this workspace
+    for (nbk_ctx* o : std::vector<nbk_ctx*>(c->group)) {
+        if (o == c) continue;
+        o->group.clear();
+        destroy_graphs(o);
+    }
     delete c;
 }
 

@@ -12,6 +12,7 @@
 
 #define NBK_MAX_NITER 10000
 #define NBK_VEC_GRID_MAX (148 * 8)
+#define NBK_MAX_RANKS 64
 
 struct nbk_graph {
     cudaGraph_t graph = nullptr;
@@ -47,6 +48,17 @@ struct nbk_ctx {
     unsigned char* scratch = nullptr;  // set-up scratch (aliases the vector region)
     size_t scratch_bytes = 0;
 
+    // multi-rank z-slabs; nranks == 1: none of this is used
+    int rank = 0, nranks = 1;
+    int has_lo = 0, has_hi = 0;        // neighbour slab below / above
+    int64_t nlayer = 0, nplane = 0;    // face layer values ex*ey*N^2, plane nodes Gx*Gy
+    void *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
+    nbk::dd* gather = nullptr;         // P per-rank partials (group-shared in virtual mode)
+    nbk::dd* gather_own = nullptr;
+    void* comm = nullptr;              // ncclComm_t (NCCL mode)
+    std::vector<nbk_ctx*> group;       // virtual slabs: all P contexts of the process
+    int h0_dirty = 0;
+
     double h0_64 = 0.0;  // sqrt(glsc3(f64, c, f64)) (C12 denominator)
     int profiling = 0;
     std::map<std::tuple<int, int, int>, nbk_graph> graphs;  // (precision, niter, profiling)
@@ -58,7 +70,9 @@ namespace nbk {
 
 struct Layout {
     size_t off_state, off_D64, off_D32, off_hist, off_trace, off_parts, off_segoff, off_segidx, off_grp,
-        off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
+        off_face, off_gather, off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
+    int64_t nlayer, nplane;
+    int has_lo, has_hi;
     int64_t E, n, n_global, nseg, ncopies, nparts, e_offset;
     size_t scratch_need;
 };

@@ -329,6 +329,67 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     }
 }
 
+// ------------------------------------------------------- scalar finalisers
+// CG scalars from the globally reduced inner products (rules C7, C9); run by
+// one thread: the last block of the reducing kernel (1 rank) or k_fin after
+// the rank-ordered combination of the per-rank partials (several ranks).
+__device__ __forceinline__ void fin_alpha(CgState* st, double pap, double* trace)
+{
+    const int k = st->it;
+    const double rtz1 = st->rtr;
+    double alpha = 0.0;
+    if (!st->zero) alpha = rtz1 / pap;                                   // C7
+    if (!st->zero && st->defect == 0 && (!(pap > 0.0) || !isfinite(pap)))
+        st->defect = k;                                                  // C9
+    st->alpha = alpha;
+    st->alpham = -alpha;
+    st->alpha32 = (float)alpha;
+    st->alpham32 = -(float)alpha;
+    double* tr = trace + 5 * (int64_t)(k - 1);
+    tr[0] = rtz1;
+    tr[1] = st->beta;
+    tr[2] = alpha;
+    tr[3] = pap;
+}
+
+enum VecMode { VEC_INIT = 0, VEC_RUPD = 1, VEC_TRUE = 2, VEC_DOT = 3 };
+
+template <int MODE>
+__device__ __forceinline__ void fin_rtr(CgState* st, double rtr, double* hist, double* trace)
+{
+    if constexpr (MODE == VEC_INIT) {
+        st->rtr = rtr;
+        st->rtz2 = 0.0;
+        st->beta = 0.0;
+        st->beta32 = 0.0f;
+        st->alpha = 0.0;
+        st->alpha32 = 0.0f;
+        st->alpham = 0.0;
+        st->alpham32 = 0.0f;
+        st->zero = (rtr == 0.0);
+        st->defect = 0;
+        st->it = 1;
+        hist[0] = sqrt(rtr);
+    } else if constexpr (MODE == VEC_RUPD) {
+        const int k = st->it;
+        hist[k] = sqrt(rtr);                    // h_k (R13)
+        trace[5 * (int64_t)(k - 1) + 4] = rtr;
+        if (!st->zero && st->defect == 0 && !isfinite(rtr)) st->defect = k;
+        const double rtz1_next = rtr, rtz2_next = st->rtr;
+        st->rtz2 = rtz2_next;
+        st->rtr = rtz1_next;
+        if (rtz1_next == 0.0) st->zero = 1;     // C9
+        const double beta = st->zero ? 0.0 : rtz1_next / rtz2_next;  // C7
+        st->beta = beta;
+        st->beta32 = (float)beta;
+        st->it = k + 1;
+    } else if constexpr (MODE == VEC_TRUE) {
+        st->true_rtr = rtr;
+    } else {
+        st->dot = rtr;
+    }
+}
+
 // ---------------------------------------------------------------- K_B
 // The dssum plan groups the segments (unique shared nodes) by multiplicity
 // m in {2, 4, 8}: group m is a dense int32 array of m ascending local indices
@@ -350,6 +411,7 @@ struct DssumArgs {
     CgState* st;
     double* trace;            // fused: per-iteration trace (niter*5)
     int mask;                 // standalone: assign +0 to masked shared nodes
+    int fin;                  // fused: 1 = last block forms alpha (1 rank); 0 = publish only
     MeshView mesh;
 };
 
@@ -452,35 +514,24 @@ __global__ void __launch_bounds__(256) k_dssum(DssumArgs<T> a)
     pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
+        if (!a.fin) {
+            // multi-rank: the face-merge kernel adds the slab-face terms and
+            // reduces every partial (K_A, K_B, merge) of this rank
+            if (threadIdx.x == 0) a.parts[a.nA + blockIdx.x] = v;
+            return;
+        }
         const unsigned int total = gridDim.x;
         if (publish_and_check_last(a.parts, a.nA + blockIdx.x, v, &a.st->cnt[0], total)) {
             dd pap_dd = reduce_partials(a.parts, a.nA + (int)gridDim.x);
             if (threadIdx.x == 0) {
-                CgState* st = a.st;
-                const int k = st->it;
-                const double pap = pap_dd.hi;
-                const double rtz1 = st->rtr;
-                double alpha = 0.0;
-                if (!st->zero) alpha = rtz1 / pap;                     // C7
-                if (!st->zero && st->defect == 0 && (!(pap > 0.0) || !isfinite(pap)))
-                    st->defect = k;                                   // C9
-                st->alpha = alpha;
-                st->alpham = -alpha;
-                st->alpha32 = (float)alpha;
-                st->alpham32 = -(float)alpha;
-                double* tr = a.trace + 5 * (int64_t)(k - 1);
-                tr[0] = rtz1;
-                tr[1] = st->beta;
-                tr[2] = alpha;
-                tr[3] = pap;
-                st->cnt[0] = 0;
+                fin_alpha(a.st, pap_dd.hi, a.trace);
+                a.st->cnt[0] = 0;
             }
         }
     }
 }
 
 // ---------------------------------------------------------------- K_C
-enum VecMode { VEC_INIT = 0, VEC_RUPD = 1, VEC_TRUE = 2, VEC_DOT = 3 };
 
 template <typename T>
 struct VecArgs {
@@ -496,6 +547,7 @@ struct VecArgs {
     CgState* st;
     double* hist;
     double* trace;
+    dd* slot;           // multi-rank: this rank's reduced partial (NULL: finalise here)
     MeshView mesh;
 };
 
@@ -613,40 +665,14 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
     if (publish_and_check_last(a.parts, blockIdx.x, v, &a.st->cnt[1], gridDim.x)) {
         dd tot = reduce_partials(a.parts, (int)gridDim.x);
         if (threadIdx.x == 0) {
-            CgState* st = a.st;
-            const double rtr = tot.hi;
-            if constexpr (MODE == VEC_INIT) {
-                st->rtr = rtr;
-                st->rtz2 = 0.0;
-                st->beta = 0.0;
-                st->beta32 = 0.0f;
-                st->alpha = 0.0;
-                st->alpha32 = 0.0f;
-                st->alpham = 0.0;
-                st->alpham32 = 0.0f;
-                st->zero = (rtr == 0.0);
-                st->defect = 0;
-                st->it = 1;
-                a.hist[0] = sqrt(rtr);
-            } else if constexpr (MODE == VEC_RUPD) {
-                const int k = st->it;
-                a.hist[k] = sqrt(rtr);                  // h_k (R13)
-                a.trace[5 * (int64_t)(k - 1) + 4] = rtr;
-                if (!st->zero && st->defect == 0 && !isfinite(rtr)) st->defect = k;
-                const double rtz1_next = rtr, rtz2_next = st->rtr;
-                st->rtz2 = rtz2_next;
-                st->rtr = rtz1_next;
-                if (rtz1_next == 0.0) st->zero = 1;     // C9
-                const double beta = st->zero ? 0.0 : rtz1_next / rtz2_next;  // C7
-                st->beta = beta;
-                st->beta32 = (float)beta;
-                st->it = k + 1;
-            } else if constexpr (MODE == VEC_TRUE) {
-                st->true_rtr = rtr;
+            if (a.slot) {
+                // multi-rank: publish this rank's partial; k_fin finalises
+                a.slot->hi = tot.hi;
+                a.slot->lo = tot.lo;
             } else {
-                st->dot = rtr;
+                fin_rtr<MODE>(a.st, tot.hi, a.hist, a.trace);
             }
-            st->cnt[1] = 0;
+            a.st->cnt[1] = 0;
         }
     }
 }
@@ -689,6 +715,145 @@ __global__ void __launch_bounds__(256) k_mask(T* w, MeshView m)
         ElemCoord ec = elem_coord(m, e);
         if (is_masked(m, ec, rem % N, (rem / N) % N, rem / (N * N))) w[L] = 0;
     }
+}
+
+// ------------------------------------------------------- multi-rank slabs
+// Contiguous z-slabs (R21).  A global node on the plane between
+// the slabs of ranks r and r+1 has its copies in the top element layer of
+// rank r (k = N-1) and the bottom layer of rank r+1 (k = 0).  The canonical
+// chain (C4: ascending GLOBAL local index) visits all of rank r's copies, in
+// ascending element order, then all of rank r+1's.  Each rank sends the raw
+// face layer of its own copies to the neighbour and both ranks evaluate the
+// same chain from the same values: bit-identical sums on both sides, equal to
+// the one-rank result.  The local dssum plan excludes these plane nodes.
+template <typename T>
+struct FaceArgs {
+    T* w;
+    const T* p;            // fused: p (face pap term, counted by the lower rank)
+    T* send_lo;            // own bottom layer (k = 0 of local layer 0), ex*ey*N^2
+    T* send_hi;            // own top layer (k = N-1 of the last local layer)
+    const T* recv_lo;      // lower neighbour's top layer
+    const T* recv_hi;      // upper neighbour's bottom layer
+    int has_lo, has_hi;
+    int mask;              // standalone: assign +0 to Dirichlet plane nodes (C5)
+    dd* parts;             // fused: partials [0, nprev) of K_A and K_B, then this kernel's
+    int nprev;
+    CgState* st;
+    dd* slot;              // fused: this rank's reduced pap partial
+    MeshView mesh;
+};
+
+// Pack the raw face layers: layer index q = el*N^2 + j*N + i, el = ax + ex*ay.
+template <typename T>
+__global__ void __launch_bounds__(256) k_face_pack(FaceArgs<T> a)
+{
+    const int N = a.mesh.N, N2 = N * N, N3 = N2 * N;
+    const int64_t nl = (int64_t)a.mesh.ex * a.mesh.ey * N2;
+    const int64_t exy = (int64_t)a.mesh.ex * a.mesh.ey;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < 2 * nl;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const bool hi = q >= nl;
+        const int64_t t = hi ? q - nl : q;
+        if (hi ? !a.has_hi : !a.has_lo) continue;
+        const int64_t el = t / N2;
+        const int pos = (int)(t - el * N2);
+        if (hi) {
+            const int64_t e = (int64_t)(a.mesh.ez_local - 1) * exy + el;
+            a.send_hi[t] = a.w[e * N3 + (int64_t)(N - 1) * N2 + pos];
+        } else {
+            a.send_lo[t] = a.w[el * N3 + pos];
+        }
+    }
+}
+
+// Elements (ascending) containing global plane coordinate g along one axis.
+__device__ __forceinline__ int plane_elems(int g, int ne, int N, int (&ae)[2], int (&loc)[2])
+{
+    const int n1 = N - 1;
+    const int a = g / n1;
+    int c = 0;
+    if (g - a * n1 == 0) {
+        if (a > 0) { ae[c] = a - 1; loc[c] = n1; ++c; }
+        if (a < ne) { ae[c] = a; loc[c] = 0; ++c; }
+    } else {
+        ae[c] = a; loc[c] = g - a * n1; ++c;
+    }
+    return c;
+}
+
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
+{
+    const MeshView& m = a.mesh;
+    const int N = m.N, N2 = N * N, N3 = N2 * N;
+    const int Gx = m.ex * (N - 1) + 1, Gy = m.ey * (N - 1) + 1;
+    const int64_t np = (int64_t)Gx * Gy;
+    const int64_t exy = (int64_t)m.ex * m.ey;
+    const int nplanes = a.has_lo + a.has_hi;
+    acc_t acc;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nplanes * np;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const bool upper = a.has_lo ? (q >= np) : true;   // upper = shared with rank + 1
+        const int64_t t = q >= np ? q - np : q;
+        const int gy = (int)(t / Gx), gx = (int)(t - (int64_t)gy * Gx);
+        int axe[2], il[2], aye[2], jl[2];
+        const int nx = plane_elems(gx, m.ex, N, axe, il);
+        const int ny = plane_elems(gy, m.ey, N, aye, jl);
+        // own copies: layer base element and plane k
+        const int64_t ebase = upper ? (int64_t)(m.ez_local - 1) * exy : 0;
+        const int kpl = upper ? N - 1 : 0;
+        const T* other = upper ? a.recv_hi : a.recv_lo;
+        T sum = 0;
+        bool first = true;
+        // chain: lower rank's copies first (ascending element), then the upper's
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const bool own = upper ? (side == 0) : (side == 1);
+            for (int by = 0; by < ny; ++by)
+                for (int bx = 0; bx < nx; ++bx) {
+                    const int64_t el = axe[bx] + (int64_t)m.ex * aye[by];
+                    const int pos = jl[by] * N + il[bx];
+                    const T v = own ? a.w[(ebase + el) * N3 + (int64_t)kpl * N2 + pos]
+                                    : other[el * N2 + pos];
+                    sum = first ? v : add_t<T>(sum, v);
+                    first = false;
+                }
+        }
+        if (!FUSED && a.mask && (gx == 0 || gx == Gx - 1 || gy == 0 || gy == Gy - 1)) sum = 0;
+        T p0 = 0;
+        for (int by = 0; by < ny; ++by)
+            for (int bx = 0; bx < nx; ++bx) {
+                const int64_t el = axe[bx] + (int64_t)m.ex * aye[by];
+                const int64_t L = (ebase + el) * N3 + (int64_t)kpl * N2 + jl[by] * N + il[bx];
+                if (FUSED && by == 0 && bx == 0) p0 = a.p[L];
+                a.w[L] = sum;
+            }
+        if constexpr (FUSED)
+            if (upper) acc.add(dot_term(sum, p0, 1.0));  // one term per node (lower rank)
+    }
+    if constexpr (FUSED) {
+        dd v = block_reduce_dd(acc.get());
+        if (publish_and_check_last(a.parts, a.nprev + blockIdx.x, v, &a.st->cnt[2], gridDim.x)) {
+            dd tot = reduce_partials(a.parts, a.nprev + (int)gridDim.x);
+            if (threadIdx.x == 0) {
+                a.slot->hi = tot.hi;
+                a.slot->lo = tot.lo;
+                a.st->cnt[2] = 0;
+            }
+        }
+    }
+}
+
+// Combine the P per-rank partials in rank order (identical on every rank)
+// and run the scalar finaliser.  KIND: 0 = alpha (pap); 1 + VecMode = rtr etc.
+template <int KIND>
+__global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double* trace)
+{
+    if (threadIdx.x != 0) return;
+    dd t{__ldcg(&gather[0].hi), __ldcg(&gather[0].lo)};
+    for (int r = 1; r < P; ++r) t = dd_add(t, dd{__ldcg(&gather[r].hi), __ldcg(&gather[r].lo)});
+    if constexpr (KIND == 0) fin_alpha(st, t.hi, trace);
+    else fin_rtr<KIND - 1>(st, t.hi, hist, trace);
 }
 
 }  // namespace nbk

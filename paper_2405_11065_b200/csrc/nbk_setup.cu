@@ -32,7 +32,7 @@ bool validate_mesh(const nbk_mesh* m, const nbk_dist* d, std::string& why)
     int nr = d ? d->nranks : 1, rk = d ? d->rank : 0;
     if (nr < 1 || rk < 0 || rk >= nr) { why = "bad rank / nranks"; return false; }
     if (m->ez % nr != 0) { why = "ez must be divisible by nranks"; return false; }
-    if (nr != 1) { why = "multi-rank slabs are not enabled in this build (nranks must be 1)"; return false; }
+    if (nr > NBK_MAX_RANKS) { why = "nranks exceeds NBK_MAX_RANKS (64)"; return false; }
     int64_t n = (int64_t)m->ex * m->ey * (m->ez / nr) * m->N * m->N * m->N;
     if (n >= (int64_t)1 << 31) { why = "local point count must fit in int32"; return false; }
     int64_t ng = ((int64_t)m->ex * (m->N - 1) + 1) * ((int64_t)m->ey * (m->N - 1) + 1) *
@@ -96,7 +96,19 @@ Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
     box_counts(m->ex, m->ey, m->ez, N, L.n_global, nsh_dummy);
     box_counts(m->ex, m->ey, v.ez_local, N, ngl, L.nseg);
     L.ncopies = L.n - (ngl - L.nseg);
-    L.nparts = L.E + 2 * NBK_VEC_GRID_MAX + 64;  // >= K_A CTAs for every EPB
+    // rank-boundary planes are summed by the face exchange, not the local plan
+    const int nr = d ? d->nranks : 1, rk = d ? d->rank : 0;
+    L.has_lo = rk > 0;
+    L.has_hi = rk < nr - 1;
+    const int64_t Gx = (int64_t)m->ex * (N - 1) + 1, Gy = (int64_t)m->ey * (N - 1) + 1;
+    const int64_t U = (Gx - m->ex + 1) * (Gy - m->ey + 1);  // plane nodes with one in-plane copy
+    const int nb = L.has_lo + L.has_hi;
+    L.nlayer = (int64_t)m->ex * m->ey * N * N;
+    L.nplane = Gx * Gy;
+    L.nseg -= nb * (L.nplane - U);
+    L.ncopies -= nb * (L.nlayer - U);
+    // partial slots: K_A (<= E CTAs), K_B, face merge, vector kernels (<= 1184 each)
+    L.nparts = L.E + 3 * NBK_VEC_GRID_MAX + 64;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
     L.off_state = take(sizeof(CgState));
@@ -108,6 +120,8 @@ Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
     L.off_segoff = take(4 * (size_t)(L.nseg + 1));
     L.off_segidx = take(4 * (size_t)(L.ncopies > 0 ? L.ncopies : 1));
     L.off_grp = take(4 * (size_t)L.ncopies + 64);
+    L.off_face = take(nb ? 4 * 8 * (size_t)L.nlayer : 8);
+    L.off_gather = take(sizeof(dd) * NBK_MAX_RANKS);
     L.off_G64 = take(8 * 6 * (size_t)L.n);
     L.off_f64 = take(8 * (size_t)L.n);
     L.scratch_need = plan_scratch_bytes(L.n, L.nseg);
@@ -296,17 +310,28 @@ __global__ void __launch_bounds__(256) k_gid_keys(MeshView m, uint32_t* keys, ui
     }
 }
 
-// flag_head[q] = 1 if q starts a run of length > 1; in_run[q] = 1 if q's run has length > 1
-__global__ void __launch_bounds__(256) k_run_flags(const uint32_t* keys, int64_t n, uint32_t* head,
-                                                   uint32_t* inrun)
+// flag_head[q] = 1 if q starts a run of length > 1; in_run[q] = 1 if q's run has length > 1.
+// Points on a rank-boundary plane (all copies of such a node lie on it) are
+// left to the face exchange: never part of a local segment.
+__global__ void __launch_bounds__(256) k_run_flags(const uint32_t* keys, const uint32_t* vals,
+                                                   int64_t n, MeshView m, int has_lo, int has_hi,
+                                                   uint32_t* head, uint32_t* inrun)
 {
+    const int N = m.N, N2 = N * N, N3 = N2 * N;
+    const int64_t exy = (int64_t)m.ex * m.ey;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = keys[q];
         const bool same_prev = q > 0 && keys[q - 1] == k;
         const bool same_next = q + 1 < n && keys[q + 1] == k;
-        head[q] = (!same_prev && same_next) ? 1u : 0u;
-        inrun[q] = (same_prev || same_next) ? 1u : 0u;
+        const int64_t L = vals[q];
+        const int64_t e = L / N3;
+        const int kk = (int)((L / N2) % N);
+        const int64_t az = e / exy;
+        const bool excl = (has_lo && az == 0 && kk == 0) ||
+                          (has_hi && az == m.ez_local - 1 && kk == N - 1);
+        head[q] = (!excl && !same_prev && same_next) ? 1u : 0u;
+        inrun[q] = (!excl && (same_prev || same_next)) ? 1u : 0u;
     }
 }
 
@@ -404,7 +429,8 @@ cudaError_t build_plan(nbk_ctx* ctx)
     uint32_t* vals = vb.Current();
     uint32_t* kalt = kb.Alternate();  // reuse as head_pos
     uint32_t* valt = vb.Alternate();  // reuse as run_pos
-    k_run_flags<<<grid_for(n), 256, 0, s>>>(keys, n, head, inrun);
+    k_run_flags<<<grid_for(n), 256, 0, s>>>(keys, vals, n, ctx->view, ctx->has_lo, ctx->has_hi,
+                                            head, inrun);
     err = cub::DeviceScan::ExclusiveSum(nullptr, need, head, kalt, (int)n, s);
     if (err != cudaSuccess) return err;
     if (need > tmp_bytes) return cudaErrorMemoryAllocation;
@@ -476,7 +502,7 @@ cudaError_t build_plan(nbk_ctx* ctx)
     ctx->n4 = cnt[1] + lastf[1];
     ctx->n8 = cnt[2] + lastf[2];
     ctx->nother = ns - ctx->n2 - ctx->n4 - ctx->n8;
-    if (ctx->nother != 0) return cudaErrorInvalidValue;  // single-rank box: m in {2, 4, 8}
+    if (ctx->nother != 0) return cudaErrorInvalidValue;  // box slabs: local m in {2, 4, 8}
     ctx->g2 = ctx->grp;
     ctx->g4 = ctx->g2 + ((2 * ctx->n2 + 3) & ~(int64_t)3);   // 16-byte aligned rows
     ctx->g8 = ctx->g4 + 4 * ctx->n4;

@@ -25,10 +25,12 @@ AX_LOCAL, AX_DSSUM, AX_MASK = 0, 1, 2
 PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32}
 
 # every symbol include/nbk.h declares
-SYMBOLS = ["nbk_workspace_bytes", "nbk_cg_setup", "nbk_load_arrays", "nbk_get_arrays",
-           "nbk_ax_apply", "nbk_dssum", "nbk_glsc3", "nbk_cg_solve", "nbk_cg_solve_host",
-           "nbk_get_solution", "nbk_solution_ptr", "nbk_set_profiling", "nbk_query",
-           "nbk_solve_launches", "nbk_last_error", "nbk_version", "nbk_destroy"]
+SYMBOLS = ["nbk_workspace_bytes", "nbk_partition", "nbk_nccl_unique_id", "nbk_cg_setup",
+           "nbk_load_arrays", "nbk_get_arrays", "nbk_ax_apply", "nbk_dssum", "nbk_glsc3",
+           "nbk_cg_solve", "nbk_cg_solve_host", "nbk_get_solution", "nbk_solution_ptr",
+           "nbk_set_profiling", "nbk_query", "nbk_solve_launches", "nbk_group_link",
+           "nbk_group_ax_apply", "nbk_group_dssum", "nbk_group_glsc3", "nbk_group_cg_solve",
+           "nbk_last_error", "nbk_version", "nbk_destroy"]
 
 
 class NbkError(RuntimeError):
@@ -45,14 +47,15 @@ class CMesh(ctypes.Structure):
 
 class CDist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("nccl_id", ctypes.c_void_p)]
 
 
 class CInfo(ctypes.Structure):
     _fields_ = [("n_local", ctypes.c_int64), ("n_global", ctypes.c_int64),
                 ("e_local", ctypes.c_int64), ("e_offset", ctypes.c_int64),
                 ("n_shared", ctypes.c_int64), ("n_copies", ctypes.c_int64),
-                ("N", ctypes.c_int32), ("has_fp32", ctypes.c_int32)]
+                ("N", ctypes.c_int32), ("has_fp32", ctypes.c_int32),
+                ("face_layer", ctypes.c_int64), ("face_nodes", ctypes.c_int64)]
 
 
 class CResult(ctypes.Structure):
@@ -77,6 +80,13 @@ def load() -> ctypes.CDLL:
     P = ctypes.POINTER
     sig = {
         "nbk_workspace_bytes": [P(CMesh), ctypes.c_int, P(CDist), P(ctypes.c_size_t)],
+        "nbk_partition": [P(CMesh), P(CDist), P(CInfo)],
+        "nbk_nccl_unique_id": [vp],
+        "nbk_group_link": [P(vp), i32],
+        "nbk_group_ax_apply": [P(vp), i32, P(vp), P(vp), i32, ctypes.c_int],
+        "nbk_group_dssum": [P(vp), i32, P(vp), i32, ctypes.c_int],
+        "nbk_group_glsc3": [P(vp), i32, P(vp), P(vp), ctypes.c_int, P(ctypes.c_double)],
+        "nbk_group_cg_solve": [P(vp), i32, i32, ctypes.c_int, vp, vp, P(CResult)],
         "nbk_cg_setup": [P(CMesh), ctypes.c_int, P(CDist), vp, ctypes.c_size_t, P(vp)],
         "nbk_load_arrays": [vp, vp, vp, vp],
         "nbk_get_arrays": [vp, vp, vp, vp],
@@ -140,28 +150,51 @@ class MeshSpec:
 
 def workspace_bytes(mesh: MeshSpec, precision: str = "fp32", nranks: int = 1, rank: int = 0) -> int:
     out = ctypes.c_size_t(0)
-    d = CDist(rank, nranks, 0, None)
+    d = CDist(rank, nranks, 0, None, None)
     _check(load().nbk_workspace_bytes(ctypes.byref(mesh.c()), PREC[precision], ctypes.byref(d),
                                       ctypes.byref(out)))
     return int(out.value)
 
 
-class Context:
-    """cg_setup(mesh, N, precision): a device-resident problem (one per GPU)."""
+def partition(mesh: MeshSpec, nranks: int = 1, rank: int = 0) -> dict:
+    """Slab partition of the mesh for one rank (host only; no device needed)."""
+    info = CInfo()
+    d = CDist(rank, nranks, 0, None, None)
+    _check(load().nbk_partition(ctypes.byref(mesh.c()), ctypes.byref(d), ctypes.byref(info)))
+    return {k: getattr(info, k) for k, _ in CInfo._fields_}
 
-    def __init__(self, mesh: MeshSpec, precision: str = "fp32", device: int = 0, stream=None):
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load().nbk_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """cg_setup(mesh, N, precision): a device-resident problem (one per GPU).
+
+    nranks > 1: this context owns z-slab `rank`.  With `nccl_id` (128 bytes from
+    nccl_unique_id() on rank 0) the set-up and every call are collective over
+    NCCL; without it the context is a virtual slab to be linked with Group."""
+
+    def __init__(self, mesh: MeshSpec, precision: str = "fp32", device: int = 0, stream=None,
+                 rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None):
         import torch
         self.torch = torch
         if not torch.cuda.is_available():
             raise NbkError(NBK_ECUDA, "no CUDA device: libnbk has no CPU fallback")
         self.lib = load()
         self.mesh = mesh
+        self.rank, self.nranks = rank, nranks
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
-        nbytes = workspace_bytes(mesh, precision)
+        nbytes = workspace_bytes(mesh, precision, nranks, rank)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self._ctx = ctypes.c_void_p(None)
-        d = CDist(0, 1, device, ctypes.c_void_p(self.stream.cuda_stream))
+        self._id = None if nccl_id is None else ctypes.create_string_buffer(bytes(nccl_id), 128)
+        d = CDist(rank, nranks, device, ctypes.c_void_p(self.stream.cuda_stream),
+                  None if self._id is None else ctypes.cast(self._id, ctypes.c_void_p))
         _check(self.lib.nbk_cg_setup(ctypes.byref(mesh.c()), PREC[precision], ctypes.byref(d),
                                      ctypes.c_void_p(self.workspace.data_ptr()), nbytes,
                                      ctypes.byref(self._ctx)))
@@ -271,8 +304,74 @@ class Context:
         return int(n.value)
 
 
-def cg_setup(mesh: MeshSpec, precision: str = "fp32", device: int = 0, stream=None) -> Context:
-    return Context(mesh, precision, device, stream)
+def cg_setup(mesh: MeshSpec, precision: str = "fp32", device: int = 0, stream=None,
+             rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None) -> Context:
+    return Context(mesh, precision, device, stream, rank, nranks, nccl_id)
+
+
+class Group:
+    """Virtual slabs: P contexts (rank r of P) of one mesh on one device and
+    stream, linked in process (nbk_group_link) and driven together; the same
+    kernels as NCCL mode run with faces / partials shared by pointer."""
+
+    def __init__(self, mesh: MeshSpec, P: int, precision: str = "fp32", device: int = 0,
+                 stream=None):
+        import torch
+        self.torch = torch
+        self.lib = load()
+        self.P = P
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
+        self.ctxs = [Context(mesh, precision, device, self.stream, rank=r, nranks=P)
+                     for r in range(P)]
+        self._arr = (ctypes.c_void_p * P)(*[c._ctx.value for c in self.ctxs])
+        _check(self.lib.nbk_group_link(self._arr, P), self.ctxs[0]._ctx)
+        self.n_global = self.ctxs[0].n_global
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()
+
+    def sync(self):
+        self.stream.synchronize()
+
+    def _ptrs(self, ts):
+        assert len(ts) == self.P
+        return (ctypes.c_void_p * self.P)(*[t.data_ptr() for t in ts])
+
+    def load_arrays(self, D, G_slabs, f_slabs):
+        for c, G, f in zip(self.ctxs, G_slabs, f_slabs):
+            c.load_arrays(D, G, f)
+
+    def ax_apply(self, us, ws, flags: int = AX_DSSUM | AX_MASK):
+        prec = Context._prec_of(us[0])
+        _check(self.lib.nbk_group_ax_apply(self._arr, self.P, self._ptrs(us), self._ptrs(ws),
+                                           flags, PREC[prec]), self.ctxs[0]._ctx)
+        return ws
+
+    def dssum(self, fs, apply_mask: bool = False):
+        prec = Context._prec_of(fs[0])
+        _check(self.lib.nbk_group_dssum(self._arr, self.P, self._ptrs(fs), int(apply_mask),
+                                        PREC[prec]), self.ctxs[0]._ctx)
+        return fs
+
+    def glsc3(self, a_s, b_s) -> float:
+        prec = Context._prec_of(a_s[0])
+        out = ctypes.c_double(0.0)
+        _check(self.lib.nbk_group_glsc3(self._arr, self.P, self._ptrs(a_s), self._ptrs(b_s),
+                                        PREC[prec], ctypes.byref(out)), self.ctxs[0]._ctx)
+        return float(out.value)
+
+    def cg_solve(self, niter: int, precision: str = "fp32", trace: bool = True):
+        hist = np.zeros(niter + 1)
+        tr = np.zeros((niter, 5)) if trace else None
+        res = CResult()
+        st = self.lib.nbk_group_cg_solve(self._arr, self.P, niter, PREC[precision], _ptr(hist),
+                                         _ptr(tr) if trace else None, ctypes.byref(res))
+        _check(st, self.ctxs[0]._ctx, ok=(NBK_OK, NBK_EDEFECT))
+        return hist, tr, {k: getattr(res, k) for k, _ in CResult._fields_}
+
+    def solution(self) -> np.ndarray:
+        return np.concatenate([c.solution() for c in self.ctxs], axis=0)
 
 
 def version() -> str:
