@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <new>
 #include <vector>
 
@@ -115,20 +116,52 @@ static cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only 
 #undef AXN
 }
 
+// Resident CTAs of a kernel on the whole device (SM count x occupancy), cached
+// per kernel: grids of the streaming kernels are sized to exactly one wave.
+static int resident_grid(const void* kern, int block, size_t smem)
+{
+    static std::map<const void*, int> cache;
+    auto it = cache.find(kern);
+    if (it != cache.end()) return it->second;
+    int dev = 0, sms = 148, nb = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, block, smem) != cudaSuccess || nb < 1) nb = 1;
+    int g = nb * sms;
+    if (g > NBK_VEC_GRID_MAX) g = NBK_VEC_GRID_MAX;
+    cache[kern] = g;
+    return g;
+}
+
+template <typename T, int N, int MODE>
+static cudaError_t launch_vec_n(const VecArgs<T>& a, cudaStream_t s, bool pdl)
+{
+    const int cap = resident_grid((const void*)k_vec<T, N, MODE>, 256, 0);
+    int64_t g = (a.n / 4 + 511) / 512;  // >= 2 chunks of 4 points per thread
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return launch_k(k_vec<T, N, MODE>, (unsigned)g, 256, 0, s, pdl, a);
+}
+
 template <typename T, int MODE>
 static cudaError_t launch_vec(const VecArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
-    const int g = vec_grid(a.n);
-#define VECN(n) launch_k(k_vec<T, n, MODE>, g, 256, 0, s, pdl, a)
+#define VECN(n) launch_vec_n<T, n, MODE>(a, s, pdl)
     NBK_SWITCH_N(a.mesh.N, VECN)
 #undef VECN
 }
 
 template <typename T, bool FUSED>
+static int dssum_grid_t(int ntiles)
+{
+    const int cap = resident_grid((const void*)k_dssum<T, FUSED>, 256, 0);
+    return ntiles < 1 ? 1 : (ntiles > cap ? cap : ntiles);
+}
+
+template <typename T, bool FUSED>
 static cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
-    const int g = vec_grid((a.n2 + a.n4 + a.n8 + a.nother + 1) / 2);
-    return launch_k(k_dssum<T, FUSED>, g, 256, 0, s, pdl, a);
+    return launch_k(k_dssum<T, FUSED>, dssum_grid_t<T, FUSED>(a.ntiles), 256, 0, s, pdl, a);
 }
 
 // ------------------------------------------------------------ NCCL (dlopen)
@@ -283,8 +316,7 @@ static DssumArgs<T> dssum_args(nbk_ctx* c, T* w)
     DssumArgs<T> d{};
     d.w = w;
     d.g2 = c->g2; d.g4 = c->g4; d.g8 = c->g8;
-    d.n2 = c->n2; d.n4 = c->n4; d.n8 = c->n8;
-    d.seg_off = c->seg_off; d.seg_idx = c->seg_idx; d.nother = c->nother;
+    d.toff = c->toff; d.ntiles = (int)c->ntiles;
     d.st = c->st; d.trace = c->trace; d.mesh = c->view; d.mask = 0; d.fin = 1;
     return d;
 }
@@ -338,8 +370,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         f.mask = mask;
         if (FUSED) {
             f.p = p[q];
-            f.nprev = ax_blocks_n<T>(c->E, c->N) +
-                      vec_grid((c->n2 + c->n4 + c->n8 + c->nother + 1) / 2);
+            f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED>((int)c->ntiles);
         }
         const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
         k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);
@@ -731,6 +762,7 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     c->seg_off = (int32_t*)(b + L.off_segoff);
     c->seg_idx = (int32_t*)(b + L.off_segidx);
     c->grp = (int32_t*)(b + L.off_grp);
+    c->toff = (int32_t*)(b + L.off_toff);
     if (c->has_lo || c->has_hi) {
         const size_t fb = 8 * (size_t)L.nlayer;
         c->send_lo = b + L.off_face;

@@ -45,6 +45,8 @@ struct nbk_ctx {
     int32_t *grp = nullptr;                               // group index storage
     int32_t *g2 = nullptr, *g4 = nullptr, *g8 = nullptr;  // segments grouped by multiplicity
     int64_t n2 = 0, n4 = 0, n8 = 0, nother = 0;
+    int32_t* toff = nullptr;              // dssum tiles: (ntiles + 1) x 3 offsets
+    int64_t ntiles = 0, tile_elems = 1;
     unsigned char* scratch = nullptr;  // set-up scratch (aliases the vector region)
     size_t scratch_bytes = 0;
 
@@ -70,7 +72,7 @@ namespace nbk {
 
 struct Layout {
     size_t off_state, off_D64, off_D32, off_hist, off_trace, off_parts, off_segoff, off_segidx, off_grp,
-        off_face, off_gather, off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
+        off_face, off_gather, off_toff, off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
     int64_t nlayer, nplane;
     int has_lo, has_hi;
     int64_t E, n, n_global, nseg, ncopies, nparts, e_offset;

@@ -393,8 +393,13 @@ __device__ __forceinline__ void fin_rtr(CgState* st, double rtr, double* hist, d
 // ---------------------------------------------------------------- K_B
 // The dssum plan groups the segments (unique shared nodes) by multiplicity
 // m in {2, 4, 8}: group m is a dense int32 array of m ascending local indices
-// per node, read with one vector load.  Segments of any other length (none
-// on a single-rank box) use the generic offset list.
+// per node (one vector load), each group ordered by the node's first copy.
+// The domain is cut into tiles of `te` consecutive elements; toff[3t + g] is
+// the first node of group g whose first copy lies in tile t or later.  A block
+// processes whole tiles -- all three groups of a tile back to back -- so the
+// sectors of w a tile touches (its own elements and the neighbours at +1,
+// +ex, +ex*ey) are re-used from L2 instead of being streamed from HBM once
+// per group.
 template <typename T>
 struct DssumArgs {
     T* w;
@@ -402,10 +407,8 @@ struct DssumArgs {
     const int32_t* g2;        // n2 x 2
     const int32_t* g4;        // n4 x 4
     const int32_t* g8;        // n8 x 8
-    int64_t n2, n4, n8;
-    const int32_t* seg_off;   // generic segments (nother)
-    const int32_t* seg_idx;
-    int64_t nother;
+    const int32_t* toff;      // (ntiles + 1) x 3 tile offsets into g2, g4, g8
+    int ntiles;
     dd* parts;                // fused: partials [0, nA) from K_A, [nA, nA+gridDim) here
     int nA;
     CgState* st;
@@ -425,42 +428,28 @@ __device__ __forceinline__ bool masked_local(const MeshView& m, int32_t L)
     return is_masked(m, ec, rem % N, (rem / N) % N, rem / (N * N));
 }
 
-// Sum the M copies (C4: ascending local index), write back, pap term.
-template <typename T, int M, bool FUSED>
-__device__ __forceinline__ void dssum_node(const DssumArgs<T>& a, const int32_t (&ix)[M], acc_t& acc)
+// Load the (ascending) local indices of node q of a tile (q counts the tile's
+// g2 nodes, then its g4, then its g8 nodes); returns the multiplicity.
+__device__ __forceinline__ int tile_seg_load(const int32_t* g2, const int32_t* g4, const int32_t* g8,
+                                             int s2, int n2, int s4, int n4, int s8, int q,
+                                             int32_t (&ix)[8])
 {
-    T v[M];
-#pragma unroll
-    for (int q = 0; q < M; ++q) v[q] = a.w[ix[q]];
-    T p0 = 0;
-    if constexpr (FUSED) p0 = a.p[ix[0]];
-    T sum = v[0];
-#pragma unroll
-    for (int q = 1; q < M; ++q) sum = add_t<T>(sum, v[q]);
-    if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[0])) sum = 0;
-#pragma unroll
-    for (int q = 0; q < M; ++q) a.w[ix[q]] = sum;
-    if constexpr (FUSED) acc.add(dot_term(sum, p0, 1.0));  // one term per node (m c = 1)
-}
-
-// Load the (ascending) local indices of segment s; returns its length m.
-template <typename T>
-__device__ __forceinline__ int seg_load(const DssumArgs<T>& a, int64_t s, int32_t (&ix)[8])
-{
-    const int64_t n24 = a.n2 + a.n4;
-    if (s < a.n2) {
-        const int2 q = reinterpret_cast<const int2*>(a.g2)[s];
-        ix[0] = q.x; ix[1] = q.y;
+    if (q < n2) {
+        const int2 v = reinterpret_cast<const int2*>(g2)[s2 + q];
+        ix[0] = v.x; ix[1] = v.y;
         return 2;
-    } else if (s < n24) {
-        const int4 q = reinterpret_cast<const int4*>(a.g4)[s - a.n2];
-        ix[0] = q.x; ix[1] = q.y; ix[2] = q.z; ix[3] = q.w;
+    }
+    q -= n2;
+    if (q < n4) {
+        const int4 v = reinterpret_cast<const int4*>(g4)[s4 + q];
+        ix[0] = v.x; ix[1] = v.y; ix[2] = v.z; ix[3] = v.w;
         return 4;
     }
-    const int4* g = reinterpret_cast<const int4*>(a.g8) + 2 * (s - n24);
-    const int4 q0 = g[0], q1 = g[1];
-    ix[0] = q0.x; ix[1] = q0.y; ix[2] = q0.z; ix[3] = q0.w;
-    ix[4] = q1.x; ix[5] = q1.y; ix[6] = q1.z; ix[7] = q1.w;
+    q -= n4;
+    const int4* g = reinterpret_cast<const int4*>(g8) + 2 * (int64_t)(s8 + q);
+    const int4 v0 = g[0], v1 = g[1];
+    ix[0] = v0.x; ix[1] = v0.y; ix[2] = v0.z; ix[3] = v0.w;
+    ix[4] = v1.x; ix[5] = v1.y; ix[6] = v1.z; ix[7] = v1.w;
     return 8;
 }
 
@@ -469,47 +458,42 @@ __global__ void __launch_bounds__(256) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
     pdl_wait();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t tot = a.n2 + a.n4 + a.n8;
-    // two segments per thread per step, all loads of both issued before use
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < tot; s += 2 * stride) {
-        const int64_t s2 = s + stride;
-        int32_t ix[2][8];
-        int m[2];
-        m[0] = seg_load(a, s, ix[0]);
-        m[1] = s2 < tot ? seg_load(a, s2, ix[1]) : 0;
-        T v[2][8];
-        T p0[2] = {0, 0};
+    for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const int s2 = __ldg(&a.toff[3 * t]), s4 = __ldg(&a.toff[3 * t + 1]), s8 = __ldg(&a.toff[3 * t + 2]);
+        const int n2 = __ldg(&a.toff[3 * t + 3]) - s2, n4 = __ldg(&a.toff[3 * t + 4]) - s4;
+        const int n8 = __ldg(&a.toff[3 * t + 5]) - s8;
+        const int tot = n2 + n4 + n8;
+        // two nodes per thread per step, all loads of both issued before use
+        for (int q = threadIdx.x; q < tot; q += 2 * blockDim.x) {
+            const int q2 = q + blockDim.x;
+            int32_t ix[2][8];
+            int m[2];
+            m[0] = tile_seg_load(a.g2, a.g4, a.g8, s2, n2, s4, n4, s8, q, ix[0]);
+            m[1] = q2 < tot ? tile_seg_load(a.g2, a.g4, a.g8, s2, n2, s4, n4, s8, q2, ix[1]) : 0;
+            T v[2][8];
+            T p0[2] = {0, 0};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (q < m[h]) v[h][q] = a.w[ix[h][q]];
-            if constexpr (FUSED)
-                if (m[h]) p0[h] = a.p[ix[h][0]];
+                for (int c = 0; c < 8; ++c)
+                    if (c < m[h]) v[h][c] = a.w[ix[h][c]];
+                if constexpr (FUSED)
+                    if (m[h]) p0[h] = a.p[ix[h][0]];
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!m[h]) continue;
+                T sum = v[h][0];                          // C4: ascending local index
+#pragma unroll
+                for (int c = 1; c < 8; ++c)
+                    if (c < m[h]) sum = add_t<T>(sum, v[h][c]);
+                if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[h][0])) sum = 0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < m[h]) a.w[ix[h][c]] = sum;
+                if constexpr (FUSED) acc.add(dot_term(sum, p0[h], 1.0));  // one term per node
+            }
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (!m[h]) continue;
-            T sum = v[h][0];                          // C4: ascending local index
-#pragma unroll
-            for (int q = 1; q < 8; ++q)
-                if (q < m[h]) sum = add_t<T>(sum, v[h][q]);
-            if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[h][0])) sum = 0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (q < m[h]) a.w[ix[h][q]] = sum;
-            if constexpr (FUSED) acc.add(dot_term(sum, p0[h], 1.0));  // one term per node
-        }
-    }
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nother; s += stride) {
-        const int32_t o0 = a.seg_off[s], o1 = a.seg_off[s + 1];
-        const int32_t L0 = a.seg_idx[o0];
-        T sum = a.w[L0];
-        for (int32_t q = o0 + 1; q < o1; ++q) sum = add_t<T>(sum, a.w[a.seg_idx[q]]);
-        if (!FUSED && a.mask && masked_local<T>(a.mesh, L0)) sum = 0;
-        for (int32_t q = o0; q < o1; ++q) a.w[a.seg_idx[q]] = sum;
-        if constexpr (FUSED) acc.add(dot_term(sum, a.p[L0], 1.0));
     }
     pdl_launch_dependents();
     if constexpr (FUSED) {
@@ -557,10 +541,18 @@ struct VecT {
     T v[V];
     __device__ __forceinline__ void load(const T* p)
     {
-        if constexpr (V * sizeof(T) % 16 == 0) {
+        if constexpr (sizeof(T) == 4 && V % 4 == 0) {
 #pragma unroll
-            for (int q = 0; q < V * (int)sizeof(T) / 16; ++q)
-                reinterpret_cast<float4*>(v)[q] = reinterpret_cast<const float4*>(p)[q];
+            for (int q = 0; q < V / 4; ++q) {
+                const float4 f = reinterpret_cast<const float4*>(p)[q];
+                v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+            }
+        } else if constexpr (sizeof(T) == 8 && V % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < V / 2; ++q) {
+                const double2 d = reinterpret_cast<const double2*>(p)[q];
+                v[2 * q] = d.x; v[2 * q + 1] = d.y;
+            }
         } else {
 #pragma unroll
             for (int q = 0; q < V; ++q) v[q] = p[q];
@@ -568,10 +560,14 @@ struct VecT {
     }
     __device__ __forceinline__ void store(T* p) const
     {
-        if constexpr (V * sizeof(T) % 16 == 0) {
+        if constexpr (sizeof(T) == 4 && V % 4 == 0) {
 #pragma unroll
-            for (int q = 0; q < V * (int)sizeof(T) / 16; ++q)
-                reinterpret_cast<float4*>(p)[q] = reinterpret_cast<const float4*>(v)[q];
+            for (int q = 0; q < V / 4; ++q)
+                reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else if constexpr (sizeof(T) == 8 && V % 2 == 0) {
+#pragma unroll
+            for (int q = 0; q < V / 2; ++q)
+                reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
         } else {
 #pragma unroll
             for (int q = 0; q < V; ++q) p[q] = v[q];
@@ -579,13 +575,38 @@ struct VecT {
     }
 };
 
+// c = 1/m (R8) of the V consecutive points L..L+V-1 (one element, N3 % V == 0),
+// stepping (i, j, k) incrementally from one division.
+template <int N, int V>
+__device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, double (&c)[V])
+{
+    constexpr int N2 = N * N, N3 = N * N * N, n1 = N - 1;
+    const uint32_t e = (uint32_t)(L / N3);
+    const int rem = (int)(L - (int64_t)e * N3);
+    const ElemCoord ec = elem_coord(m, e);
+    int i = rem % N, j = (rem / N) % N, k = rem / N2;
+    const bool xl = ec.ax > 0, xh = ec.ax < m.ex - 1, yl = ec.ay > 0, yh = ec.ay < m.ey - 1;
+    const bool zl = ec.azg > 0, zh = ec.azg < m.ezg - 1;
+    int myz = (((j == 0 && yl) || (j == n1 && yh)) ? 2 : 1) * (((k == 0 && zl) || (k == n1 && zh)) ? 2 : 1);
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+        const int mx = ((i == 0 && xl) || (i == n1 && xh)) ? 2 : 1;
+        c[t] = inv_mult(mx * myz);
+        if (t + 1 < V && ++i == N) {
+            i = 0;
+            if (++j == N) { j = 0; ++k; }
+            myz = (((j == 0 && yl) || (j == n1 && yh)) ? 2 : 1) * (((k == 0 && zl) || (k == n1 && zh)) ? 2 : 1);
+        }
+    }
+}
+
 // Vector kernel over all local points: chunks of V = 4 consecutive points
 // (N^3 % 4 == 0) in one element, 16-byte loads/stores; structural c = 1/m.
 template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 {
-    constexpr int N2 = N * N, N3 = N * N * N;
-    constexpr int V = (N3 % 4 == 0) ? 4 : 1;
+    constexpr int N3 = N * N * N;
+    constexpr int V = (N3 % 4 == 0) ? 4 : ((N3 % 2 == 0) ? 2 : 1);
     acc_t acc;
     T am = 0;
     pdl_wait();
@@ -594,70 +615,65 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
     }
     const int64_t nch = a.n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nch; q += stride) {
-        const int64_t L = q * V;
-        const uint32_t e = (uint32_t)(L / N3);
-        const int rem = (int)(L - (int64_t)e * N3);
-        const ElemCoord ec = elem_coord(a.mesh, e);
-        double c[V];
-        if constexpr (N % V == 0) {
-            // the chunk lies in one (j, k) row: c = c_yz * c_x(i)
-            const int i0 = rem % N, j = (rem / N) % N, k = rem / N2;
-            const int n1 = N - 1;
-            const int myz = (((j == 0 && ec.ay > 0) || (j == n1 && ec.ay < a.mesh.ey - 1)) ? 2 : 1) *
-                            (((k == 0 && ec.azg > 0) || (k == n1 && ec.azg < a.mesh.ezg - 1)) ? 2 : 1);
+    // two chunks of V points per thread per step; every load of both is issued
+    // before any use (more bytes in flight per thread)
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nch; q0 += 2 * stride) {
+        const bool two = q0 + stride < nch;
+        VecT<T, V> A[2], B[2];
+        VecT<double, V> F[2];
 #pragma unroll
-            for (int t = 0; t < V; ++t) {
-                const int i = i0 + t;
-                const int mx = ((i == 0 && ec.ax > 0) || (i == n1 && ec.ax < a.mesh.ex - 1)) ? 2 : 1;
-                c[t] = inv_mult(mx * myz);
-            }
-        } else {
-#pragma unroll
-            for (int t = 0; t < V; ++t) {
-                const int pt = rem + t;
-                c[t] = inv_mult(multiplicity(a.mesh, ec, pt % N, (pt / N) % N, pt / N2));
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int64_t L = (q0 + h * stride) * V;
+            if constexpr (MODE == VEC_INIT) {
+                F[h].load(a.f + L);
+            } else if constexpr (MODE == VEC_RUPD) {
+                A[h].load(a.w + L);
+                B[h].load(a.r + L);
+            } else if constexpr (MODE == VEC_TRUE) {
+                A[h].load(a.w + L);
+                F[h].load(a.f + L);
+            } else {
+                A[h].load(a.a + L);
+                B[h].load(a.b + L);
             }
         }
-        if constexpr (MODE == VEC_INIT) {
-            VecT<double, V> f;
-            f.load(a.f + L);
-            VecT<T, V> r, z;
 #pragma unroll
-            for (int t = 0; t < V; ++t) {
-                r.v[t] = (T)f.v[t];  // C11: f32 = RN32(f64)
-                z.v[t] = 0;
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int64_t L = (q0 + h * stride) * V;
+            double c[V];
+            chunk_weights<N, V>(a.mesh, L, c);
+            if constexpr (MODE == VEC_INIT) {
+                VecT<T, V> r, z;
+#pragma unroll
+                for (int t = 0; t < V; ++t) {
+                    r.v[t] = (T)F[h].v[t];  // C11: f32 = RN32(f64)
+                    z.v[t] = 0;
+                }
+                r.store(a.r + L);
+                z.store(a.x + L);
+                z.store(a.p + L);
+#pragma unroll
+                for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+            } else if constexpr (MODE == VEC_RUPD) {
+                VecT<T, V> r;
+#pragma unroll
+                for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, A[h].v[t], B[h].v[t]);  // C8
+                r.store(a.r + L);
+#pragma unroll
+                for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+            } else if constexpr (MODE == VEC_TRUE) {
+                VecT<T, V> r;
+#pragma unroll
+                for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, A[h].v[t], (T)F[h].v[t]);  // C12
+                r.store(a.r + L);
+#pragma unroll
+                for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+            } else {
+#pragma unroll
+                for (int t = 0; t < V; ++t) acc.add(dot_term(A[h].v[t], B[h].v[t], c[t]));
             }
-            r.store(a.r + L);
-            z.store(a.x + L);
-            z.store(a.p + L);
-#pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
-        } else if constexpr (MODE == VEC_RUPD) {
-            VecT<T, V> w, r;
-            w.load(a.w + L);
-            r.load(a.r + L);
-#pragma unroll
-            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, w.v[t], r.v[t]);  // C8
-            r.store(a.r + L);
-#pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
-        } else if constexpr (MODE == VEC_TRUE) {
-            VecT<T, V> w, r;
-            VecT<double, V> f;
-            w.load(a.w + L);
-            f.load(a.f + L);
-#pragma unroll
-            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, w.v[t], (T)f.v[t]);  // C12
-            r.store(a.r + L);
-#pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
-        } else {
-            VecT<T, V> x, y;
-            x.load(a.a + L);
-            y.load(a.b + L);
-#pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(x.v[t], y.v[t], c[t]));
         }
     }
     pdl_launch_dependents();

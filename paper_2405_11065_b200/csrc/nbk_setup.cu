@@ -122,6 +122,7 @@ Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
     L.off_grp = take(4 * (size_t)L.ncopies + 64);
     L.off_face = take(nb ? 4 * 8 * (size_t)L.nlayer : 8);
     L.off_gather = take(sizeof(dd) * NBK_MAX_RANKS);
+    L.off_toff = take(4 * 3 * ((size_t)L.E + 2));
     L.off_G64 = take(8 * 6 * (size_t)L.n);
     L.off_f64 = take(8 * (size_t)L.n);
     L.scratch_need = plan_scratch_bytes(L.n, L.nseg);
@@ -393,6 +394,31 @@ __global__ void __launch_bounds__(256) k_group_scatter(const int32_t* off, const
     }
 }
 
+// toff[3t + g] = first node of group g (rows of m = 2, 4, 8 indices) whose
+// first copy lies at local index >= t * te * N^3 (binary search; groups are
+// ordered by first copy).
+__global__ void __launch_bounds__(256) k_tile_offsets(const int32_t* g2, const int32_t* g4,
+                                                      const int32_t* g8, int64_t n2, int64_t n4,
+                                                      int64_t n8, int64_t ntiles, int64_t te,
+                                                      int64_t N3, int32_t* toff)
+{
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < 3 * (ntiles + 1);
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = q / 3;
+        const int g = (int)(q - 3 * t);
+        const int32_t* arr = g == 0 ? g2 : (g == 1 ? g4 : g8);
+        const int m = g == 0 ? 2 : (g == 1 ? 4 : 8);
+        const int64_t cnt = g == 0 ? n2 : (g == 1 ? n4 : n8);
+        const int64_t key = t * te * N3;
+        int64_t lo = 0, hi = cnt;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if ((int64_t)arr[mid * m] < key) lo = mid + 1; else hi = mid;
+        }
+        toff[q] = (int32_t)lo;
+    }
+}
+
 static int grid_for(int64_t n, int cap = 148 * 16)
 {
     int64_t g = (n + 255) / 256;
@@ -455,6 +481,7 @@ cudaError_t build_plan(nbk_ctx* ctx)
     const int64_t ns = ctx->nseg;
     ctx->n2 = ctx->n4 = ctx->n8 = ctx->nother = 0;
     ctx->g2 = ctx->g4 = ctx->g8 = ctx->grp;
+    ctx->ntiles = 0;
     if (ns == 0) return cudaGetLastError();
     o = 0;
     uint32_t* f2 = (uint32_t*)take(4 * ns);
@@ -508,6 +535,16 @@ cudaError_t build_plan(nbk_ctx* ctx)
     ctx->g8 = ctx->g4 + 4 * ctx->n4;
     k_group_scatter<<<grid_for(ns), 256, 0, s>>>(ctx->seg_off, ctx->seg_idx, order, ns, f2, f4, f8, q2,
                                                  q4, q8, ctx->g2, ctx->g4, ctx->g8);
+    // dssum tiles: ~1024 nodes per tile (a few per thread of a 256-thread block)
+    const int64_t N3 = (int64_t)ctx->N * ctx->N * ctx->N;
+    const int64_t per_elem = (ns + ctx->E - 1) / ctx->E;
+    int64_t te = (1024 + per_elem - 1) / per_elem;
+    if (te < 1) te = 1;
+    ctx->tile_elems = te;
+    ctx->ntiles = (ctx->E + te - 1) / te;
+    k_tile_offsets<<<grid_for(3 * (ctx->ntiles + 1)), 256, 0, s>>>(ctx->g2, ctx->g4, ctx->g8, ctx->n2,
+                                                                 ctx->n4, ctx->n8, ctx->ntiles, te, N3,
+                                                                 ctx->toff);
     err = cudaStreamSynchronize(s);
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
