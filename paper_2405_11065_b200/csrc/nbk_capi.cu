@@ -553,6 +553,7 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
     AxArgs<float> a32{};
     a32.mesh = c->view;
     cudaError_t e;
+
     if ((e = launch_ax<double, false>(a64, c->stream, true)) != cudaSuccess) return e;
     if ((e = launch_ax<double, true>(a64, c->stream, true)) != cudaSuccess) return e;
     if ((e = launch_ax<float, false>(a32, c->stream, true)) != cudaSuccess) return e;

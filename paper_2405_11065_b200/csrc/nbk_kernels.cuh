@@ -453,17 +453,17 @@ __device__ __forceinline__ int tile_seg_load(const int32_t* g2, const int32_t* g
     return 8;
 }
 
+// The tiles of this block (grid-stride), node by node (all multiplicities of
+// a tile in one loop, two nodes per thread per step, every load of both
+// issued before use; p by the read-only path).
 template <typename T, bool FUSED>
-__global__ void __launch_bounds__(256) k_dssum(DssumArgs<T> a)
+__device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
 {
-    acc_t acc;
-    pdl_wait();
     for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         const int s2 = __ldg(&a.toff[3 * t]), s4 = __ldg(&a.toff[3 * t + 1]), s8 = __ldg(&a.toff[3 * t + 2]);
         const int n2 = __ldg(&a.toff[3 * t + 3]) - s2, n4 = __ldg(&a.toff[3 * t + 4]) - s4;
         const int n8 = __ldg(&a.toff[3 * t + 5]) - s8;
         const int tot = n2 + n4 + n8;
-        // two nodes per thread per step, all loads of both issued before use
         for (int q = threadIdx.x; q < tot; q += 2 * blockDim.x) {
             const int q2 = q + blockDim.x;
             int32_t ix[2][8];
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(256) k_dssum(DssumArgs<T> a)
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) v[h][c] = a.w[ix[h][c]];
                 if constexpr (FUSED)
-                    if (m[h]) p0[h] = a.p[ix[h][0]];
+                    if (m[h]) p0[h] = __ldg(a.p + ix[h][0]);
             }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -495,6 +495,14 @@ __global__ void __launch_bounds__(256) k_dssum(DssumArgs<T> a)
             }
         }
     }
+}
+
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_dssum(DssumArgs<T> a)
+{
+    acc_t acc;
+    pdl_wait();
+    dssum_tiles<T, FUSED>(a, acc);
     pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
@@ -544,13 +552,15 @@ struct VecT {
         if constexpr (sizeof(T) == 4 && V % 4 == 0) {
 #pragma unroll
             for (int q = 0; q < V / 4; ++q) {
-                const float4 f = reinterpret_cast<const float4*>(p)[q];
+                const float4* a = reinterpret_cast<const float4*>(p) + q;
+                const float4 f = *a;
                 v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
             }
         } else if constexpr (sizeof(T) == 8 && V % 2 == 0) {
 #pragma unroll
             for (int q = 0; q < V / 2; ++q) {
-                const double2 d = reinterpret_cast<const double2*>(p)[q];
+                const double2* a = reinterpret_cast<const double2*>(p) + q;
+                const double2 d = *a;
                 v[2 * q] = d.x; v[2 * q + 1] = d.y;
             }
         } else {
@@ -588,6 +598,15 @@ __device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, doub
     const bool xl = ec.ax > 0, xh = ec.ax < m.ex - 1, yl = ec.ay > 0, yh = ec.ay < m.ey - 1;
     const bool zl = ec.azg > 0, zh = ec.azg < m.ezg - 1;
     int myz = (((j == 0 && yl) || (j == n1 && yh)) ? 2 : 1) * (((k == 0 && zl) || (k == n1 && zh)) ? 2 : 1);
+    if constexpr (N % V == 0) {  // the chunk lies in one (j, k) row
+#pragma unroll
+        for (int t = 0; t < V; ++t) {
+            const int ii = i + t;
+            const int mx = ((ii == 0 && xl) || (ii == n1 && xh)) ? 2 : 1;
+            c[t] = inv_mult(mx * myz);
+        }
+        return;
+    }
 #pragma unroll
     for (int t = 0; t < V; ++t) {
         const int mx = ((i == 0 && xl) || (i == n1 && xh)) ? 2 : 1;
@@ -602,80 +621,105 @@ __device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, doub
 
 // Vector kernel over all local points: chunks of V = 4 consecutive points
 // (N^3 % 4 == 0) in one element, 16-byte loads/stores; structural c = 1/m.
+// Per-chunk loads and arithmetic of each mode (split so that the loads of two
+// chunks can be issued before either is used).
+template <typename T, int V, int MODE>
+struct VecChunk {
+    VecT<T, V> A, B;
+    VecT<double, V> F;
+    __device__ __forceinline__ void load(const VecArgs<T>& a, int64_t L)
+    {
+        if constexpr (MODE == VEC_INIT) {
+            F.load(a.f + L);
+        } else if constexpr (MODE == VEC_RUPD) {
+            A.load(a.w + L);
+            B.load(a.r + L);
+        } else if constexpr (MODE == VEC_TRUE) {
+            A.load(a.w + L);
+            F.load(a.f + L);
+        } else {
+            A.load(a.a + L);
+            B.load(a.b + L);
+        }
+    }
+    __device__ __forceinline__ void run(const VecArgs<T>& a, int64_t L, const double (&c)[V], T am,
+                                        acc_t& acc)
+    {
+        if constexpr (MODE == VEC_INIT) {
+            VecT<T, V> r, z;
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                r.v[t] = (T)F.v[t];  // C11: f32 = RN32(f64)
+                z.v[t] = 0;
+            }
+            r.store(a.r + L);
+            z.store(a.x + L);
+            z.store(a.p + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+        } else if constexpr (MODE == VEC_RUPD) {
+            VecT<T, V> r;
+#pragma unroll
+            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, A.v[t], B.v[t]);  // C8
+            r.store(a.r + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+        } else if constexpr (MODE == VEC_TRUE) {
+            VecT<T, V> r;
+#pragma unroll
+            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, A.v[t], (T)F.v[t]);  // C12
+            r.store(a.r + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+        } else {
+#pragma unroll
+            for (int t = 0; t < V; ++t) acc.add(dot_term(A.v[t], B.v[t], c[t]));
+        }
+    }
+};
+
+// All chunks of this block (grid-stride).
 template <typename T, int N, int MODE>
-__global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
+__device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc)
 {
     constexpr int N3 = N * N * N;
     constexpr int V = (N3 % 4 == 0) ? 4 : ((N3 % 2 == 0) ? 2 : 1);
+    const int64_t nch = a.n / V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // two chunks of V points per thread per step; every load of both is issued
+    // before any use (more bytes in flight per thread)
+    for (; q0 + stride < nch; q0 += 2 * stride) {
+        VecChunk<T, V, MODE> C0, C1;
+        const int64_t L0 = q0 * V, L1 = (q0 + stride) * V;
+        C0.load(a, L0);
+        C1.load(a, L1);
+        double c[V];
+        chunk_weights<N, V>(a.mesh, L0, c);
+        C0.run(a, L0, c, am, acc);
+        chunk_weights<N, V>(a.mesh, L1, c);
+        C1.run(a, L1, c, am, acc);
+    }
+    if (q0 < nch) {
+        VecChunk<T, V, MODE> C0;
+        const int64_t L0 = q0 * V;
+        C0.load(a, L0);
+        double c[V];
+        chunk_weights<N, V>(a.mesh, L0, c);
+        C0.run(a, L0, c, am, acc);
+    }
+}
+
+template <typename T, int N, int MODE>
+__global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
+{
     acc_t acc;
     T am = 0;
     pdl_wait();
     if constexpr (MODE == VEC_RUPD) {
         if constexpr (sizeof(T) == 8) am = (T)a.st->alpham; else am = (T)a.st->alpham32;
     }
-    const int64_t nch = a.n / V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // two chunks of V points per thread per step; every load of both is issued
-    // before any use (more bytes in flight per thread)
-    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nch; q0 += 2 * stride) {
-        const bool two = q0 + stride < nch;
-        VecT<T, V> A[2], B[2];
-        VecT<double, V> F[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !two) break;
-            const int64_t L = (q0 + h * stride) * V;
-            if constexpr (MODE == VEC_INIT) {
-                F[h].load(a.f + L);
-            } else if constexpr (MODE == VEC_RUPD) {
-                A[h].load(a.w + L);
-                B[h].load(a.r + L);
-            } else if constexpr (MODE == VEC_TRUE) {
-                A[h].load(a.w + L);
-                F[h].load(a.f + L);
-            } else {
-                A[h].load(a.a + L);
-                B[h].load(a.b + L);
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !two) break;
-            const int64_t L = (q0 + h * stride) * V;
-            double c[V];
-            chunk_weights<N, V>(a.mesh, L, c);
-            if constexpr (MODE == VEC_INIT) {
-                VecT<T, V> r, z;
-#pragma unroll
-                for (int t = 0; t < V; ++t) {
-                    r.v[t] = (T)F[h].v[t];  // C11: f32 = RN32(f64)
-                    z.v[t] = 0;
-                }
-                r.store(a.r + L);
-                z.store(a.x + L);
-                z.store(a.p + L);
-#pragma unroll
-                for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
-            } else if constexpr (MODE == VEC_RUPD) {
-                VecT<T, V> r;
-#pragma unroll
-                for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, A[h].v[t], B[h].v[t]);  // C8
-                r.store(a.r + L);
-#pragma unroll
-                for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
-            } else if constexpr (MODE == VEC_TRUE) {
-                VecT<T, V> r;
-#pragma unroll
-                for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, A[h].v[t], (T)F[h].v[t]);  // C12
-                r.store(a.r + L);
-#pragma unroll
-                for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
-            } else {
-#pragma unroll
-                for (int t = 0; t < V; ++t) acc.add(dot_term(A[h].v[t], B[h].v[t], c[t]));
-            }
-        }
-    }
+    vec_loop<T, N, MODE>(a, am, acc);
     pdl_launch_dependents();
     dd v = block_reduce_dd(acc.get());
     if (publish_and_check_last(a.parts, blockIdx.x, v, &a.st->cnt[1], gridDim.x)) {

@@ -15,6 +15,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "nbk_internal.h"
@@ -535,10 +536,12 @@ cudaError_t build_plan(nbk_ctx* ctx)
     ctx->g8 = ctx->g4 + 4 * ctx->n4;
     k_group_scatter<<<grid_for(ns), 256, 0, s>>>(ctx->seg_off, ctx->seg_idx, order, ns, f2, f4, f8, q2,
                                                  q4, q8, ctx->g2, ctx->g4, ctx->g8);
-    // dssum tiles: ~1024 nodes per tile (a few per thread of a 256-thread block)
+    // dssum tiles: ~tile_nodes nodes per tile (several per thread of a 256-thread block)
     const int64_t N3 = (int64_t)ctx->N * ctx->N * ctx->N;
     const int64_t per_elem = (ns + ctx->E - 1) / ctx->E;
-    int64_t te = (1024 + per_elem - 1) / per_elem;
+    int64_t tile_nodes = 1024;
+    if (const char* env = getenv("NBK_DSSUM_TILE_NODES")) tile_nodes = atol(env) > 0 ? atol(env) : tile_nodes;
+    int64_t te = (tile_nodes + per_elem - 1) / per_elem;
     if (te < 1) te = 1;
     ctx->tile_elems = te;
     ctx->ntiles = (ctx->E + te - 1) / te;
