@@ -341,7 +341,7 @@ static dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - NBK_VEC_GRID_MA
 // k_fin (rank-ordered combination, alpha).
 template <typename T, bool FUSED>
 static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std::vector<const T*>& p,
-                              int mask, bool pdl, std::string& err)
+                              int mask, bool pdl, std::string& err, int rev = 0)
 {
     cudaError_t e;
     const cudaStream_t s = t.s;
@@ -349,6 +349,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         nbk_ctx* c = t.m[q];
         DssumArgs<T> d = dssum_args<T>(c, w[q]);
         d.mask = mask;
+        d.rev = rev;
         if (FUSED) {
             d.p = p[q];
             d.parts = c->parts;
@@ -463,6 +464,8 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
     if ((e = vec_team<T, VEC_INIT>(t, vi, false, err)) != cudaSuccess) return e;
     launches += (int64_t)P * (1 + per_fin);
 
+    // sweep directions alternate kernel by kernel: K_A f, K_B b, K_C f, K_A b, ...
+    int rev = 0;
     for (int k = 1; k <= niter; ++k) {
         const bool prof = g && profiling && P == 1;
         if (prof) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1)], s, cudaEventRecordExternal);
@@ -472,11 +475,14 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             AxArgs<T> aa = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
                                 : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
             aa.u = nullptr; aa.w = w[q]; aa.p = p[q]; aa.r = r[q]; aa.x = x[q]; aa.mask = 1;
+            aa.rev = rev;
             if ((e = launch_ax<T, true>(aa, s, false, pdl)) != cudaSuccess) return e;
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err)) != cudaSuccess) return e;
+        if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err, !rev)) != cudaSuccess) return e;
+        for (size_t q = 0; q < P; ++q) vr[q].rev = rev;
         if ((e = vec_team<T, VEC_RUPD>(t, vr, pdl, err)) != cudaSuccess) return e;
+        rev = !rev;
         launches += (int64_t)P * (3 + nface + 2 * per_fin);
     }
     for (size_t q = 0; q < P; ++q) {

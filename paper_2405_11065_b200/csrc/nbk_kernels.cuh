@@ -133,6 +133,7 @@ struct AxArgs {
     dd* parts;         // fused: pap partial per block
     MeshView mesh;
     int mask;          // assign +0 to Dirichlet points of w
+    int rev;           // sweep the element tiles in reverse order (L2 reuse, see k_vec)
 };
 
 // ---------------------------------------------------------------- K_A
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     const int tid = threadIdx.x;
     const int el = tid / N2, ij = tid - el * N2;
     const int i = ij % N, j = ij / N;
-    const int64_t e0 = (int64_t)blockIdx.x * EPB;
+    const int64_t e0 = (int64_t)(a.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * EPB;
     const int64_t e = e0 + el;
     const int nel = (int)((a.mesh.E - e0) < EPB ? (a.mesh.E - e0) : EPB);
     const bool valid = el < nel;
@@ -415,6 +416,7 @@ struct DssumArgs {
     double* trace;            // fused: per-iteration trace (niter*5)
     int mask;                 // standalone: assign +0 to masked shared nodes
     int fin;                  // fused: 1 = last block forms alpha (1 rank); 0 = publish only
+    int rev;                  // visit the tiles in reverse order
     MeshView mesh;
 };
 
@@ -459,7 +461,8 @@ __device__ __forceinline__ int tile_seg_load(const int32_t* g2, const int32_t* g
 template <typename T, bool FUSED>
 __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
 {
-    for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x) {
+        const int t = a.rev ? a.ntiles - 1 - i : i;
         const int s2 = __ldg(&a.toff[3 * t]), s4 = __ldg(&a.toff[3 * t + 1]), s8 = __ldg(&a.toff[3 * t + 2]);
         const int n2 = __ldg(&a.toff[3 * t + 3]) - s2, n4 = __ldg(&a.toff[3 * t + 4]) - s4;
         const int n8 = __ldg(&a.toff[3 * t + 5]) - s8;
@@ -540,6 +543,7 @@ struct VecArgs {
     double* hist;
     double* trace;
     dd* slot;           // multi-rank: this rank's reduced partial (NULL: finalise here)
+    int rev;            // visit the chunks in reverse order
     MeshView mesh;
 };
 
@@ -678,7 +682,10 @@ struct VecChunk {
     }
 };
 
-// All chunks of this block (grid-stride).
+// All chunks of this block (grid-stride).  The CG loop alternates the sweep
+// direction from kernel to kernel (K_A forward, K_B backward, K_C forward, next
+// K_A backward, ...): each kernel starts where its predecessor ended, on the
+// data still resident in the 126 MB L2.
 template <typename T, int N, int MODE>
 __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc)
 {
@@ -691,7 +698,8 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc)
     // before any use (more bytes in flight per thread)
     for (; q0 + stride < nch; q0 += 2 * stride) {
         VecChunk<T, V, MODE> C0, C1;
-        const int64_t L0 = q0 * V, L1 = (q0 + stride) * V;
+        const int64_t c0 = a.rev ? nch - 1 - q0 : q0, c1 = a.rev ? nch - 1 - (q0 + stride) : q0 + stride;
+        const int64_t L0 = c0 * V, L1 = c1 * V;
         C0.load(a, L0);
         C1.load(a, L1);
         double c[V];
@@ -702,7 +710,7 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc)
     }
     if (q0 < nch) {
         VecChunk<T, V, MODE> C0;
-        const int64_t L0 = q0 * V;
+        const int64_t L0 = (a.rev ? nch - 1 - q0 : q0) * V;
         C0.load(a, L0);
         double c[V];
         chunk_weights<N, V>(a.mesh, L0, c);

@@ -43,8 +43,13 @@ METRICS = [
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """Header, units and rows of an ncu raw page: from a .ncu-rep (via ncu -i)
+    or from the CSV `ncu -i REP --page raw --csv` wrote on the GPU box."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
@@ -67,6 +72,7 @@ def main():
     ap.add_argument("--rep", action="append", default=[], help="CFG:PREC:path.ncu-rep")
     ap.add_argument("--launches", action="append", default=[], help="CFG:path.csv")
     ap.add_argument("--note", default="")
+    ap.add_argument("--fresh", action="store_true", help="overwrite profiles/<round>_ncu.md")
     a = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     md = [f"# ncu summaries, round {a.round}", ""]
@@ -110,7 +116,7 @@ def main():
             md.append(f"| {c} | {v[1] / c / 1e3:.2f} us ({100 * v[1] / tot:.1f}% of listed) | "
                       f"{v[2] / c / 1e6:.2f} MB | {v[3] / c / 1e6:.2f} MB | `{n}` |")
         md.append("")
-    with open(os.path.join(ROOT, "profiles", f"{a.round}_ncu.md"), "a") as fh:
+    with open(os.path.join(ROOT, "profiles", f"{a.round}_ncu.md"), "w" if a.fresh else "a") as fh:
         fh.write("\n".join(md) + "\n")
     with open(js_path, "w") as fh:
         json.dump(js, fh, indent=1)
