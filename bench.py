@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="nbk", choices=["nbk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp64", action="store_true")
+    ap.add_argument("--others", default="C3,C4,C5",
+                    help="other configs measured briefly after the headline (1 GPU; '' = none)")
     return ap.parse_args()
 
 
@@ -98,6 +100,35 @@ class ClockSampler:
         med = statistics.median(self.samples) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
+
+
+class Energy:
+    """GPU energy (NVML total-energy counter, mJ) over a region (SURVEY 8(f) NEXT-3:
+    energy-to-solution, the paper's third axis)."""
+
+    def __init__(self, device_index: int):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(device_index)
+        except Exception:
+            self.nv = None
+        self.joules = None
+
+    def __enter__(self):
+        self.e0 = self._read()
+        return self
+
+    def _read(self):
+        try:
+            return self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h) if self.nv else None
+        except Exception:
+            return None
+
+    def __exit__(self, *a):
+        e1 = self._read()
+        if self.e0 is not None and e1 is not None:
+            self.joules = (e1 - self.e0) / 1e3
 
 
 def max_over_ranks(value: float, world: int, device="cuda") -> float:
@@ -214,6 +245,27 @@ def time_solves(ctx, torch, cfg, precision, steps, warmup, flush, profile):
     return ms, kA, graph_ms, res, hist
 
 
+def measure_other(nbk, torch, name, flush, stream, peak, steps=3, warmup=2):
+    """Short measurement of another BASELINE config on 1 GPU (not the headline):
+    FP32 and FP64 solver GDOF*iter/s, K_A roofline fraction, FP32/FP64 ratio."""
+    cfg = nbk.CONFIGS[name]
+    ctx = nbk.cg_setup(nbk.MeshSpec(**cfg.mesh_args(1)), "fp32", stream=stream)
+    out = {"workload": workload_name(cfg, "fp32"), "n_global": ctx.n_global, "steps": steps}
+    n = ctx.n_local
+    with torch.cuda.stream(stream):
+        for prec, s_b in (("fp32", 4), ("fp64", 8)):
+            ms, _, _, res, _ = time_solves(ctx, torch, cfg, prec, steps, warmup, flush, profile=False)
+            _, kA, _, _, _ = time_solves(ctx, torch, cfg, prec, 1, 1, flush, profile=True)
+            ka = sum(kA) / cfg.niter
+            out[prec] = {"value": ctx.n_global * cfg.niter * steps / (sum(ms) / 1e3) / 1e9,
+                         "ms_per_step": sum(ms) / steps,
+                         "k_ax_hbm_frac": 12 * s_b * n / (ka / 1e3) / 1e9 / peak,
+                         "true_res_rel": res["true_res_rel"]}
+    out["speedup_fp32_vs_fp64"] = out["fp32"]["value"] / out["fp64"]["value"]
+    ctx.close()
+    return out
+
+
 def run_gpu(args):
     import torch
     rank, world, local = dist_env()
@@ -246,9 +298,10 @@ def run_gpu(args):
 
     # ---- timed region (headline precision; plain graph, PDL edges on) ----
     barrier()
-    with torch.cuda.stream(stream), ClockSampler(local) as clk:
+    with torch.cuda.stream(stream), ClockSampler(local) as clk, Energy(local) as en32:
         ms, _, graph_ms, res, hist = time_solves(ctx, torch, cfg, prec, args.steps, args.warmup,
                                                  flush, profile=False)
+        ctx.sync()
     barrier()
     # ---- same solves again with CUDA events around every k_ax launch (roofline) ----
     with torch.cuda.stream(stream):
@@ -281,8 +334,10 @@ def run_gpu(args):
     if not args.no_fp64 and prec == "fp32":
         barrier()
         with torch.cuda.stream(stream):
-            ms64, _, _, res64, _ = time_solves(ctx, torch, cfg, "fp64", args.steps,
-                                               args.warmup, flush, profile=False)
+            with Energy(local) as en64:
+                ms64, _, _, res64, _ = time_solves(ctx, torch, cfg, "fp64", args.steps,
+                                                   args.warmup, flush, profile=False)
+                ctx.sync()
             _, kA64, _, _, _ = time_solves(ctx, torch, cfg, "fp64", args.steps, args.warmup,
                                            flush, profile=True)
         barrier()
@@ -293,6 +348,13 @@ def run_gpu(args):
                          "k_ax_hbm_frac": 12 * 8 * n / (ka64 / 1e3) / 1e9 / peak,
                          "true_res_rel": res64["true_res_rel"]}
         extra["speedup_fp32_vs_fp64"] = value / v64
+        if en32.joules and en64.joules:
+            # whole timed region incl. warm-up solves and L2 flushes: per-solve energy
+            # ratio is what it compares (P:682-703 energy-to-solution gain)
+            extra["energy"] = {"fp32_J_per_region": en32.joules, "fp64_J_per_region": en64.joules,
+                               "fp64_over_fp32": en64.joules / en32.joules,
+                               "note": "NVML total energy over warm-up + timed solves of each "
+                                       "solver (same step counts)"}
 
     # ---- end to end through the C ABI with host buffers ----
     import numpy as np
@@ -328,6 +390,27 @@ def run_gpu(args):
                "sample": f"{args.config} {prec} oracle CG, {iters} of {cfg.niter} iterations "
                          f"({dt:.1f} s; set-up untimed)"}
 
+    # whole-iteration algorithmic bandwidth (SURVEY 8(d) B_fused model)
+    info = ctx.info
+    phi = info["n_copies"] / n
+    psi = info["n_shared"] / n
+    s_b = 4 if prec == "fp32" else 8
+    b_fused = 15 * s_b + phi * (2 * s_b + 4) + psi * (s_b + 4)
+    t_iter = tot_ms / args.steps / cfg.niter / 1e3
+    model = {"B_fused_bytes_per_local_point": b_fused,
+             "bytes_per_global_dof": b_fused * n / ng,
+             "iteration_GBps": b_fused * n / t_iter / 1e9,
+             "iteration_hbm_frac": b_fused * n / t_iter / 1e9 / peak}
+
+    others = {}
+    if world == 1 and args.others:
+        ctx.close()
+        del ctx
+        torch.cuda.empty_cache()
+        for name in args.others.split(","):
+            others[name] = measure_other(nbk, torch, name, flush, stream, peak)
+            torch.cuda.empty_cache()
+
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if cfg.weak else "strong", "vs_baseline": None,
@@ -340,7 +423,8 @@ def run_gpu(args):
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "true_res_rel": res["true_res_rel"],
             "h_final_rel": float(hist[-1] / hist[0]) if hist[0] else 0.0,
-            "median_step_ms": statistics.median(ms), **extra}
+            "median_step_ms": statistics.median(ms), "iteration_model": model, **extra,
+            "other_configs": others or None}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
