@@ -75,6 +75,11 @@ def lib():
         for nm in ("ora_cg64", "ora_cg32"):
             getattr(L, nm).restype = ctypes.c_int
             getattr(L, nm).argtypes = [ctypes.c_int] * 4 + [_p] * 3 + [ctypes.c_int] + [_p] * 3
+        for nm in ("ora_pcg64", "ora_pcg32"):
+            getattr(L, nm).restype = ctypes.c_int
+            getattr(L, nm).argtypes = [ctypes.c_int] * 4 + [_p] * 4 + [ctypes.c_int] + [_p] * 3
+        L.ora_jacobi_dinv.restype = None
+        L.ora_jacobi_dinv.argtypes = [ctypes.c_int] * 4 + [_p] * 4
         L.ora_true_residual.restype = c_dbl
         L.ora_true_residual.argtypes = [ctypes.c_int] * 4 + [_p] * 5
         L.ora_num_threads.restype = ctypes.c_int
@@ -222,22 +227,48 @@ class CgResult:
     defect: int
 
 
-def cg(mesh: Mesh, D, G, f, niter: int, precision: str = "fp64") -> CgResult:
+def jacobi_dinv(mesh: Mesh, D, G):
+    """Jacobi preconditioner data (NEXT-1): the assembled diagonal d
+    of the stiffness operator (masked entries 1) and dinv = 1/d, FP64, local storage."""
+    D = np.ascontiguousarray(D, np.float64)
+    G = np.ascontiguousarray(G, np.float64)
+    d = np.zeros((mesh.E, mesh.N, mesh.N, mesh.N))
+    dinv = np.zeros_like(d)
+    lib().ora_jacobi_dinv(*mesh.dims, _ptr(D), _ptr(G), _ptr(d), _ptr(dinv))
+    return d, dinv
+
+
+def cg(mesh: Mesh, D, G, f, niter: int, precision: str = "fp64", dinv=None) -> CgResult:
     """Fixed-iteration CG (T1).  precision 'fp64' or 'fp32' (mixed: FP64 set-up
-    data rounded once to binary32, FP64 accumulation of glsc3)."""
+    data rounded once to binary32, FP64 accumulation of glsc3).  dinv (FP64
+    local array) selects Jacobi PCG: z = r * dinv (dinv rounded to the loop's
+    precision), rtz1 = glsc3(r, c, z)."""
     D = np.ascontiguousarray(D, np.float64)
     G = np.ascontiguousarray(G, np.float64)
     f = np.ascontiguousarray(f, np.float64)
     hist = np.zeros(niter + 1)
     trace = np.zeros((niter, 5))
-    if precision == "fp64":
+    L = lib()
+    if dinv is not None:
+        di = np.ascontiguousarray(dinv, np.float64)
+        if precision == "fp64":
+            x = np.zeros_like(f)
+            rc = L.ora_pcg64(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), _ptr(di), niter, _ptr(x),
+                             _ptr(hist), _ptr(trace))
+        elif precision == "fp32":
+            x = np.zeros(f.shape, np.float32)
+            rc = L.ora_pcg32(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), _ptr(di), niter, _ptr(x),
+                             _ptr(hist), _ptr(trace))
+        else:
+            raise ValueError(precision)
+    elif precision == "fp64":
         x = np.zeros_like(f)
-        rc = lib().ora_cg64(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), niter, _ptr(x), _ptr(hist),
-                            _ptr(trace))
+        rc = L.ora_cg64(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), niter, _ptr(x), _ptr(hist),
+                        _ptr(trace))
     elif precision == "fp32":
         x = np.zeros(f.shape, np.float32)
-        rc = lib().ora_cg32(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), niter, _ptr(x), _ptr(hist),
-                            _ptr(trace))
+        rc = L.ora_cg32(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), niter, _ptr(x), _ptr(hist),
+                        _ptr(trace))
     else:
         raise ValueError(precision)
     return CgResult(x=x, hist=hist, trace=trace, defect=int(rc))

@@ -19,6 +19,8 @@
  *   add2s1/add2s2 (T1 lines 4,7,8): p = beta p + z, x += alpha p, r -= alpha w.
  *   CG loop in FP64, and in FP32 with FP64 accumulation
  *   of the inner products (north_star), plus the final FP64 residual check.
+ *   Jacobi PCG (SURVEY 8(f) NEXT-1, T1 line 2 solveM): assembled diagonal,
+ *   z = r * dinv, rtz1 = glsc3(r,c,z).
  *
  * Build: gcc -O2 -ffp-contract=off -fopenmp -shared -fPIC (no -ffast-math:
  * IEEE round-to-nearest, gradual underflow, no contraction except the
@@ -571,10 +573,60 @@ void ora_multiplicity_weight(int ex, int ey, int ez, int N, double* c_out)
 }
 
 /* ------------------------------------------------------------------ */
-/* Fixed-iteration unpreconditioned CG (T1 P:142-152; C7-C9; R9, R10).  */
+/* Jacobi preconditioner (T1 line 2 "solveM"; */
+/* S:376-384): d = diag(A), the assembled diagonal of the stiffness      */
+/* operator, masked entries set to 1; dinv = 1/d.                        */
+/* A_e = sum_{m,n in r,s,t} D_m^T diag(g_mn) D_n with D_r = I x I x D   */
+/* (i fastest) etc., so its diagonal at (i,j,k) is                      */
+/*   sum_a D[a][i]^2 g1(a,j,k) + sum_b D[b][j]^2 g4(i,b,k)              */
+/*   + sum_c D[c][k]^2 g6(i,j,c)                                        */
+/*   + 2 (D[i][i] D[j][j] g2 + D[i][i] D[k][k] g3 + D[j][j] D[k][k] g5) */
+/* (only the q = L term survives in the mixed products).  A node occurs */
+/* at most once per element, so the assembled diagonal is the dssum of  */
+/* the local diagonals.  FP64 throughout (set-up).               */
+/* ------------------------------------------------------------------ */
+void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const double* G,
+                     double* d_out, double* dinv_out)
+{
+    ora_mesh m = {ex, ey, ez, N};
+    int64_t E = (int64_t)ex * ey * ez, nn = n3(&m), n = E * nn;
+    double* d = (double*)malloc(sizeof(double) * n);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+        const double* g = G + e * 6 * nn;
+        for (int k = 0; k < N; ++k)
+            for (int j = 0; j < N; ++j)
+                for (int i = 0; i < N; ++i) {
+                    int64_t q = ((int64_t)k * N + j) * N + i;
+                    double s = 0.0;
+                    for (int a = 0; a < N; ++a)
+                        s += D[a * N + i] * D[a * N + i] * g[0 * nn + ((int64_t)k * N + j) * N + a];
+                    for (int b = 0; b < N; ++b)
+                        s += D[b * N + j] * D[b * N + j] * g[3 * nn + ((int64_t)k * N + b) * N + i];
+                    for (int c = 0; c < N; ++c)
+                        s += D[c * N + k] * D[c * N + k] * g[5 * nn + ((int64_t)c * N + j) * N + i];
+                    s += 2.0 * (D[i * N + i] * D[j * N + j] * g[1 * nn + q] +
+                                D[i * N + i] * D[k * N + k] * g[2 * nn + q] +
+                                D[j * N + j] * D[k * N + k] * g[4 * nn + q]);
+                    d[e * nn + q] = s;
+                }
+    }
+    ora_dssum64(ex, ey, ez, N, d, 0);
+    for (int64_t L = 0; L < n; ++L) {
+        if (point_masked(&m, point_gid(&m, L))) d[L] = 1.0;
+        if (d_out) d_out[L] = d[L];
+        if (dinv_out) dinv_out[L] = 1.0 / d[L];
+    }
+    free(d);
+}
+
+/* ------------------------------------------------------------------ */
+/* Fixed-iteration CG (T1 P:142-152; C7-C9; R9, R10), unpreconditioned  */
+/* (dinv == NULL: solveM is the identity, z = r, MGRID off) or   */
+/* Jacobi-preconditioned (z = RN_T(r * dinv_T)).             */
 /*   x0 = 0; r0 = f; p0 = 0; rtr0 = glsc3(r,c,r); h0 = sqrt(rtr0)       */
 /*   for k = 1..niter:                                                  */
-/*     solveM: z = r (MGRID off) so rtz1 = glsc3(r,c,z) = rtr_{k-1}*/
+/*     z = solveM(r); rtz1 = glsc3(r,c,z)  (= rtr_{k-1} when z = r)     */
 /*     beta = 0 if k == 1 else rtz1/rtz2                                */
 /*     p = beta p + z       (add2s1)                                    */
 /*     w = ax(p)            (ax: local, dssum, mask)                    */
@@ -586,8 +638,8 @@ void ora_multiplicity_weight(int ex, int ey, int ez, int N, double* c_out)
 /* (defect) or 0.                                                */
 /* ------------------------------------------------------------------ */
 #define DEFINE_CG(NAME, T, FMA, AXLOCAL, DSSUM, GLSC3)                                          \
-    int NAME(int ex, int ey, int ez, int N, const T* D, const T* G, const T* f, int niter,      \
-             T* x, double* hist, double* trace)                                                 \
+    int NAME(int ex, int ey, int ez, int N, const T* D, const T* G, const T* f, const T* dinv,  \
+             int niter, T* x, double* hist, double* trace)                                      \
     {                                                                                           \
         ora_mesh m = {ex, ey, ez, N};                                                           \
         int64_t E = (int64_t)ex * ey * ez, n = E * n3(&m);                                      \
@@ -595,17 +647,23 @@ void ora_multiplicity_weight(int ex, int ey, int ez, int N, double* c_out)
         T* r = (T*)malloc(sizeof(T) * n);                                                       \
         T* p = (T*)malloc(sizeof(T) * n);                                                       \
         T* w = (T*)malloc(sizeof(T) * n);                                                       \
+        T* z = dinv ? (T*)malloc(sizeof(T) * n) : r;                                            \
         for (int64_t L = 0; L < n; ++L) { x[L] = 0; r[L] = f[L]; p[L] = 0; }                    \
         double rtr = GLSC3(n, r, r, c);                                                         \
         hist[0] = sqrt(rtr);                                                                    \
+        double rtz = rtr;                                                                       \
+        if (dinv) {                                                                             \
+            for (int64_t L = 0; L < n; ++L) z[L] = r[L] * dinv[L];                              \
+            rtz = GLSC3(n, r, z, c);                                                            \
+        }                                                                                       \
         double rtz2 = 0.0;                                                                      \
         int defect = 0, zero = 0;                                                               \
         for (int k = 1; k <= niter; ++k) {                                                      \
-            double rtz1 = rtr, beta = 0.0, alpha = 0.0, pap;                                    \
+            double rtz1 = rtz, beta = 0.0, alpha = 0.0, pap;                                    \
             if (rtz1 == 0.0) zero = 1;                                                          \
             if (!zero && k > 1) beta = rtz1 / rtz2;                                             \
             T betaT = (T)beta;                                                                  \
-            for (int64_t L = 0; L < n; ++L) p[L] = FMA(betaT, p[L], r[L]);                      \
+            for (int64_t L = 0; L < n; ++L) p[L] = FMA(betaT, p[L], z[L]);                      \
             AXLOCAL(E, N, D, G, p, w);                                                          \
             DSSUM(ex, ey, ez, N, w, 1);                                                         \
             pap = GLSC3(n, w, p, c);                                                            \
@@ -615,7 +673,13 @@ void ora_multiplicity_weight(int ex, int ey, int ez, int N, double* c_out)
             for (int64_t L = 0; L < n; ++L) r[L] = FMA(alphmT, w[L], r[L]);                     \
             rtr = GLSC3(n, r, r, c);                                                            \
             hist[k] = sqrt(rtr);                                                                \
-            if (!zero && !defect && (!(pap > 0.0) || !isfinite(pap) || !isfinite(rtr)))         \
+            rtz = rtr;                                                                          \
+            if (dinv) {                                                                         \
+                for (int64_t L = 0; L < n; ++L) z[L] = r[L] * dinv[L];                          \
+                rtz = GLSC3(n, r, z, c);                                                        \
+            }                                                                                   \
+            if (!zero && !defect &&                                                             \
+                (!(pap > 0.0) || !isfinite(pap) || !isfinite(rtr) || !isfinite(rtz)))           \
                 defect = k;                                                                     \
             if (trace) {                                                                        \
                 double* tr = trace + 5 * (int64_t)(k - 1);                                      \
@@ -624,6 +688,7 @@ void ora_multiplicity_weight(int ex, int ey, int ez, int N, double* c_out)
             rtz2 = rtz1;                                                                        \
         }                                                                                       \
         free(c); free(r); free(p); free(w);                                                     \
+        if (dinv) free(z);                                                                      \
         return defect;                                                                          \
     }
 
@@ -633,7 +698,7 @@ DEFINE_CG(ora_cg32_core, float, fmaf, ora_ax_local32, ora_dssum32, ora_glsc3_32)
 int ora_cg64(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,
              int niter, double* x, double* hist, double* trace)
 {
-    return ora_cg64_core(ex, ey, ez, N, D, G, f, niter, x, hist, trace);
+    return ora_cg64_core(ex, ey, ez, N, D, G, f, NULL, niter, x, hist, trace);
 }
 
 /* Mixed precision: FP64 setup data are converted once to
@@ -649,8 +714,33 @@ int ora_cg32(int ex, int ey, int ez, int N, const double* D, const double* G, co
 #pragma omp parallel for schedule(static)
     for (int64_t q = 0; q < 6 * n; ++q) G32[q] = (float)G[q];
     for (int64_t q = 0; q < n; ++q) f32[q] = (float)f[q];
-    int rc = ora_cg32_core(ex, ey, ez, N, D32, G32, f32, niter, x32, hist, trace);
+    int rc = ora_cg32_core(ex, ey, ez, N, D32, G32, f32, NULL, niter, x32, hist, trace);
     free(D32); free(G32); free(f32);
+    return rc;
+}
+
+/* Jacobi PCG (NEXT-1): dinv is data (FP64, e.g. from ora_jacobi_dinv);
+ * the FP32 loop uses dinv32 = RN32(dinv) (C11). */
+int ora_pcg64(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,
+              const double* dinv, int niter, double* x, double* hist, double* trace)
+{
+    return ora_cg64_core(ex, ey, ez, N, D, G, f, dinv, niter, x, hist, trace);
+}
+
+int ora_pcg32(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,
+              const double* dinv, int niter, float* x32, double* hist, double* trace)
+{
+    int64_t E = (int64_t)ex * ey * ez, nn = (int64_t)N * N * N, n = E * nn;
+    float* D32 = (float*)malloc(sizeof(float) * N * N);
+    float* G32 = (float*)malloc(sizeof(float) * 6 * n);
+    float* f32 = (float*)malloc(sizeof(float) * n);
+    float* di32 = (float*)malloc(sizeof(float) * n);
+    for (int q = 0; q < N * N; ++q) D32[q] = (float)D[q];
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < 6 * n; ++q) G32[q] = (float)G[q];
+    for (int64_t q = 0; q < n; ++q) { f32[q] = (float)f[q]; di32[q] = (float)dinv[q]; }
+    int rc = ora_cg32_core(ex, ey, ez, N, D32, G32, f32, di32, niter, x32, hist, trace);
+    free(D32); free(G32); free(f32); free(di32);
     return rc;
 }
 

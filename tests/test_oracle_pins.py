@@ -448,3 +448,118 @@ def test_cg_c1_fp64_and_fp32(ora):
     assert 1e-9 < tr32 / h0 < 1e-4
     xe = np.abs(r32.x - r64.x).max() / np.abs(r64.x).max()
     assert 1e-9 < xe < 1e-4
+
+
+# ------------------------------------------------ Jacobi PCG pins (NEXT-1)
+@pytest.mark.parametrize("mesh_args", [(2, 1, 1, 4, 0.0), (2, 2, 1, 3, 0.15), (1, 2, 2, 5, 0.1)])
+def test_jacobi_diagonal_is_dense_diagonal(ora, mesh_args):
+    """diag(A) equals the diagonal of the Kronecker-assembled dense
+    stiffness (P9 brute force) on unmasked nodes; masked entries are 1."""
+    ex, ey, ez, N, jit = mesh_args
+    m = ora.Mesh(ex, ey, ez, N, jitter=jit, seed_geom=7)
+    _, _, D = ora.gll(N)
+    s = ora.setup(m, want=("G", "gid", "mask"))
+    d, dinv = ora.jacobi_dinv(m, D, s["G"])
+    A, gid = dense_stiffness(ora, m)
+    ref = np.diag(A)[gid].reshape(d.shape)
+    msk = s["mask"].astype(bool)
+    assert np.abs(d[~msk] - ref[~msk]).max() <= 1e-13 * np.abs(ref).max()
+    assert (d[msk] == 1.0).all() and (ref[~msk] > 0).all()
+    np.testing.assert_array_equal(dinv, 1.0 / d)
+
+
+def test_jacobi_diagonal_by_indicator_vectors(ora):
+    """Second brute force: A_gg = (ax e_g) at a copy of g, with e_g the
+    continuous indicator of global node g (all copies 1), unmasked operator."""
+    m = ora.Mesh(2, 2, 1, 4, jitter=0.1, seed_geom=11)
+    _, _, D = ora.gll(4)
+    s = ora.setup(m, want=("G", "gid", "mask"))
+    d, _ = ora.jacobi_dinv(m, D, s["G"])
+    gid = s["gid"]
+    for g in range(0, m.sizes()["n_global"], 3):
+        u = (gid == g).astype(np.float64)
+        w = ora.ax(m, D, s["G"], u, apply_mask=False)
+        L = np.argwhere(gid.reshape(-1) == g)[0, 0]
+        if s["mask"].reshape(-1)[L]:
+            assert d.reshape(-1)[L] == 1.0
+        else:
+            assert w.reshape(-1)[L] == pytest.approx(d.reshape(-1)[L], rel=1e-13)
+
+
+def test_jacobi_apply_inverts_the_diagonal(ora):
+    """r = diag(A) * v gives z = r * dinv = v within 1e-13; masked
+    points have diagonal 1 so z = r there."""
+    m = ora.Mesh(2, 2, 2, 5, jitter=0.1, seed_geom=2)
+    _, _, D = ora.gll(5)
+    s = ora.setup(m, want=("G", "mask"))
+    d, dinv = ora.jacobi_dinv(m, D, s["G"])
+    v = inputs.uniform_field(d.shape, 4)
+    z = (d * v) * dinv
+    assert np.abs(z - v).max() <= 1e-13 * np.abs(v).max()
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_pcg_with_unit_diagonal_is_plain_cg(ora, prec):
+    """With dinv = 1, solveM is the identity (z = r bitwise, rtz1 = rtr): the
+    preconditioned loop must reproduce the unpreconditioned CG bit for bit."""
+    m = ora.Mesh(2, 2, 2, 6, jitter=0.1, seed_geom=5, seed_rhs=8)
+    _, _, D = ora.gll(6)
+    s = ora.setup(m, want=("G", "f"))
+    a = ora.cg(m, D, s["G"], s["f"], 30, prec)
+    b = ora.cg(m, D, s["G"], s["f"], 30, prec, dinv=np.ones_like(s["f"]))
+    np.testing.assert_array_equal(a.hist, b.hist)
+    np.testing.assert_array_equal(a.trace, b.trace)
+    np.testing.assert_array_equal(a.x, b.x)
+
+
+def test_pcg_matches_dense_solve_and_terminates(ora):
+    """Jacobi PCG (FP64) reaches the dense solution of the interior system
+     and, as CG on the symmetrically scaled system, terminates within
+    n_dof iterations (P11); it also needs fewer iterations than CG on a
+    jittered mesh."""
+    m = ora.Mesh(2, 2, 1, 4, jitter=0.2, seed_geom=3, seed_rhs=5)
+    _, _, D = ora.gll(4)
+    s = ora.setup(m, want=("G", "f", "gid"))
+    _, dinv = ora.jacobi_dinv(m, D, s["G"])
+    A, gid = dense_stiffness(ora, m)
+    mg = global_mask(ora, m)
+    fg = np.zeros(A.shape[0])
+    fg[gid] = s["f"].reshape(-1)
+    xg = np.zeros_like(fg)
+    xg[~mg] = np.linalg.solve(A[np.ix_(~mg, ~mg)], fg[~mg])
+    ndof = m.sizes()["n_interior"]
+    r = ora.cg(m, D, s["G"], s["f"], ndof + 5, "fp64", dinv=dinv)
+    assert r.defect == 0
+    assert np.abs(r.x.reshape(-1) - xg[gid]).max() <= 1e-9
+    assert (r.hist[: ndof + 1] / r.hist[0] < 1e-12).any()
+    # trace: h_k = sqrt(rtr_k); beta_1 = 0; rtz1 > 0
+    np.testing.assert_array_equal(r.hist[1:], np.sqrt(r.trace[:, 4]))
+    assert r.trace[0, 1] == 0.0 and (r.trace[:ndof, 0] > 0).all()
+    plain = ora.cg(m, D, s["G"], s["f"], 12, "fp64")
+    prec = ora.cg(m, D, s["G"], s["f"], 12, "fp64", dinv=dinv)
+    assert prec.hist[12] < plain.hist[12]
+
+
+def test_pcg_scaled_problem_equivalence(ora):
+    """Jacobi PCG on A is CG on the symmetrically scaled S^-1 A S^-1 (S^2 =
+    diag(A)): the A-norm error decreases monotonically -- checked
+    against the dense solution."""
+    m = ora.Mesh(2, 2, 2, 3, jitter=0.15, seed_geom=9, seed_rhs=2)
+    _, _, D = ora.gll(3)
+    s = ora.setup(m, want=("G", "f", "gid"))
+    _, dinv = ora.jacobi_dinv(m, D, s["G"])
+    A, gid = dense_stiffness(ora, m)
+    mg = global_mask(ora, m)
+    Ai = A[np.ix_(~mg, ~mg)]
+    fg = np.zeros(A.shape[0])
+    fg[gid] = s["f"].reshape(-1)
+    xg = np.zeros_like(fg)
+    xg[~mg] = np.linalg.solve(Ai, fg[~mg])
+    errs = []
+    for it in range(1, 20):
+        r = ora.cg(m, D, s["G"], s["f"], it, "fp64", dinv=dinv)
+        eg = np.zeros_like(xg)
+        eg[gid] = r.x.reshape(-1)
+        dd = (eg - xg)[~mg]
+        errs.append(dd @ Ai @ dd)
+    assert all(errs[i + 1] <= errs[i] * (1 + 1e-9) + 1e-28 for i in range(len(errs) - 1))
