@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="nbk", choices=["nbk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp64", action="store_true")
+    ap.add_argument("--no-jacobi", dest="jacobi", action="store_false",
+                    help="skip the Jacobi-PCG measurement beside the headline")
     ap.add_argument("--others", default="C3,C4,C5",
                     help="other configs measured briefly after the headline (1 GPU; '' = none)")
     return ap.parse_args()
@@ -355,6 +357,24 @@ def run_gpu(args):
                                "fp64_over_fp32": en64.joules / en32.joules,
                                "note": "NVML total energy over warm-up + timed solves of each "
                                        "solver (same step counts)"}
+
+    # ---- Jacobi PCG beside it: same workload, z = r / diag(A) ----
+    if args.jacobi:
+        barrier()
+        jac = {}
+        with torch.cuda.stream(stream):
+            ctx.set_precond("jacobi")
+            for p_ in ("fp32", "fp64"):
+                msj, _, _, resj, histj = time_solves(ctx, torch, cfg, p_, args.steps, args.warmup,
+                                                     flush, profile=False)
+                jac[p_] = {"value": ng * cfg.niter * args.steps /
+                           (max_over_ranks(sum(msj), world) / 1e3) / 1e9,
+                           "ms_per_step": sum(msj) / args.steps,
+                           "h_final_rel": float(histj[-1] / histj[0]) if histj[0] else 0.0,
+                           "true_res_rel": resj["true_res_rel"]}
+            ctx.set_precond("none")
+        barrier()
+        extra["jacobi_pcg"] = jac
 
     # ---- end to end through the C ABI with host buffers ----
     import numpy as np

@@ -109,6 +109,11 @@ typedef struct {
 
 typedef struct nbk_ctx nbk_ctx;
 
+/* Preconditioner of nbk_cg_solve (T1 line 2 "solveM"). */
+#define NBK_PRECOND_NONE 0   /* z = r (MGRID off): the north_star path                      */
+#define NBK_PRECOND_JACOBI 1 /* z = r * dinv, dinv = 1 / diag(A) assembled, masked entries 1
+                                (S:376-384); rtz1 = glsc3(r, c, z) replaces rtr_{k-1}        */
+
 /* Flags of nbk_ax_apply. */
 #define NBK_AX_LOCAL 0 /* w = ax_e(u) per element only (T1 line 5, F2 ax_e)             */
 #define NBK_AX_DSSUM 1 /* ... followed by direct-stiffness summation (dssum)      */
@@ -197,6 +202,22 @@ nbk_status nbk_get_solution(nbk_ctx* ctx, double* x_host);
 
 /* Device pointer of the last solution in its native precision (do not free). */
 nbk_status nbk_solution_ptr(nbk_ctx* ctx, nbk_precision precision, void** x_dev);
+
+/* Select the preconditioner of the following solves (default NBK_PRECOND_NONE).
+ * Jacobi: K_A forms z = RN_T(r * dinv_T) for p = beta p + z, K_C reduces
+ * rtz = glsc3(r, c, z) beside rtr (the history stays h_k = sqrt(rtr_k)); the
+ * FP32 solver uses dinv32 = RN32(dinv) (C11).  In a virtual group every member
+ * must be set alike. */
+nbk_status nbk_set_precond(nbk_ctx* ctx, int32_t precond);
+
+/* Jacobi data.  By default the library assembles its own FP64 diagonal (per
+ * element closed form, dssum, masked entries 1, inverse) at the first Jacobi
+ * solve after set-up / nbk_load_arrays.  nbk_load_precond replaces it with a
+ * host array dinv_host (e_local*N^3 doubles, local storage; the parity path,
+ * C10); nbk_get_precond copies the current dinv (FP64) to the host.
+ * Synchronous. */
+nbk_status nbk_load_precond(nbk_ctx* ctx, const double* dinv_host);
+nbk_status nbk_get_precond(nbk_ctx* ctx, double* dinv_host);
 
 /* Per-kernel timing inside the solve graph (CUDA events around the fused ax
  * kernel each iteration).  Takes effect at the next graph build. */

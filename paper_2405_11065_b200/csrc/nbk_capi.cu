@@ -74,7 +74,7 @@ static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned bloc
 }
 // attr_only: set the dynamic shared-memory limit (done once at set-up, never
 // under stream capture).
-template <typename T, int N, bool FUSED>
+template <typename T, int N, int FUSED>
 static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
                                bool pdl = false)
 {
@@ -107,7 +107,7 @@ static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_onl
     default: return cudaErrorInvalidValue;    \
     }
 
-template <typename T, bool FUSED>
+template <typename T, int FUSED>
 static cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
                              bool pdl = false)
 {
@@ -238,9 +238,9 @@ static Team team_self(nbk_ctx* c)
 template <typename T>
 static T* fld(nbk_ctx* c, int which, bool fp32)
 {
-    // which: 0 x, 1 r, 2 p, 3 w
-    void* v64[4] = {c->x64, c->r64, c->p64, c->w64};
-    void* v32[4] = {c->x32, c->r32, c->p32, c->w32};
+    // which: 0 x, 1 r, 2 p, 3 w, 4 dinv
+    void* v64[5] = {c->x64, c->r64, c->p64, c->w64, c->dinv64};
+    void* v32[5] = {c->x32, c->r32, c->p32, c->w32, c->dinv32};
     return (T*)(fp32 ? v32[which] : v64[which]);
 }
 
@@ -279,7 +279,7 @@ static cudaError_t xchg_gather(const Team& t, cudaStream_t s, std::string& err)
         std::string why;
         const NcclApi* A = nccl_api(why);
         if (!A) { err = why; return cudaErrorUnknown; }
-        ncclResult_t r = A->allGather(c->gather + c->rank, c->gather, 2, ncclFloat64,
+        ncclResult_t r = A->allGather(c->gather + 2 * c->rank, c->gather, 4, ncclFloat64,
                                       (ncclComm_t)c->comm, s);
         if (r != ncclSuccess) {
             err = std::string("NCCL allgather: ") + A->errorString(r);
@@ -329,11 +329,12 @@ static FaceArgs<T> face_args(nbk_ctx* c, T* w)
     f.send_lo = (T*)c->send_lo; f.send_hi = (T*)c->send_hi;
     f.recv_lo = (const T*)c->recv_lo; f.recv_hi = (const T*)c->recv_hi;
     f.has_lo = c->has_lo; f.has_hi = c->has_hi;
-    f.parts = c->parts; f.st = c->st; f.slot = c->gather + c->rank; f.mesh = c->view;
+    f.parts = c->parts; f.st = c->st; f.slot = c->gather + 2 * c->rank; f.mesh = c->view;
     return f;
 }
 
-static dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - NBK_VEC_GRID_MAX; }
+// vector kernels: two banks of NBK_VEC_GRID_MAX partials (rtr, rtz) at the end
+static dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - 2 * NBK_VEC_GRID_MAX; }
 
 // dssum (+ mask) of w over a team.  fused: shared-node pap terms, alpha.
 // One rank: K_B (its last block forms alpha).  Several: K_B (publish only) and
@@ -396,7 +397,7 @@ static cudaError_t vec_team(const Team& t, const std::vector<VecArgs<T>>& args, 
     cudaError_t e;
     for (size_t q = 0; q < t.m.size(); ++q) {
         VecArgs<T> a = args[q];
-        a.slot = t.multi ? t.m[q]->gather + t.m[q]->rank : nullptr;
+        a.slot = t.multi ? t.m[q]->gather + 2 * t.m[q]->rank : nullptr;
         if ((e = launch_vec<T, MODE>(a, t.s, pdl && !t.multi)) != cudaSuccess) return e;
     }
     if (!t.multi) return cudaSuccess;
@@ -429,7 +430,7 @@ static cudaError_t ax_team(const Team& t, const std::vector<const T*>& u, const 
         AxArgs<T> a = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
                            : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
         a.u = u[q]; a.w = w[q]; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
-        if ((e = launch_ax<T, false>(a, t.s)) != cudaSuccess) return e;
+        if ((e = launch_ax<T, 0>(a, t.s)) != cudaSuccess) return e;
     }
     if (flags & NBK_AX_DSSUM) return dssum_team<T, false>(t, w, {}, 0, false, err);
     return cudaSuccess;
@@ -454,14 +455,18 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
     const int64_t per_fin = t.multi ? 1 : 0;  // k_fin launches per reduction and member
     const int64_t nface = t.multi ? 2 : 0;    // pack + merge per dssum and member
 
+    // Jacobi PCG (NEXT-1): z = r * dinv formed in K_A and K_C, rtz reduced beside rtr
+    const bool jac = t.m[0]->precond == NBK_PRECOND_JACOBI;
     std::vector<VecArgs<T>> vi(P), vr(P);
     for (size_t q = 0; q < P; ++q) {
         vi[q] = vec_args<T>(t.m[q]);
         vi[q].r = r[q]; vi[q].x = x[q]; vi[q].p = p[q]; vi[q].f = t.m[q]->f64;
+        vi[q].dinv = fld<T>(t.m[q], 4, fp32);
         vr[q] = vi[q];
         vr[q].w = w[q];
     }
-    if ((e = vec_team<T, VEC_INIT>(t, vi, false, err)) != cudaSuccess) return e;
+    e = jac ? vec_team<T, VEC_INIT_J>(t, vi, false, err) : vec_team<T, VEC_INIT>(t, vi, false, err);
+    if (e != cudaSuccess) return e;
     launches += (int64_t)P * (1 + per_fin);
 
     // sweep directions alternate kernel by kernel: K_A f, K_B b, K_C f, K_A b, ...
@@ -476,12 +481,15 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
                                 : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
             aa.u = nullptr; aa.w = w[q]; aa.p = p[q]; aa.r = r[q]; aa.x = x[q]; aa.mask = 1;
             aa.rev = rev;
-            if ((e = launch_ax<T, true>(aa, s, false, pdl)) != cudaSuccess) return e;
+            aa.dinv = fld<T>(c, 4, fp32);
+            e = jac ? launch_ax<T, 2>(aa, s, false, pdl) : launch_ax<T, 1>(aa, s, false, pdl);
+            if (e != cudaSuccess) return e;
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1) + 1], s, cudaEventRecordExternal);
         if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err, !rev)) != cudaSuccess) return e;
         for (size_t q = 0; q < P; ++q) vr[q].rev = rev;
-        if ((e = vec_team<T, VEC_RUPD>(t, vr, pdl, err)) != cudaSuccess) return e;
+        e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pdl, err) : vec_team<T, VEC_RUPD>(t, vr, pdl, err);
+        if (e != cudaSuccess) return e;
         rev = !rev;
         launches += (int64_t)P * (3 + nface + 2 * per_fin);
     }
@@ -515,7 +523,7 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
 static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_graph** out)
 {
     nbk_ctx* c = t.m[0];
-    auto key = std::make_tuple((int)prec, niter, c->profiling);
+    auto key = std::make_tuple((int)prec, niter, c->profiling * 2 + c->precond);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) { *out = &it->second; return NBK_OK; }
     nbk_graph g;
@@ -560,10 +568,12 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
     a32.mesh = c->view;
     cudaError_t e;
 
-    if ((e = launch_ax<double, false>(a64, c->stream, true)) != cudaSuccess) return e;
-    if ((e = launch_ax<double, true>(a64, c->stream, true)) != cudaSuccess) return e;
-    if ((e = launch_ax<float, false>(a32, c->stream, true)) != cudaSuccess) return e;
-    return launch_ax<float, true>(a32, c->stream, true);
+    if ((e = launch_ax<double, 0>(a64, c->stream, true)) != cudaSuccess) return e;
+    if ((e = launch_ax<double, 1>(a64, c->stream, true)) != cudaSuccess) return e;
+    if ((e = launch_ax<double, 2>(a64, c->stream, true)) != cudaSuccess) return e;
+    if ((e = launch_ax<float, 0>(a32, c->stream, true)) != cudaSuccess) return e;
+    if ((e = launch_ax<float, 1>(a32, c->stream, true)) != cudaSuccess) return e;
+    return launch_ax<float, 2>(a32, c->stream, true);
 }
 
 // glsc3 over a team (synchronous); result identical on every member.
@@ -588,6 +598,7 @@ static nbk_status glsc3_team(const Team& t, const std::vector<const T*>& a, cons
 static nbk_status refresh_fp32(nbk_ctx* c)
 {
     cudaStream_t s = c->stream;
+    c->dinv_dirty = 1;  // the operator may have changed: own diagonal re-assembled on demand
     if (c->G32) {
         k_downcast<<<vec_grid(6 * c->n), 256, 0, s>>>(c->G32, c->G64, 6 * c->n);
         k_downcast<<<1, 256, 0, s>>>(c->D32, c->D64, (int64_t)c->N * c->N);
@@ -615,6 +626,30 @@ static nbk_status refresh_h0(const Team& t)
     return NBK_OK;
 }
 
+// Jacobi data (NEXT-1): the library's own assembled diagonal -- per-element
+// diag(A_e) (FP64), the team's dssum (slab faces exchanged like any dssum),
+// masked entries 1, inverse, RN32 copy -- unless loaded (nbk_load_precond).
+static nbk_status refresh_dinv(const Team& t)
+{
+    bool dirty = false;
+    for (nbk_ctx* c : t.m) dirty = dirty || c->dinv_dirty;
+    if (!dirty) return NBK_OK;
+    nbk_ctx* c0 = t.m[0];
+    std::vector<double*> d(t.m.size());
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        d[q] = t.m[q]->dinv64;
+        NBK_CUDA(c0, local_diag(t.m[q], d[q]));
+    }
+    std::string err;
+    cudaError_t e = dssum_team<double, false>(t, d, {}, 0, false, err);
+    if (e != cudaSuccess)
+        return fail(c0, err.empty() ? NBK_ECUDA : NBK_ENCCL, err.empty() ? cudaGetErrorString(e) : err);
+    for (size_t q = 0; q < t.m.size(); ++q) NBK_CUDA(c0, finish_dinv(t.m[q], d[q]));
+    NBK_CUDA(c0, cudaStreamSynchronize(t.s));
+    for (nbk_ctx* c : t.m) c->dinv_dirty = 0;
+    return NBK_OK;
+}
+
 // Team of a call made on one context: errors for virtual-group members.
 static nbk_status self_team(nbk_ctx* c, Team& t)
 {
@@ -634,6 +669,12 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
         if (prec == NBK_FP32 && !m->G32) return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
     nbk_status st = refresh_h0(t);
     if (st != NBK_OK) return st;
+    if (c->precond == NBK_PRECOND_JACOBI) {
+        for (nbk_ctx* m : t.m)
+            if (m->precond != c->precond) return fail(c, NBK_EINVAL, "members differ in preconditioner");
+        st = refresh_dinv(t);
+        if (st != NBK_OK) return st;
+    }
     nbk_graph* g = nullptr;
     st = get_graph(t, niter, prec, &g);
     if (st != NBK_OK) return st;
@@ -781,6 +822,7 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     c->gather = c->gather_own;
     c->G64 = (double*)(b + L.off_G64);
     c->f64 = (double*)(b + L.off_f64);
+    c->dinv64 = (double*)(b + L.off_dinv64);
     const size_t v64 = ((size_t)8 * c->n + 255) & ~(size_t)255;
     c->x64 = (double*)(b + L.off_vec64);
     c->r64 = (double*)(b + L.off_vec64 + v64);
@@ -795,6 +837,7 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
         c->r32 = (float*)(b + L.off_vec32 + v32);
         c->p32 = (float*)(b + L.off_vec32 + 2 * v32);
         c->w32 = (float*)(b + L.off_vec32 + 3 * v32);
+        c->dinv32 = (float*)(b + L.off_dinv32);
     }
     // NCCL communicator (collective over the ranks) when an id is given
     if (c->nranks > 1 && d->nccl_id) {
@@ -810,7 +853,7 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     nbk_status st = NBK_OK;
     cudaError_t e = set_ax_attrs(c);
     if (e == cudaSuccess) e = cudaMemsetAsync(c->st, 0, sizeof(CgState), c->stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(c->gather_own, 0, sizeof(dd) * NBK_MAX_RANKS, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->gather_own, 0, 2 * sizeof(dd) * NBK_MAX_RANKS, c->stream);
     if (e == cudaSuccess) e = setup_device(c, L);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) {
@@ -962,6 +1005,47 @@ nbk_status nbk_glsc3(nbk_ctx* c, const void* a_dev, const void* b_dev, nbk_preci
     return glsc3_team_abi(t, &a_dev, &b_dev, prec, out);
 }
 
+nbk_status nbk_set_precond(nbk_ctx* c, int32_t precond)
+{
+    if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
+    if (precond != NBK_PRECOND_NONE && precond != NBK_PRECOND_JACOBI)
+        return fail(c, NBK_EINVAL, "bad preconditioner");
+    c->precond = precond;
+    return NBK_OK;
+}
+
+nbk_status nbk_load_precond(nbk_ctx* c, const double* dinv_host)
+{
+    if (!c || !dinv_host) return fail(c, NBK_EINVAL, "NULL argument");
+    NBK_CUDA(c, cudaMemcpyAsync(c->dinv64, dinv_host, 8 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
+    if (c->dinv32) {
+        k_downcast<<<vec_grid(c->n), 256, 0, c->stream>>>(c->dinv32, c->dinv64, c->n);
+        NBK_CUDA(c, cudaGetLastError());
+    }
+    NBK_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->dinv_dirty = 0;
+    return NBK_OK;
+}
+
+nbk_status nbk_get_precond(nbk_ctx* c, double* dinv_host)
+{
+    if (!c || !dinv_host) return fail(c, NBK_EINVAL, "NULL argument");
+    Team t;
+    if (c->group.empty()) {
+        nbk_status st = self_team(c, t);
+        if (st != NBK_OK) return st;
+    } else {
+        t.m = c->group;
+        t.multi = true;
+        t.s = c->group[0]->stream;
+    }
+    nbk_status st = refresh_dinv(t);
+    if (st != NBK_OK) return st;
+    NBK_CUDA(c, cudaMemcpyAsync(dinv_host, c->dinv64, 8 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+    NBK_CUDA(c, cudaStreamSynchronize(c->stream));
+    return NBK_OK;
+}
+
 nbk_status nbk_set_profiling(nbk_ctx* c, int32_t enable)
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
@@ -1079,6 +1163,7 @@ nbk_status nbk_group_link(nbk_ctx* const* ctxs, int32_t P)
         if (c->has_lo) c->recv_lo = ctxs[r - 1]->send_hi;
         if (c->has_hi) c->recv_hi = ctxs[r + 1]->send_lo;
         c->h0_dirty = 1;
+        c->dinv_dirty = 1;
         destroy_graphs(c);
     }
     return NBK_OK;

@@ -38,6 +38,10 @@ struct nbk_ctx {
     double *x64 = nullptr, *r64 = nullptr, *p64 = nullptr, *w64 = nullptr;
     float *D32 = nullptr, *G32 = nullptr;
     float *x32 = nullptr, *r32 = nullptr, *p32 = nullptr, *w32 = nullptr;
+    double* dinv64 = nullptr;             // Jacobi: 1 / assembled diag(A) (masked: 1)
+    float* dinv32 = nullptr;              // RN32(dinv64) (C11)
+    int precond = NBK_PRECOND_NONE;
+    int dinv_dirty = 1;                   // own diagonal to be (re)assembled
     double *hist = nullptr, *trace = nullptr;
     nbk::dd* parts = nullptr;
     int64_t nparts = 0;
@@ -72,7 +76,7 @@ namespace nbk {
 
 struct Layout {
     size_t off_state, off_D64, off_D32, off_hist, off_trace, off_parts, off_segoff, off_segidx, off_grp,
-        off_face, off_gather, off_toff, off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
+        off_face, off_gather, off_toff, off_dinv64, off_dinv32, off_G64, off_f64, off_vec64, off_G32, off_vec32, total;
     int64_t nlayer, nplane;
     int has_lo, has_hi;
     int64_t E, n, n_global, nseg, ncopies, nparts, e_offset;
@@ -86,5 +90,7 @@ MeshView make_view(const nbk_mesh* m, const nbk_dist* d);
 void gll_host(int N, double* xi, double* rho, double* D);
 cudaError_t setup_device(nbk_ctx* ctx, const Layout& L);
 cudaError_t build_plan(nbk_ctx* ctx);
+cudaError_t local_diag(nbk_ctx* ctx, double* d);        // per-element diag(A_e), FP64
+cudaError_t finish_dinv(nbk_ctx* ctx, double* d);       // mask -> 1, invert, RN32 copy
 
 }  // namespace nbk

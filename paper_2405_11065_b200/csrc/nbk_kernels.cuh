@@ -130,6 +130,7 @@ struct AxArgs {
     const T* r;        // fused: r
     T* x;              // fused: x (in/out)
     const CgState* st; // fused: beta, alpha_prev
+    const T* dinv;     // fused Jacobi PCG: z = r * dinv replaces r in the p update
     dd* parts;         // fused: pap partial per block
     MeshView mesh;
     int mask;          // assign +0 to Dirichlet points of w
@@ -137,7 +138,9 @@ struct AxArgs {
 };
 
 // ---------------------------------------------------------------- K_A
-template <typename T, int N, bool FUSED>
+// FUSED: 0 = plain ax (u -> w); 1 = CG step (p = beta p + r); 2 = Jacobi PCG
+// step (p = beta p + z, z = RN(r * dinv) formed here: S:376-384, T1 line 2).
+template <typename T, int N, int FUSED>
 __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     k_ax(AxArgs<T> a)
 {
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
 
     const int64_t base = e * N3 + ij;
     T betaT = 0, alphaT = 0;
-    T rreg[FUSED ? N : 1], xreg[FUSED ? N : 1];
+    T rreg[FUSED ? N : 1], xreg[FUSED ? N : 1], dreg[FUSED == 2 ? N : 1];
     if constexpr (FUSED) {
         if constexpr (sizeof(T) == 8) {
             betaT = (T)a.st->beta;
@@ -205,6 +208,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             for (int k = 0; k < N; ++k) {
                 rreg[k] = a.r[base + k * N2];
                 xreg[k] = a.x[base + k * N2];
+                if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + base + k * N2);
             }
         }
     }
@@ -223,7 +227,9 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             T v = ue[k * N2 + ij];
             if constexpr (FUSED) {
                 const T po = v;
-                v = fma_t<T>(betaT, po, rreg[k]);
+                T zk = rreg[k];
+                if constexpr (FUSED == 2) zk = mul_t<T>(rreg[k], dreg[k]);  // solveM (Jacobi)
+                v = fma_t<T>(betaT, po, zk);
                 a.x[base + k * N2] = fma_t<T>(alphaT, po, xreg[k]);
                 a.p[base + k * N2] = v;
                 ue[k * N2 + ij] = v;
@@ -353,13 +359,20 @@ __device__ __forceinline__ void fin_alpha(CgState* st, double pap, double* trace
     tr[3] = pap;
 }
 
-enum VecMode { VEC_INIT = 0, VEC_RUPD = 1, VEC_TRUE = 2, VEC_DOT = 3 };
+// VEC_INIT_J / VEC_RUPD_J: the Jacobi PCG forms of INIT / RUPD, which also
+// form z = r * dinv and reduce rtz = glsc3(r, c, z) beside rtr.
+enum VecMode { VEC_INIT = 0, VEC_RUPD = 1, VEC_TRUE = 2, VEC_DOT = 3, VEC_INIT_J = 4, VEC_RUPD_J = 5 };
 
+__host__ __device__ constexpr bool vec_jacobi(int mode) { return mode == VEC_INIT_J || mode == VEC_RUPD_J; }
+
+// rtr: glsc3(r,c,r) (the residual norm h_k); rtz: glsc3(r,c,z), the
+// preconditioned product that drives alpha / beta (= rtr when z = r).
+// st->rtr holds the current rtz1.
 template <int MODE>
-__device__ __forceinline__ void fin_rtr(CgState* st, double rtr, double* hist, double* trace)
+__device__ __forceinline__ void fin_rtr(CgState* st, double rtr, double rtz, double* hist, double* trace)
 {
-    if constexpr (MODE == VEC_INIT) {
-        st->rtr = rtr;
+    if constexpr (MODE == VEC_INIT || MODE == VEC_INIT_J) {
+        st->rtr = rtz;
         st->rtz2 = 0.0;
         st->beta = 0.0;
         st->beta32 = 0.0f;
@@ -367,16 +380,16 @@ __device__ __forceinline__ void fin_rtr(CgState* st, double rtr, double* hist, d
         st->alpha32 = 0.0f;
         st->alpham = 0.0;
         st->alpham32 = 0.0f;
-        st->zero = (rtr == 0.0);
+        st->zero = (rtz == 0.0);
         st->defect = 0;
         st->it = 1;
         hist[0] = sqrt(rtr);
-    } else if constexpr (MODE == VEC_RUPD) {
+    } else if constexpr (MODE == VEC_RUPD || MODE == VEC_RUPD_J) {
         const int k = st->it;
         hist[k] = sqrt(rtr);                    // h_k (R13)
         trace[5 * (int64_t)(k - 1) + 4] = rtr;
-        if (!st->zero && st->defect == 0 && !isfinite(rtr)) st->defect = k;
-        const double rtz1_next = rtr, rtz2_next = st->rtr;
+        if (!st->zero && st->defect == 0 && (!isfinite(rtr) || !isfinite(rtz))) st->defect = k;
+        const double rtz1_next = rtz, rtz2_next = st->rtr;
         st->rtz2 = rtz2_next;
         st->rtr = rtz1_next;
         if (rtz1_next == 0.0) st->zero = 1;     // C9
@@ -537,6 +550,7 @@ struct VecArgs {
     T* p;               // INIT: zeroed
     const T* a;         // DOT
     const T* b;         // DOT
+    const T* dinv;      // INIT_J / RUPD_J
     int64_t n;
     dd* parts;
     CgState* st;
@@ -629,7 +643,7 @@ __device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, doub
 // chunks can be issued before either is used).
 template <typename T, int V, int MODE>
 struct VecChunk {
-    VecT<T, V> A, B;
+    VecT<T, V> A, B, C;
     VecT<double, V> F;
     __device__ __forceinline__ void load(const VecArgs<T>& a, int64_t L)
     {
@@ -641,13 +655,20 @@ struct VecChunk {
         } else if constexpr (MODE == VEC_TRUE) {
             A.load(a.w + L);
             F.load(a.f + L);
+        } else if constexpr (MODE == VEC_INIT_J) {
+            F.load(a.f + L);
+            C.load(a.dinv + L);
+        } else if constexpr (MODE == VEC_RUPD_J) {
+            A.load(a.w + L);
+            B.load(a.r + L);
+            C.load(a.dinv + L);
         } else {
             A.load(a.a + L);
             B.load(a.b + L);
         }
     }
     __device__ __forceinline__ void run(const VecArgs<T>& a, int64_t L, const double (&c)[V], T am,
-                                        acc_t& acc)
+                                        acc_t& acc, acc_t& acc2)
     {
         if constexpr (MODE == VEC_INIT) {
             VecT<T, V> r, z;
@@ -675,6 +696,31 @@ struct VecChunk {
             r.store(a.r + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+        } else if constexpr (MODE == VEC_INIT_J) {
+            VecT<T, V> r, z;
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                r.v[t] = (T)F.v[t];  // C11: f32 = RN32(f64)
+                z.v[t] = 0;
+            }
+            r.store(a.r + L);
+            z.store(a.x + L);
+            z.store(a.p + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                acc.add(dot_term(r.v[t], r.v[t], c[t]));
+                acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t]));  // z = r dinv
+            }
+        } else if constexpr (MODE == VEC_RUPD_J) {
+            VecT<T, V> r;
+#pragma unroll
+            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, A.v[t], B.v[t]);  // C8
+            r.store(a.r + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                acc.add(dot_term(r.v[t], r.v[t], c[t]));
+                acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t]));  // z = r dinv
+            }
         } else {
 #pragma unroll
             for (int t = 0; t < V; ++t) acc.add(dot_term(A.v[t], B.v[t], c[t]));
@@ -687,7 +733,7 @@ struct VecChunk {
 // K_A backward, ...): each kernel starts where its predecessor ended, on the
 // data still resident in the 126 MB L2.
 template <typename T, int N, int MODE>
-__device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc)
+__device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, acc_t& acc2)
 {
     constexpr int N3 = N * N * N;
     constexpr int V = (N3 % 4 == 0) ? 4 : ((N3 % 2 == 0) ? 2 : 1);
@@ -704,9 +750,9 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc)
         C1.load(a, L1);
         double c[V];
         chunk_weights<N, V>(a.mesh, L0, c);
-        C0.run(a, L0, c, am, acc);
+        C0.run(a, L0, c, am, acc, acc2);
         chunk_weights<N, V>(a.mesh, L1, c);
-        C1.run(a, L1, c, am, acc);
+        C1.run(a, L1, c, am, acc, acc2);
     }
     if (q0 < nch) {
         VecChunk<T, V, MODE> C0;
@@ -714,31 +760,38 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc)
         C0.load(a, L0);
         double c[V];
         chunk_weights<N, V>(a.mesh, L0, c);
-        C0.run(a, L0, c, am, acc);
+        C0.run(a, L0, c, am, acc, acc2);
     }
 }
 
 template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 {
-    acc_t acc;
+    constexpr bool J = vec_jacobi(MODE);
+    acc_t acc, acc2;
     T am = 0;
     pdl_wait();
-    if constexpr (MODE == VEC_RUPD) {
+    if constexpr (MODE == VEC_RUPD || MODE == VEC_RUPD_J) {
         if constexpr (sizeof(T) == 8) am = (T)a.st->alpham; else am = (T)a.st->alpham32;
     }
-    vec_loop<T, N, MODE>(a, am, acc);
+    vec_loop<T, N, MODE>(a, am, acc, acc2);
     pdl_launch_dependents();
     dd v = block_reduce_dd(acc.get());
+    dd v2 = J ? block_reduce_dd(acc2.get()) : dd{0.0, 0.0};
+    if (J && threadIdx.x == 0) {  // rtz partials in the second bank (ordered by the release below)
+        __stcg(&a.parts[gridDim.x + blockIdx.x].hi, v2.hi);
+        __stcg(&a.parts[gridDim.x + blockIdx.x].lo, v2.lo);
+    }
     if (publish_and_check_last(a.parts, blockIdx.x, v, &a.st->cnt[1], gridDim.x)) {
         dd tot = reduce_partials(a.parts, (int)gridDim.x);
+        dd tot2 = J ? reduce_partials(a.parts + gridDim.x, (int)gridDim.x) : tot;
         if (threadIdx.x == 0) {
             if (a.slot) {
-                // multi-rank: publish this rank's partial; k_fin finalises
-                a.slot->hi = tot.hi;
-                a.slot->lo = tot.lo;
+                // multi-rank: publish this rank's partials; k_fin finalises
+                a.slot[0] = tot;
+                a.slot[1] = tot2;
             } else {
-                fin_rtr<MODE>(a.st, tot.hi, a.hist, a.trace);
+                fin_rtr<MODE>(a.st, tot.hi, tot2.hi, a.hist, a.trace);
             }
             a.st->cnt[1] = 0;
         }
@@ -914,14 +967,19 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
 
 // Combine the P per-rank partials in rank order (identical on every rank)
 // and run the scalar finaliser.  KIND: 0 = alpha (pap); 1 + VecMode = rtr etc.
+// gather holds two dd per rank: [2r] the value, [2r + 1] rtz (Jacobi modes).
 template <int KIND>
 __global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double* trace)
 {
     if (threadIdx.x != 0) return;
     dd t{__ldcg(&gather[0].hi), __ldcg(&gather[0].lo)};
-    for (int r = 1; r < P; ++r) t = dd_add(t, dd{__ldcg(&gather[r].hi), __ldcg(&gather[r].lo)});
+    dd t2{__ldcg(&gather[1].hi), __ldcg(&gather[1].lo)};
+    for (int r = 1; r < P; ++r) {
+        t = dd_add(t, dd{__ldcg(&gather[2 * r].hi), __ldcg(&gather[2 * r].lo)});
+        t2 = dd_add(t2, dd{__ldcg(&gather[2 * r + 1].hi), __ldcg(&gather[2 * r + 1].lo)});
+    }
     if constexpr (KIND == 0) fin_alpha(st, t.hi, trace);
-    else fin_rtr<KIND - 1>(st, t.hi, hist, trace);
+    else fin_rtr<KIND - 1>(st, t.hi, vec_jacobi(KIND - 1) ? t2.hi : t.hi, hist, trace);
 }
 
 }  // namespace nbk

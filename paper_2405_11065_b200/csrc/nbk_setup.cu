@@ -108,8 +108,8 @@ Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
     L.nplane = Gx * Gy;
     L.nseg -= nb * (L.nplane - U);
     L.ncopies -= nb * (L.nlayer - U);
-    // partial slots: K_A (<= E CTAs), K_B, face merge, vector kernels (<= 1184 each)
-    L.nparts = L.E + 3 * NBK_VEC_GRID_MAX + 64;
+    // partial slots: K_A (<= E CTAs), K_B, face merge (<= 1184 each), vector kernels (2 x 1184)
+    L.nparts = L.E + 4 * NBK_VEC_GRID_MAX + 64;
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o += align256(bytes); return r; };
     L.off_state = take(sizeof(CgState));
@@ -122,18 +122,20 @@ Layout compute_layout(const nbk_mesh* m, nbk_precision prec, const nbk_dist* d)
     L.off_segidx = take(4 * (size_t)(L.ncopies > 0 ? L.ncopies : 1));
     L.off_grp = take(4 * (size_t)L.ncopies + 64);
     L.off_face = take(nb ? 4 * 8 * (size_t)L.nlayer : 8);
-    L.off_gather = take(sizeof(dd) * NBK_MAX_RANKS);
+    L.off_gather = take(2 * sizeof(dd) * NBK_MAX_RANKS);
     L.off_toff = take(4 * 3 * ((size_t)L.E + 2));
     L.off_G64 = take(8 * 6 * (size_t)L.n);
     L.off_f64 = take(8 * (size_t)L.n);
+    L.off_dinv64 = take(8 * (size_t)L.n);
     L.scratch_need = plan_scratch_bytes(L.n, L.nseg);
     size_t vec64 = 4 * align256(8 * (size_t)L.n);
     L.off_vec64 = take(vec64 > L.scratch_need ? vec64 : L.scratch_need);
     if (prec == NBK_FP32) {
         L.off_G32 = take(4 * 6 * (size_t)L.n);
         L.off_vec32 = take(4 * align256(4 * (size_t)L.n));
+        L.off_dinv32 = take(4 * (size_t)L.n);
     } else {
-        L.off_G32 = L.off_vec32 = 0;
+        L.off_G32 = L.off_vec32 = L.off_dinv32 = 0;
     }
     L.total = o;
     return L;
@@ -550,6 +552,64 @@ cudaError_t build_plan(nbk_ctx* ctx)
                                                                  ctx->toff);
     err = cudaStreamSynchronize(s);
     if (err != cudaSuccess) return err;
+    return cudaGetLastError();
+}
+
+// Jacobi preconditioner (NEXT-1): diagonal of the element matrix
+// A_e = sum_mn D_m^T diag(g_mn) D_n at (i,j,k):
+//   sum_a D[a][i]^2 g1(a,j,k) + sum_a D[a][j]^2 g4(i,a,k) + sum_a D[a][k]^2 g6(i,j,a)
+//   + 2 (D[i][i] D[j][j] g2 + D[i][i] D[k][k] g3 + D[j][j] D[k][k] g5).
+// One block per element.  FP64 set-up; assembled by the library's
+// own dssum afterwards.
+__global__ void __launch_bounds__(256) k_local_diag(const double* G, const double* Dg, int N, double* d)
+{
+    __shared__ double D[256];
+    const int N2 = N * N, N3 = N2 * N;
+    for (int q = threadIdx.x; q < N2; q += blockDim.x) D[q] = Dg[q];
+    __syncthreads();
+    const int64_t e = blockIdx.x;
+    const double* g = G + e * 6 * N3;
+    for (int pt = threadIdx.x; pt < N3; pt += blockDim.x) {
+        const int i = pt % N, j = (pt / N) % N, k = pt / N2;
+        double s = 0.0;
+        for (int a = 0; a < N; ++a) {
+            s += D[a * N + i] * D[a * N + i] * g[0 * N3 + k * N2 + j * N + a];
+            s += D[a * N + j] * D[a * N + j] * g[3 * N3 + k * N2 + a * N + i];
+            s += D[a * N + k] * D[a * N + k] * g[5 * N3 + a * N2 + j * N + i];
+        }
+        const double di = D[i * N + i], dj = D[j * N + j], dk = D[k * N + k];
+        s += 2.0 * (di * dj * g[1 * N3 + pt] + di * dk * g[2 * N3 + pt] + dj * dk * g[4 * N3 + pt]);
+        d[e * N3 + pt] = s;
+    }
+}
+
+// masked -> 1, dinv = 1/d, dinv32 = RN32(dinv) (C11)
+__global__ void __launch_bounds__(256) k_finish_dinv(MeshView m, double* d, float* d32)
+{
+    const int N = m.N, N3 = N * N * N;
+    const int64_t n = m.E * N3;
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
+         L += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = (uint32_t)(L / N3);
+        const int rem = (int)(L - (int64_t)e * N3);
+        ElemCoord ec = elem_coord(m, e);
+        double v = d[L];
+        if (is_masked(m, ec, rem % N, (rem / N) % N, rem / (N * N))) v = 1.0;
+        const double inv = 1.0 / v;
+        d[L] = inv;
+        if (d32) d32[L] = __double2float_rn(inv);
+    }
+}
+
+cudaError_t local_diag(nbk_ctx* ctx, double* d)
+{
+    k_local_diag<<<(unsigned)ctx->E, 256, 0, ctx->stream>>>(ctx->G64, ctx->D64, ctx->N, d);
+    return cudaGetLastError();
+}
+
+cudaError_t finish_dinv(nbk_ctx* ctx, double* d)
+{
+    k_finish_dinv<<<grid_for(ctx->n), 256, 0, ctx->stream>>>(ctx->view, d, ctx->dinv32);
     return cudaGetLastError();
 }
 

@@ -23,12 +23,14 @@ NBK_OK, NBK_EINVAL, NBK_EDEFECT, NBK_ECUDA, NBK_ENCCL, NBK_ENOMEM, NBK_ESTATE = 
 NBK_FP64, NBK_FP32 = 0, 1
 AX_LOCAL, AX_DSSUM, AX_MASK = 0, 1, 2
 PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32}
+PRECOND = {"none": 0, "jacobi": 1}
 
 # every symbol include/nbk.h declares
 SYMBOLS = ["nbk_workspace_bytes", "nbk_partition", "nbk_nccl_unique_id", "nbk_cg_setup",
            "nbk_load_arrays", "nbk_get_arrays", "nbk_ax_apply", "nbk_dssum", "nbk_glsc3",
            "nbk_cg_solve", "nbk_cg_solve_host", "nbk_get_solution", "nbk_solution_ptr",
-           "nbk_set_profiling", "nbk_query", "nbk_solve_launches", "nbk_group_link",
+           "nbk_set_precond", "nbk_load_precond", "nbk_get_precond", "nbk_set_profiling",
+           "nbk_query", "nbk_solve_launches", "nbk_group_link",
            "nbk_group_ax_apply", "nbk_group_dssum", "nbk_group_glsc3", "nbk_group_cg_solve",
            "nbk_last_error", "nbk_version", "nbk_destroy"]
 
@@ -98,6 +100,9 @@ def load() -> ctypes.CDLL:
         "nbk_get_solution": [vp, vp],
         "nbk_solution_ptr": [vp, ctypes.c_int, P(vp)],
         "nbk_set_profiling": [vp, i32],
+        "nbk_set_precond": [vp, i32],
+        "nbk_load_precond": [vp, vp],
+        "nbk_get_precond": [vp, vp],
         "nbk_query": [vp, P(CInfo)],
         "nbk_solve_launches": [vp, i32, ctypes.c_int, P(i64)],
     }
@@ -265,6 +270,20 @@ class Context:
                                   PREC[prec], ctypes.byref(out)), self._ctx)
         return float(out.value)
 
+    def set_precond(self, precond: str):
+        """'none' (z = r, the default) or 'jacobi' (z = r / diag(A))."""
+        _check(self.lib.nbk_set_precond(self._ctx, PRECOND[precond]), self._ctx)
+
+    def load_precond(self, dinv):
+        """Parity path: use the host array dinv (FP64, local storage) as 1/diag(A)."""
+        a = np.ascontiguousarray(dinv, dtype=np.float64)
+        _check(self.lib.nbk_load_precond(self._ctx, _ptr(a)), self._ctx)
+
+    def get_precond(self) -> np.ndarray:
+        out = np.zeros(self.shape)
+        _check(self.lib.nbk_get_precond(self._ctx, _ptr(out)), self._ctx)
+        return out
+
     def set_profiling(self, on: bool):
         _check(self.lib.nbk_set_profiling(self._ctx, int(on)), self._ctx)
 
@@ -372,6 +391,14 @@ class Group:
 
     def solution(self) -> np.ndarray:
         return np.concatenate([c.solution() for c in self.ctxs], axis=0)
+
+    def set_precond(self, precond: str):
+        for c in self.ctxs:
+            c.set_precond(precond)
+
+    def load_precond(self, dinv_slabs):
+        for c, d in zip(self.ctxs, dinv_slabs):
+            c.load_precond(d)
 
 
 def version() -> str:
