@@ -232,7 +232,7 @@ def time_solves(ctx, torch, cfg, precision, steps, warmup, flush, profile):
     s = ctx.stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(steps)]
-    kA = []
+    kA, kBC = [], []
     ctx.sync()
     graph_ms = []
     for i in range(steps):
@@ -241,9 +241,11 @@ def time_solves(ctx, torch, cfg, precision, steps, warmup, flush, profile):
         hist, _, res = ctx.cg_solve(cfg.niter, precision, trace=False)
         ev[i][1].record(s)
         kA.append(res["kA_ms"])
+        kBC.append((res["kB_ms"], res["kC_ms"]))
         graph_ms.append(res["solve_ms"])
     ctx.sync()
     ms = [a.elapsed_time(b) for a, b in ev]
+    time_solves.kBC = kBC
     return ms, kA, graph_ms, res, hist
 
 
@@ -322,6 +324,15 @@ def run_gpu(args):
     ka_avg_ms = sum(kA) / (args.steps * cfg.niter)
     peak, peak_src = measured_peak()
     achieved = bytes_ka / (ka_avg_ms / 1e3) / 1e9
+    kb_ms = sum(x[0] for x in time_solves.kBC) / (args.steps * cfg.niter)
+    kc_ms = sum(x[1] for x in time_solves.kBC) / (args.steps * cfg.niter)
+    s_b = 4 if prec == "fp32" else 8
+    info0 = ctx.info
+    phi0, psi0 = info0["n_copies"] / n, info0["n_shared"] / n
+    kernels = {"K_A_ms": ka_avg_ms, "K_B_ms": kb_ms, "K_C_ms": kc_ms,
+               "K_B_alg_GBps": n * (phi0 * (2 * s_b + 4) + psi0 * (s_b + 4)) / (kb_ms / 1e3) / 1e9,
+               "K_C_alg_GBps": 3 * s_b * n / (kc_ms / 1e3) / 1e9,
+               "timing": "CUDA events between the kernels of every iteration (profiling replay)"}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config, prec),
                 "kernel": "k_ax<fused> (p,x update + ax_e + mask + interior pap)",
@@ -443,7 +454,8 @@ def run_gpu(args):
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "true_res_rel": res["true_res_rel"],
             "h_final_rel": float(hist[-1] / hist[0]) if hist[0] else 0.0,
-            "median_step_ms": statistics.median(ms), "iteration_model": model, **extra,
+            "median_step_ms": statistics.median(ms), "iteration_model": model,
+            "kernels": kernels, **extra,
             "other_configs": others or None}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -104,7 +104,9 @@ typedef struct {
     int32_t defect_iter;  /* first iteration with pap <= 0 or a non-finite scalar, 0   */
     int32_t niter;
     float solve_ms;       /* device time of the CG loop (CUDA events)                  */
-    float kA_ms;          /* summed device time of the fused ax kernel (if profiling)  */
+    float kA_ms;          /* summed device time of the fused ax kernel K_A (if profiling) */
+    float kB_ms;          /* ... of the dssum phase K_B (+ face exchange when multi-rank) */
+    float kC_ms;          /* ... of the r update K_C (+ all-gather when multi-rank)       */
 } nbk_result;
 
 typedef struct nbk_ctx nbk_ctx;

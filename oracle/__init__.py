@@ -78,6 +78,12 @@ def lib():
         for nm in ("ora_pcg64", "ora_pcg32"):
             getattr(L, nm).restype = ctypes.c_int
             getattr(L, nm).argtypes = [ctypes.c_int] * 4 + [_p] * 4 + [ctypes.c_int] + [_p] * 3
+        L.ora_cg32s.restype = ctypes.c_int
+        L.ora_cg32s.argtypes = [ctypes.c_int] * 4 + [_p] * 4 + [ctypes.c_int] + [_p] * 3
+        L.ora_glsc3_32s.restype = ctypes.c_float
+        L.ora_glsc3_32s.argtypes = [c_i64, _p, _p, _p]
+        L.ora_fsum32.restype = ctypes.c_float
+        L.ora_fsum32.argtypes = [c_i64, _p]
         L.ora_jacobi_dinv.restype = None
         L.ora_jacobi_dinv.argtypes = [ctypes.c_int] * 4 + [_p] * 4
         L.ora_true_residual.restype = c_dbl
@@ -210,6 +216,20 @@ def fsum(t) -> float:
     return float(lib().ora_fsum(t.size, _ptr(t)))
 
 
+def glsc3_single(a, b, c) -> float:
+    """Paper-literal binary32 glsc3 (NEXT-2): RN32 of the exact sum of RN32(a b) c."""
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    return float(lib().ora_glsc3_32s(a.size, _ptr(a), _ptr(b), _ptr(c)))
+
+
+def fsum32(t) -> float:
+    """RN32 of the exact sum of binary64 terms."""
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    return float(lib().ora_fsum32(t.size, _ptr(t)))
+
+
 def glsc3(a, b, c) -> float:
     a = np.ascontiguousarray(a)
     b = np.ascontiguousarray(b)
@@ -239,8 +259,9 @@ def jacobi_dinv(mesh: Mesh, D, G):
 
 
 def cg(mesh: Mesh, D, G, f, niter: int, precision: str = "fp64", dinv=None) -> CgResult:
-    """Fixed-iteration CG (T1).  precision 'fp64' or 'fp32' (mixed: FP64 set-up
-    data rounded once to binary32, FP64 accumulation of glsc3).  dinv (FP64
+    """Fixed-iteration CG (T1).  precision 'fp64', 'fp32' (mixed: FP64 set-up
+    data rounded once to binary32, FP64 accumulation of glsc3) or 'fp32s'
+    (paper-literal single: binary32 inner products and scalars).  dinv (FP64
     local array) selects Jacobi PCG: z = r * dinv (dinv rounded to the loop's
     precision), rtz1 = glsc3(r, c, z)."""
     D = np.ascontiguousarray(D, np.float64)
@@ -249,6 +270,12 @@ def cg(mesh: Mesh, D, G, f, niter: int, precision: str = "fp64", dinv=None) -> C
     hist = np.zeros(niter + 1)
     trace = np.zeros((niter, 5))
     L = lib()
+    if precision == "fp32s":  # paper-literal single precision (NEXT-2)
+        di = None if dinv is None else np.ascontiguousarray(dinv, np.float64)
+        x = np.zeros(f.shape, np.float32)
+        rc = L.ora_cg32s(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), _ptr(di), niter, _ptr(x),
+                         _ptr(hist), _ptr(trace))
+        return CgResult(x=x, hist=hist, trace=trace, defect=int(rc))
     if dinv is not None:
         di = np.ascontiguousarray(dinv, np.float64)
         if precision == "fp64":

@@ -553,6 +553,60 @@ double ora_fsum(int64_t n, const double* t)
 DEFINE_GLSC3(ora_glsc3_64, double)
 DEFINE_GLSC3(ora_glsc3_32, float)
 
+/* RN32 of the exact sum held in an expansion: h = RN64(S); RN32(h) equals
+ * RN32(S) unless h is exactly half-way between two binary32 neighbours and
+ * S != h, in which case the sign of S - h (from the expansion) decides. */
+static float xsum_round32(const xsum* s)
+{
+    double h = xsum_round(s);
+    float f = (float)h;
+    if (!isfinite(h) || (double)f == h) return f;
+    float a = nextafterf(f, h > (double)f ? INFINITY : -INFINITY);
+    double mid = ((double)f + (double)a) * 0.5;  /* exact: two binary32 values */
+    if (h != mid) return f;
+    xsum t = *s;
+    xsum_add(&t, -h);
+    double r = xsum_round(&t);
+    if (r == 0.0) return f;  /* exact tie: (float)h rounded half to even */
+    return r > 0.0 ? (f > a ? f : a) : (f < a ? f : a);
+}
+
+/* Paper-literal single-precision glsc3 ("solver
+ * runs exclusively in single", P:507 math.f in single; reading R11b in
+ * DESIGN.md): terms RN32(a_L b_L) c_L (c = 1/m exact), the sum rounded once
+ * to binary32 -- the best a binary32 accumulator can return. */
+float ora_glsc3_32s(int64_t n, const float* a, const float* b, const double* c)
+{
+    int64_t nch = (n + CHUNK - 1) / CHUNK;
+    xsum* part = (xsum*)malloc(sizeof(xsum) * (nch > 0 ? nch : 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        xsum_init(&part[ch]);
+        int64_t lo = ch * CHUNK, hi = lo + CHUNK < n ? lo + CHUNK : n;
+        for (int64_t L = lo; L < hi; ++L) {
+            float ab = a[L] * b[L];
+            xsum_add(&part[ch], (double)ab * c[L]);
+        }
+    }
+    xsum tot;
+    xsum_init(&tot);
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        if (part[ch].has_special) { tot.special += part[ch].special; tot.has_special = 1; }
+        for (int q = 0; q < part[ch].n; ++q) xsum_add(&tot, part[ch].p[q]);
+    }
+    free(part);
+    return xsum_round32(&tot);
+}
+
+/* RN32 of an exact sum of binary64 terms (pins the GPU's dd -> binary32 step) */
+float ora_fsum32(int64_t n, const double* t)
+{
+    xsum s;
+    xsum_init(&s);
+    for (int64_t i = 0; i < n; ++i) xsum_add(&s, t[i]);
+    return xsum_round32(&s);
+}
+
 /* c = 1/m per local point of the whole mesh (R8) */
 static double* make_c(const ora_mesh* m)
 {
@@ -637,7 +691,7 @@ void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const doubl
 /* Returns the first iteration with pap <= 0 or a non-finite scalar     */
 /* (defect) or 0.                                                */
 /* ------------------------------------------------------------------ */
-#define DEFINE_CG(NAME, T, FMA, AXLOCAL, DSSUM, GLSC3)                                          \
+#define DEFINE_CG(NAME, T, S, FMA, SQRT, AXLOCAL, DSSUM, GLSC3)                                          \
     int NAME(int ex, int ey, int ez, int N, const T* D, const T* G, const T* f, const T* dinv,  \
              int niter, T* x, double* hist, double* trace)                                      \
     {                                                                                           \
@@ -649,17 +703,17 @@ void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const doubl
         T* w = (T*)malloc(sizeof(T) * n);                                                       \
         T* z = dinv ? (T*)malloc(sizeof(T) * n) : r;                                            \
         for (int64_t L = 0; L < n; ++L) { x[L] = 0; r[L] = f[L]; p[L] = 0; }                    \
-        double rtr = GLSC3(n, r, r, c);                                                         \
-        hist[0] = sqrt(rtr);                                                                    \
-        double rtz = rtr;                                                                       \
+        S rtr = GLSC3(n, r, r, c);                                                              \
+        hist[0] = (double)SQRT(rtr);                                                            \
+        S rtz = rtr;                                                                            \
         if (dinv) {                                                                             \
             for (int64_t L = 0; L < n; ++L) z[L] = r[L] * dinv[L];                              \
             rtz = GLSC3(n, r, z, c);                                                            \
         }                                                                                       \
-        double rtz2 = 0.0;                                                                      \
+        S rtz2 = 0;                                                                             \
         int defect = 0, zero = 0;                                                               \
         for (int k = 1; k <= niter; ++k) {                                                      \
-            double rtz1 = rtz, beta = 0.0, alpha = 0.0, pap;                                    \
+            S rtz1 = rtz, beta = 0, alpha = 0, pap;                                             \
             if (rtz1 == 0.0) zero = 1;                                                          \
             if (!zero && k > 1) beta = rtz1 / rtz2;                                             \
             T betaT = (T)beta;                                                                  \
@@ -672,7 +726,7 @@ void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const doubl
             for (int64_t L = 0; L < n; ++L) x[L] = FMA(alphaT, p[L], x[L]);                     \
             for (int64_t L = 0; L < n; ++L) r[L] = FMA(alphmT, w[L], r[L]);                     \
             rtr = GLSC3(n, r, r, c);                                                            \
-            hist[k] = sqrt(rtr);                                                                \
+            hist[k] = (double)SQRT(rtr);                                                        \
             rtz = rtr;                                                                          \
             if (dinv) {                                                                         \
                 for (int64_t L = 0; L < n; ++L) z[L] = r[L] * dinv[L];                          \
@@ -692,8 +746,11 @@ void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const doubl
         return defect;                                                                          \
     }
 
-DEFINE_CG(ora_cg64_core, double, fma, ora_ax_local64, ora_dssum64, ora_glsc3_64)
-DEFINE_CG(ora_cg32_core, float, fmaf, ora_ax_local32, ora_dssum32, ora_glsc3_32)
+DEFINE_CG(ora_cg64_core, double, double, fma, sqrt, ora_ax_local64, ora_dssum64, ora_glsc3_64)
+DEFINE_CG(ora_cg32_core, float, double, fmaf, sqrt, ora_ax_local32, ora_dssum32, ora_glsc3_32)
+/* paper-literal single precision: binary32 inner products (above) and binary32
+ * scalars: beta = rtz1/rtz2, alpha = rtz1/pap, sqrt in binary32 (NEXT-2) */
+DEFINE_CG(ora_cg32s_core, float, float, fmaf, sqrtf, ora_ax_local32, ora_dssum32, ora_glsc3_32s)
 
 int ora_cg64(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,
              int niter, double* x, double* hist, double* trace)
@@ -716,6 +773,29 @@ int ora_cg32(int ex, int ey, int ez, int N, const double* D, const double* G, co
     for (int64_t q = 0; q < n; ++q) f32[q] = (float)f[q];
     int rc = ora_cg32_core(ex, ey, ez, N, D32, G32, f32, NULL, niter, x32, hist, trace);
     free(D32); free(G32); free(f32);
+    return rc;
+}
+
+/* Paper-literal single-precision solver (NEXT-2): as ora_cg32 / ora_pcg32
+ * but the inner products and the CG scalars are binary32 too (dinv may be
+ * NULL: unpreconditioned). */
+int ora_cg32s(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,
+              const double* dinv, int niter, float* x32, double* hist, double* trace)
+{
+    int64_t E = (int64_t)ex * ey * ez, nn = (int64_t)N * N * N, n = E * nn;
+    float* D32 = (float*)malloc(sizeof(float) * N * N);
+    float* G32 = (float*)malloc(sizeof(float) * 6 * n);
+    float* f32 = (float*)malloc(sizeof(float) * n);
+    float* di32 = dinv ? (float*)malloc(sizeof(float) * n) : NULL;
+    for (int q = 0; q < N * N; ++q) D32[q] = (float)D[q];
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < 6 * n; ++q) G32[q] = (float)G[q];
+    for (int64_t q = 0; q < n; ++q) {
+        f32[q] = (float)f[q];
+        if (di32) di32[q] = (float)dinv[q];
+    }
+    int rc = ora_cg32s_core(ex, ey, ez, N, D32, G32, f32, di32, niter, x32, hist, trace);
+    free(D32); free(G32); free(f32); free(di32);
     return rc;
 }
 

@@ -473,7 +473,7 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
     int rev = 0;
     for (int k = 1; k <= niter; ++k) {
         const bool prof = g && profiling && P == 1;
-        if (prof) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1)], s, cudaEventRecordExternal);
+        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1)], s, cudaEventRecordExternal);
         const bool pdl = !prof;  // events between kernels break PDL edges
         for (size_t q = 0; q < P; ++q) {
             nbk_ctx* c = t.m[q];
@@ -485,11 +485,13 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             e = jac ? launch_ax<T, 2>(aa, s, false, pdl) : launch_ax<T, 1>(aa, s, false, pdl);
             if (e != cudaSuccess) return e;
         }
-        if (prof) cudaEventRecordWithFlags(g->prof_events[2 * (k - 1) + 1], s, cudaEventRecordExternal);
+        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 1], s, cudaEventRecordExternal);
         if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err, !rev)) != cudaSuccess) return e;
+        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 2], s, cudaEventRecordExternal);
         for (size_t q = 0; q < P; ++q) vr[q].rev = rev;
         e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pdl, err) : vec_team<T, VEC_RUPD>(t, vr, pdl, err);
         if (e != cudaSuccess) return e;
+        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 3], s, cudaEventRecordExternal);
         rev = !rev;
         launches += (int64_t)P * (3 + nface + 2 * per_fin);
     }
@@ -528,7 +530,7 @@ static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_gr
     if (it != c->graphs.end()) { *out = &it->second; return NBK_OK; }
     nbk_graph g;
     if (c->profiling && t.m.size() == 1) {
-        g.prof_events.resize(2 * niter);
+        g.prof_events.resize(4 * niter);
         for (auto& ev : g.prof_events) NBK_CUDA(c, cudaEventCreate(&ev));
     }
     NBK_CUDA(c, cudaStreamBeginCapture(t.s, cudaStreamCaptureModeThreadLocal));
@@ -697,14 +699,21 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
         result->defect_iter = hs.defect;
         result->niter = niter;
         float ka = 0.f;
+        float kb = 0.f, kc = 0.f;
         if (c->profiling && !g->prof_events.empty()) {
             for (int k = 0; k < niter; ++k) {
-                float tk = 0.f;
-                cudaEventElapsedTime(&tk, g->prof_events[2 * k], g->prof_events[2 * k + 1]);
-                ka += tk;
+                float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+                cudaEventElapsedTime(&t0, g->prof_events[4 * k], g->prof_events[4 * k + 1]);
+                cudaEventElapsedTime(&t1, g->prof_events[4 * k + 1], g->prof_events[4 * k + 2]);
+                cudaEventElapsedTime(&t2, g->prof_events[4 * k + 2], g->prof_events[4 * k + 3]);
+                ka += t0;
+                kb += t1;
+                kc += t2;
             }
         }
         result->kA_ms = ka;
+        result->kB_ms = kb;
+        result->kC_ms = kc;
     }
     return hs.defect ? fail(c, NBK_EDEFECT, "CG defect: pap <= 0 or non-finite scalar") : NBK_OK;
 }

@@ -63,7 +63,8 @@ class CInfo(ctypes.Structure):
 class CResult(ctypes.Structure):
     _fields_ = [("true_res", ctypes.c_double), ("true_res_rel", ctypes.c_double),
                 ("defect_iter", ctypes.c_int32), ("niter", ctypes.c_int32),
-                ("solve_ms", ctypes.c_float), ("kA_ms", ctypes.c_float)]
+                ("solve_ms", ctypes.c_float), ("kA_ms", ctypes.c_float),
+                ("kB_ms", ctypes.c_float), ("kC_ms", ctypes.c_float)]
 
 
 _lib = None

@@ -563,3 +563,64 @@ def test_pcg_scaled_problem_equivalence(ora):
         dd = (eg - xg)[~mg]
         errs.append(dd @ Ai @ dd)
     assert all(errs[i + 1] <= errs[i] * (1 + 1e-9) + 1e-28 for i in range(len(errs) - 1))
+
+
+# ------------------------------------ paper-literal single precision (NEXT-2)
+def _rn32_exact(terms):
+    """RN32 (ties to even) of the exact rational sum of binary64 terms."""
+    from fractions import Fraction
+    S = sum(Fraction(float(t)) for t in terms)
+    c = np.float32(float(S))
+    cands = [np.nextafter(c, np.float32(-np.inf)), c, np.nextafter(c, np.float32(np.inf))]
+    even = lambda v: int(np.frombuffer(np.float32(v).tobytes(), np.uint32)[0]) & 1  # noqa: E731
+    return float(min(cands, key=lambda v: (abs(Fraction(float(v)) - S), even(v))))
+
+
+def test_fsum32_is_correctly_rounded(ora):
+    """The binary32 rounding of an exact sum (used by the single-precision glsc3)
+    equals the rational-arithmetic RN32, including sums that land exactly on a
+    binary32 half-way point and half-way points perturbed by 2^-80."""
+    g = inputs.rng(3)
+    for trial in range(1500):
+        if trial % 3 == 0:
+            f = np.float32(g.standard_normal())
+            a = np.nextafter(f, np.float32(np.inf))
+            mid = (float(f) + float(a)) / 2
+            terms = [mid, float(g.choice([-1.0, 0.0, 1.0])) * 2.0 ** -80, 0.0]
+        else:
+            n = int(g.integers(1, 8))
+            terms = g.standard_normal(n) * np.exp2(g.integers(-40, 40, n))
+        assert ora.fsum32(terms) == _rn32_exact(terms)
+
+
+def test_glsc3_single_examples_and_definition(ora):
+    """S:336-337 examples in binary32, and the definition RN32(sum RN32(a b) c)."""
+    one = np.ones(3, np.float32)
+    assert ora.glsc3_single(one, one, np.ones(3)) == 3.0
+    assert ora.glsc3_single(np.array([1, 2], np.float32), np.array([3, 4], np.float32),
+                            np.array([1.0, 0.5])) == 7.0
+    a = inputs.uniform_field(5000, 1, np.float32, -3, 3)
+    b = inputs.uniform_field(5000, 2, np.float32)
+    c = inputs.rng(5).choice([1.0, 0.5, 0.25, 0.125], 5000)
+    terms = (a * b).astype(np.float64) * c   # a*b in binary32 (numpy float32 product)
+    assert ora.glsc3_single(a, b, c) == _rn32_exact(terms)
+
+
+def test_single_solver_plausibility(ora):
+    """The paper-literal single solver tracks FP64 early, converges to the
+    binary32 floor, and f = 0 gives x = 0."""
+    m = ora.Mesh(2, 2, 2, 8, seed_rhs=1001)
+    _, _, D = ora.gll(8)
+    s = ora.setup(m, want=("G", "f"))
+    r64 = ora.cg(m, D, s["G"], s["f"], 60, "fp64")
+    r1 = ora.cg(m, D, s["G"], s["f"], 60, "fp32s")
+    assert r1.defect == 0
+    rel = np.abs(r1.hist[:15] - r64.hist[:15]) / r64.hist[:15]
+    assert rel.max() < 1e-3
+    # scalars are binary32 values
+    assert (r1.trace.astype(np.float32).astype(np.float64) == r1.trace).all()
+    assert (r1.hist.astype(np.float32).astype(np.float64) == r1.hist).all()
+    tr, h0 = ora.true_residual(m, D, s["G"], s["f"], r1.x)
+    assert 1e-9 < tr / h0 < 1e-3
+    z = ora.cg(m, D, s["G"], np.zeros_like(s["f"]), 5, "fp32s")
+    assert (z.hist == 0).all() and (z.x == 0).all()
