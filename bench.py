@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="nbk", choices=["nbk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp64", action="store_true")
+    ap.add_argument("--no-accuracy", dest="accuracy", action="store_false",
+                    help="skip the FP32 / paper-literal single accuracy report")
     ap.add_argument("--no-jacobi", dest="jacobi", action="store_false",
                     help="skip the Jacobi-PCG measurement beside the headline")
     ap.add_argument("--others", default="C3,C4,C5",
@@ -368,6 +370,33 @@ def run_gpu(args):
                                "fp64_over_fp32": en64.joules / en32.joules,
                                "note": "NVML total energy over warm-up + timed solves of each "
                                        "solver (same step counts)"}
+
+    # ---- accuracy of the single-precision solvers vs FP64 (P:517-522 AE / MAE; NEXT-2) ----
+    if args.accuracy and world == 1:
+        import numpy as np
+        with torch.cuda.stream(stream):
+            h = {}
+            xs = {}
+            rs = {}
+            for p_ in ("fp64", "fp32", "fp32s"):
+                h[p_], _, rs[p_] = ctx.cg_solve(cfg.niter, p_, trace=False)
+                xs[p_] = ctx.solution()
+            ms1, _, _, _, _ = time_solves(ctx, torch, cfg, "fp32s", args.steps, args.warmup, flush,
+                                          profile=False)
+        acc = {}
+        for p_ in ("fp32", "fp32s"):
+            ae = np.abs(h[p_][1:] - h["fp64"][1:])
+            acc[p_] = {"MAE": float(ae.mean()), "AE_max": float(ae.max()),
+                       "MAE_rel_h0": float(ae.mean() / h["fp64"][0]),
+                       "true_res_rel": rs[p_]["true_res_rel"],
+                       "x_err_vs_fp64": float(np.abs(xs[p_] - xs["fp64"]).max() /
+                                              np.abs(xs["fp64"]).max())}
+        acc["fp64_true_res_rel"] = rs["fp64"]["true_res_rel"]
+        acc["fp32s_value"] = ng * cfg.niter * args.steps / (sum(ms1) / 1e3) / 1e9
+        acc["note"] = ("fp32: north_star mixed solver (FP64 inner-product accumulation); fp32s: "
+                       "paper-literal single (binary32 inner products and scalars, R11b)")
+        extra["accuracy"] = acc
+        del np
 
     # ---- Jacobi PCG beside it: same workload, z = r / diag(A) ----
     if args.jacobi:

@@ -46,8 +46,11 @@ typedef enum {
 
 typedef enum {
     NBK_FP64 = 0, /* FP64 CG solver (Nekbone's reference precision)                        */
-    NBK_FP32 = 1  /* mixed: FP64 set-up, FP32 CG loop with FP64 inner-product accumulation
+    NBK_FP32 = 1, /* mixed: FP64 set-up, FP32 CG loop with FP64 inner-product accumulation
                      (north_star; reading R11), FP64 final residual check (C12)          */
+    NBK_FP32S = 2 /* paper-literal single: as
+                     NBK_FP32 but inner products RN32(sum RN32(a b) c) and the scalars
+                     alpha, beta, sqrt in binary32 (cg_solve and glsc3 only)           */
 } nbk_precision;
 
 /* Box mesh (reading R5): cubic elements of edge h = 1/ex on

@@ -342,7 +342,7 @@ static dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - 2 * NBK_VEC_GRI
 // k_fin (rank-ordered combination, alpha).
 template <typename T, bool FUSED>
 static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std::vector<const T*>& p,
-                              int mask, bool pdl, std::string& err, int rev = 0)
+                              int mask, bool pdl, std::string& err, int rev = 0, int single = 0)
 {
     cudaError_t e;
     const cudaStream_t s = t.s;
@@ -351,6 +351,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         DssumArgs<T> d = dssum_args<T>(c, w[q]);
         d.mask = mask;
         d.rev = rev;
+        d.single = single;
         if (FUSED) {
             d.p = p[q];
             d.parts = c->parts;
@@ -370,6 +371,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         nbk_ctx* c = t.m[q];
         FaceArgs<T> f = face_args<T>(c, w[q]);
         f.mask = mask;
+        f.single = single;
         if (FUSED) {
             f.p = p[q];
             f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED>((int)c->ntiles);
@@ -381,7 +383,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
     if (FUSED) {
         if ((e = xchg_gather(t, s, err)) != cudaSuccess) return e;
         for (nbk_ctx* c : t.m) {
-            k_fin<0><<<1, 32, 0, s>>>(c->gather, c->nranks, c->st, c->hist, c->trace);
+            k_fin<0><<<1, 32, 0, s>>>(c->gather, c->nranks, c->st, c->hist, c->trace, single);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
     }
@@ -404,7 +406,8 @@ static cudaError_t vec_team(const Team& t, const std::vector<VecArgs<T>>& args, 
     if ((e = xchg_gather(t, t.s, err)) != cudaSuccess) return e;
     for (size_t q = 0; q < t.m.size(); ++q) {
         nbk_ctx* c = t.m[q];
-        k_fin<1 + MODE><<<1, 32, 0, t.s>>>(c->gather, c->nranks, c->st, c->hist, c->trace);
+        k_fin<1 + MODE><<<1, 32, 0, t.s>>>(c->gather, c->nranks, c->st, c->hist, c->trace,
+                                          args[q].single);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -439,7 +442,7 @@ static cudaError_t ax_team(const Team& t, const std::vector<const T*>& u, const 
 // Enqueue one CG solve (T1 loop, fixed niter) for the team; used under capture.
 template <typename T>
 static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp32, bool profiling,
-                                 std::string& err)
+                                 std::string& err, int single = 0)
 {
     const cudaStream_t s = t.s;
     const size_t P = t.m.size();
@@ -462,6 +465,7 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
         vi[q] = vec_args<T>(t.m[q]);
         vi[q].r = r[q]; vi[q].x = x[q]; vi[q].p = p[q]; vi[q].f = t.m[q]->f64;
         vi[q].dinv = fld<T>(t.m[q], 4, fp32);
+        vi[q].single = single;
         vr[q] = vi[q];
         vr[q].w = w[q];
     }
@@ -482,11 +486,12 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             aa.u = nullptr; aa.w = w[q]; aa.p = p[q]; aa.r = r[q]; aa.x = x[q]; aa.mask = 1;
             aa.rev = rev;
             aa.dinv = fld<T>(c, 4, fp32);
+            aa.single = single;
             e = jac ? launch_ax<T, 2>(aa, s, false, pdl) : launch_ax<T, 1>(aa, s, false, pdl);
             if (e != cudaSuccess) return e;
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err, !rev)) != cudaSuccess) return e;
+        if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err, !rev, single)) != cudaSuccess) return e;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 2], s, cudaEventRecordExternal);
         for (size_t q = 0; q < P; ++q) vr[q].rev = rev;
         e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pdl, err) : vec_team<T, VEC_RUPD>(t, vr, pdl, err);
@@ -535,8 +540,9 @@ static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_gr
     }
     NBK_CUDA(c, cudaStreamBeginCapture(t.s, cudaStreamCaptureModeThreadLocal));
     std::string err;
-    cudaError_t e = prec == NBK_FP32 ? enqueue_solve<float>(t, niter, &g, true, c->profiling, err)
-                                     : enqueue_solve<double>(t, niter, &g, false, c->profiling, err);
+    cudaError_t e = prec == NBK_FP64 ? enqueue_solve<double>(t, niter, &g, false, c->profiling, err)
+                                     : enqueue_solve<float>(t, niter, &g, true, c->profiling, err,
+                                                            prec == NBK_FP32S ? 1 : 0);
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(t.s, &graph);
     if (e != cudaSuccess) {
@@ -581,13 +587,14 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
 // glsc3 over a team (synchronous); result identical on every member.
 template <typename T>
 static nbk_status glsc3_team(const Team& t, const std::vector<const T*>& a, const std::vector<const T*>& b,
-                             double* out)
+                             double* out, int single = 0)
 {
     nbk_ctx* c0 = t.m[0];
     std::vector<VecArgs<T>> v(t.m.size());
     for (size_t q = 0; q < t.m.size(); ++q) {
         v[q] = vec_args<T>(t.m[q]);
         v[q].a = a[q]; v[q].b = b[q];
+        v[q].single = single;
     }
     std::string err;
     cudaError_t e = vec_team<T, VEC_DOT>(t, v, false, err);
@@ -666,9 +673,9 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
 {
     nbk_ctx* c = t.m[0];
     if (niter < 1 || niter > NBK_MAX_NITER) return fail(c, NBK_EINVAL, "niter out of range");
-    if (prec != NBK_FP64 && prec != NBK_FP32) return fail(c, NBK_EINVAL, "bad precision");
+    if (prec != NBK_FP64 && prec != NBK_FP32 && prec != NBK_FP32S) return fail(c, NBK_EINVAL, "bad precision");
     for (nbk_ctx* m : t.m)
-        if (prec == NBK_FP32 && !m->G32) return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
+        if (prec != NBK_FP64 && !m->G32) return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
     nbk_status st = refresh_h0(t);
     if (st != NBK_OK) return st;
     if (c->precond == NBK_PRECOND_JACOBI) {
@@ -997,10 +1004,10 @@ static nbk_status glsc3_team_abi(const Team& t, const void* const* a_dev, const 
         std::vector<const double*> a(P), b(P);
         for (size_t q = 0; q < P; ++q) { a[q] = (const double*)a_dev[q]; b[q] = (const double*)b_dev[q]; }
         return glsc3_team<double>(t, a, b, out);
-    } else if (prec == NBK_FP32) {
+    } else if (prec == NBK_FP32 || prec == NBK_FP32S) {
         std::vector<const float*> a(P), b(P);
         for (size_t q = 0; q < P; ++q) { a[q] = (const float*)a_dev[q]; b[q] = (const float*)b_dev[q]; }
-        return glsc3_team<float>(t, a, b, out);
+        return glsc3_team<float>(t, a, b, out, prec == NBK_FP32S ? 1 : 0);
     }
     return fail(c, NBK_EINVAL, "bad precision");
 }
@@ -1130,7 +1137,7 @@ nbk_status nbk_solve_launches(const nbk_ctx* c, int32_t niter, nbk_precision pre
     const int64_t multi = c->nranks > 1 ? 1 : 0;
     // init (+fin), per iteration K_A, K_B, K_C (+ pack, merge, 2 fin), tail_x, [upcast],
     // final check K_A, K_B, K_C (+ pack, merge, fin)
-    *launches = (1 + multi) + (3 + 4 * multi) * (int64_t)niter + 1 + (prec == NBK_FP32 ? 1 : 0) +
+    *launches = (1 + multi) + (3 + 4 * multi) * (int64_t)niter + 1 + (prec != NBK_FP64 ? 1 : 0) +
                 (3 + 3 * multi);
     return NBK_OK;
 }

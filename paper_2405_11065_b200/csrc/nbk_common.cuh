@@ -222,6 +222,29 @@ __device__ __forceinline__ double dot_term(float a, float b, double c)
 {
     return __dmul_rn(__dmul_rn((double)a, (double)b), c);
 }
+// Paper-literal single-precision glsc3 (NEXT-2): the product rounded to
+// binary32 first, RN32(a b) c (c = 1/m, exact).  FP64 vectors: unchanged.
+__device__ __forceinline__ double dot_term(float a, float b, double c, bool single)
+{
+    return single ? __dmul_rn((double)__fmul_rn(a, b), c) : dot_term(a, b, c);
+}
+__device__ __forceinline__ double dot_term(double a, double b, double c, bool)
+{
+    return dot_term(a, b, c);
+}
+
+// RN32 of the sum represented by a double-double (hi = RN64(hi + lo)): RN32(hi)
+// unless hi lies exactly half-way between two binary32 neighbours, where the
+// sign of lo (the rest of the sum) decides.
+__device__ __forceinline__ float dd_to_float_rn(double hi, double lo)
+{
+    const float f = __double2float_rn(hi);
+    if (!isfinite(hi) || (double)f == hi) return f;
+    const float a = nextafterf(f, hi > (double)f ? INFINITY : -INFINITY);
+    const double mid = __dmul_rn(__dadd_rn((double)f, (double)a), 0.5);
+    if (hi != mid || lo == 0.0) return f;
+    return lo > 0.0 ? fmaxf(f, a) : fminf(f, a);
+}
 
 template <typename T>
 __device__ __forceinline__ T fma_t(T a, T b, T c);
@@ -311,7 +334,7 @@ struct CgState {
     double beta;       // beta of the current iteration (for the p update)
     double alpha;      // alpha of the latest completed pap (x update, r update)
     double alpham;     // -alpha
-    float beta32, alpha32, alpham32, pad0;
+    float beta32, alpha32, alpham32, pad0;   // RN32 of the FP64 scalars, or (single mode) the scalars
     double true_rtr;   // glsc3(f - A x, c, f - A x) of the final FP64 check
     double dot;        // result slot of the standalone glsc3
     int it;            // current iteration k (1-based)

@@ -131,6 +131,7 @@ struct AxArgs {
     T* x;              // fused: x (in/out)
     const CgState* st; // fused: beta, alpha_prev
     const T* dinv;     // fused Jacobi PCG: z = r * dinv replaces r in the p update
+    int single;        // paper-literal single mode: pap terms RN32(w p) (NEXT-2)
     dd* parts;         // fused: pap partial per block
     MeshView mesh;
     int mask;          // assign +0 to Dirichlet points of w
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 // element-interior points (m == 1) contribute w p c here; shared
                 // nodes contribute once per node in K_B (bitwise-equal exact sum).
                 const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
-                if (!sxy && !sz) acc.add(dot_term(wv, ureg[k], 1.0));
+                if (!sxy && !sz) acc.add(dot_term(wv, ureg[k], 1.0, a.single));
             }
         }
     }
@@ -340,12 +341,19 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
 // CG scalars from the globally reduced inner products (rules C7, C9); run by
 // one thread: the last block of the reducing kernel (1 rank) or k_fin after
 // the rank-ordered combination of the per-rank partials (several ranks).
-__device__ __forceinline__ void fin_alpha(CgState* st, double pap, double* trace)
+__device__ __forceinline__ void fin_alpha(CgState* st, dd pap_dd, double* trace, bool single)
 {
     const int k = st->it;
     const double rtz1 = st->rtr;
-    double alpha = 0.0;
-    if (!st->zero) alpha = rtz1 / pap;                                   // C7
+    double alpha = 0.0, pap;
+    if (single) {  // NEXT-2: binary32 scalars (rtz1 already a binary32 value)
+        const float pap32 = dd_to_float_rn(pap_dd.hi, pap_dd.lo);
+        pap = pap32;
+        if (!st->zero) alpha = __fdiv_rn((float)rtz1, pap32);
+    } else {
+        pap = pap_dd.hi;
+        if (!st->zero) alpha = rtz1 / pap;                               // C7
+    }
     if (!st->zero && st->defect == 0 && (!(pap > 0.0) || !isfinite(pap)))
         st->defect = k;                                                  // C9
     st->alpha = alpha;
@@ -369,8 +377,13 @@ __host__ __device__ constexpr bool vec_jacobi(int mode) { return mode == VEC_INI
 // preconditioned product that drives alpha / beta (= rtr when z = r).
 // st->rtr holds the current rtz1.
 template <int MODE>
-__device__ __forceinline__ void fin_rtr(CgState* st, double rtr, double rtz, double* hist, double* trace)
+__device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, double* hist, double* trace,
+                                        bool single)
 {
+    // single mode (NEXT-2): binary32 sums, sqrt and division
+    const double rtr = single ? (double)dd_to_float_rn(rtr_dd.hi, rtr_dd.lo) : rtr_dd.hi;
+    const double rtz = single ? (double)dd_to_float_rn(rtz_dd.hi, rtz_dd.lo) : rtz_dd.hi;
+    const double h = single ? (double)__fsqrt_rn((float)rtr) : sqrt(rtr);
     if constexpr (MODE == VEC_INIT || MODE == VEC_INIT_J) {
         st->rtr = rtz;
         st->rtz2 = 0.0;
@@ -383,17 +396,20 @@ __device__ __forceinline__ void fin_rtr(CgState* st, double rtr, double rtz, dou
         st->zero = (rtz == 0.0);
         st->defect = 0;
         st->it = 1;
-        hist[0] = sqrt(rtr);
+        hist[0] = h;
     } else if constexpr (MODE == VEC_RUPD || MODE == VEC_RUPD_J) {
         const int k = st->it;
-        hist[k] = sqrt(rtr);                    // h_k (R13)
+        hist[k] = h;                            // h_k (R13)
         trace[5 * (int64_t)(k - 1) + 4] = rtr;
         if (!st->zero && st->defect == 0 && (!isfinite(rtr) || !isfinite(rtz))) st->defect = k;
         const double rtz1_next = rtz, rtz2_next = st->rtr;
         st->rtz2 = rtz2_next;
         st->rtr = rtz1_next;
         if (rtz1_next == 0.0) st->zero = 1;     // C9
-        const double beta = st->zero ? 0.0 : rtz1_next / rtz2_next;  // C7
+        double beta = 0.0;
+        if (!st->zero)
+            beta = single ? (double)__fdiv_rn((float)rtz1_next, (float)rtz2_next)
+                          : rtz1_next / rtz2_next;  // C7
         st->beta = beta;
         st->beta32 = (float)beta;
         st->it = k + 1;
@@ -430,6 +446,7 @@ struct DssumArgs {
     int mask;                 // standalone: assign +0 to masked shared nodes
     int fin;                  // fused: 1 = last block forms alpha (1 rank); 0 = publish only
     int rev;                  // visit the tiles in reverse order
+    int single;               // paper-literal single mode (NEXT-2)
     MeshView mesh;
 };
 
@@ -507,7 +524,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) a.w[ix[h][c]] = sum;
-                if constexpr (FUSED) acc.add(dot_term(sum, p0[h], 1.0));  // one term per node
+                if constexpr (FUSED) acc.add(dot_term(sum, p0[h], 1.0, a.single));  // one term per node
             }
         }
     }
@@ -532,7 +549,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_dssum(DssumArgs
         if (publish_and_check_last(a.parts, a.nA + blockIdx.x, v, &a.st->cnt[0], total)) {
             dd pap_dd = reduce_partials(a.parts, a.nA + (int)gridDim.x);
             if (threadIdx.x == 0) {
-                fin_alpha(a.st, pap_dd.hi, a.trace);
+                fin_alpha(a.st, pap_dd, a.trace, a.single);
                 a.st->cnt[0] = 0;
             }
         }
@@ -557,6 +574,7 @@ struct VecArgs {
     double* hist;
     double* trace;
     dd* slot;           // multi-rank: this rank's reduced partial (NULL: finalise here)
+    int single;         // paper-literal single mode: RN32(a b) terms, binary32 scalars
     int rev;            // visit the chunks in reverse order
     MeshView mesh;
 };
@@ -681,21 +699,21 @@ struct VecChunk {
             z.store(a.x + L);
             z.store(a.p + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
         } else if constexpr (MODE == VEC_RUPD) {
             VecT<T, V> r;
 #pragma unroll
             for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, A.v[t], B.v[t]);  // C8
             r.store(a.r + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
         } else if constexpr (MODE == VEC_TRUE) {
             VecT<T, V> r;
 #pragma unroll
             for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, A.v[t], (T)F.v[t]);  // C12
             r.store(a.r + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t]));
+            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
         } else if constexpr (MODE == VEC_INIT_J) {
             VecT<T, V> r, z;
 #pragma unroll
@@ -708,8 +726,8 @@ struct VecChunk {
             z.store(a.p + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) {
-                acc.add(dot_term(r.v[t], r.v[t], c[t]));
-                acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t]));  // z = r dinv
+                acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
+                acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t], a.single));  // z = r dinv
             }
         } else if constexpr (MODE == VEC_RUPD_J) {
             VecT<T, V> r;
@@ -718,12 +736,12 @@ struct VecChunk {
             r.store(a.r + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) {
-                acc.add(dot_term(r.v[t], r.v[t], c[t]));
-                acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t]));  // z = r dinv
+                acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
+                acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t], a.single));  // z = r dinv
             }
         } else {
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(A.v[t], B.v[t], c[t]));
+            for (int t = 0; t < V; ++t) acc.add(dot_term(A.v[t], B.v[t], c[t], a.single));
         }
     }
 };
@@ -791,7 +809,7 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
                 a.slot[0] = tot;
                 a.slot[1] = tot2;
             } else {
-                fin_rtr<MODE>(a.st, tot.hi, tot2.hi, a.hist, a.trace);
+                fin_rtr<MODE>(a.st, tot, tot2, a.hist, a.trace, a.single);
             }
             a.st->cnt[1] = 0;
         }
@@ -861,6 +879,7 @@ struct FaceArgs {
     int nprev;
     CgState* st;
     dd* slot;              // fused: this rank's reduced pap partial
+    int single;            // paper-literal single mode (NEXT-2)
     MeshView mesh;
 };
 
@@ -950,7 +969,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
                 a.w[L] = sum;
             }
         if constexpr (FUSED)
-            if (upper) acc.add(dot_term(sum, p0, 1.0));  // one term per node (lower rank)
+            if (upper) acc.add(dot_term(sum, p0, 1.0, a.single));  // one term per node (lower rank)
     }
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
@@ -969,7 +988,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
 // and run the scalar finaliser.  KIND: 0 = alpha (pap); 1 + VecMode = rtr etc.
 // gather holds two dd per rank: [2r] the value, [2r + 1] rtz (Jacobi modes).
 template <int KIND>
-__global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double* trace)
+__global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double* trace, int single)
 {
     if (threadIdx.x != 0) return;
     dd t{__ldcg(&gather[0].hi), __ldcg(&gather[0].lo)};
@@ -978,8 +997,8 @@ __global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double
         t = dd_add(t, dd{__ldcg(&gather[2 * r].hi), __ldcg(&gather[2 * r].lo)});
         t2 = dd_add(t2, dd{__ldcg(&gather[2 * r + 1].hi), __ldcg(&gather[2 * r + 1].lo)});
     }
-    if constexpr (KIND == 0) fin_alpha(st, t.hi, trace);
-    else fin_rtr<KIND - 1>(st, t.hi, vec_jacobi(KIND - 1) ? t2.hi : t.hi, hist, trace);
+    if constexpr (KIND == 0) fin_alpha(st, t, trace, single);
+    else fin_rtr<KIND - 1>(st, t, vec_jacobi(KIND - 1) ? t2 : t, hist, trace, single);
 }
 
 }  // namespace nbk

@@ -22,7 +22,8 @@ LIB_PATH = os.path.join(HERE, "csrc", "libnbk.so")
 NBK_OK, NBK_EINVAL, NBK_EDEFECT, NBK_ECUDA, NBK_ENCCL, NBK_ENOMEM, NBK_ESTATE = 0, 2, 3, 4, 5, 6, 7
 NBK_FP64, NBK_FP32 = 0, 1
 AX_LOCAL, AX_DSSUM, AX_MASK = 0, 1, 2
-PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32}
+NBK_FP32S = 2
+PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32, "fp32s": NBK_FP32S}
 PRECOND = {"none": 0, "jacobi": 1}
 
 # every symbol include/nbk.h declares
@@ -264,8 +265,10 @@ class Context:
                self._ctx)
         return f
 
-    def glsc3(self, a, b) -> float:
+    def glsc3(self, a, b, single: bool = False) -> float:
         prec = self._prec_of(a)
+        if single:
+            prec = "fp32s"
         out = ctypes.c_double(0.0)
         _check(self.lib.nbk_glsc3(self._ctx, self._dev(a, a.dtype), self._dev(b, a.dtype),
                                   PREC[prec], ctypes.byref(out)), self._ctx)

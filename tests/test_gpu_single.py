@@ -1,0 +1,112 @@
+"""Paper-literal single-precision solver ("solver
+runs exclusively in single") through the C ABI vs the oracle.
+
+Reading R11b: inner products RN32(sum RN32(a_L b_L) c_L) -- the
+correctly rounded binary32 value of the binary32 products -- and the scalars
+alpha = rtz1/pap, beta = rtz1/rtz2, h = sqrt(rtr) in binary32.  Contract mode,
+bitwise comparisons.
+"""
+import numpy as np
+import pytest
+
+from tests import inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def nbk():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2405_11065_b200 as p
+    p.load()
+    return p
+
+
+def bits_equal(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    assert a.dtype == b.dtype and a.shape == b.shape
+    return np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def make(nbk, ora, args):
+    ex, ey, ez, N, jit, sg, sr = args
+    ctx = nbk.cg_setup(nbk.MeshSpec(ex, ey, ez, N, jit, sg, sr), "fp32")
+    om = ora.Mesh(ex, ey, ez, N, jit, sg, sr)
+    _, _, D = ora.gll(N)
+    s = ora.setup(om, want=("G", "f"))
+    ctx.load_arrays(D, s["G"], s["f"])
+    return ctx, om, D, s
+
+
+@pytest.mark.parametrize("jacobi", [False, True])
+@pytest.mark.parametrize("args", [(2, 2, 2, 8, 0.0, 0, 1001), (3, 3, 3, 12, 0.1, 2003, 1003),
+                                  (4, 4, 4, 10, 0.1, 2005, 1005), (3, 2, 2, 5, 0.2, 4, 5)])
+def test_single_solver_bitwise(nbk, ora, args, jacobi):
+    ctx, om, D, s = make(nbk, ora, args)
+    dinv = None
+    if jacobi:
+        _, dinv = ora.jacobi_dinv(om, D, s["G"])
+        ctx.load_precond(dinv)
+        ctx.set_precond("jacobi")
+    hist, trace, res = ctx.cg_solve(100, "fp32s")
+    ref = ora.cg(om, D, s["G"], s["f"], 100, "fp32s", dinv=dinv)
+    assert bits_equal(hist, ref.hist)
+    assert bits_equal(trace, ref.trace)
+    assert bits_equal(ctx.solution(), ref.x.astype(np.float64))
+    assert res["defect_iter"] == ref.defect == 0
+    ctx.close()
+
+
+def test_single_solver_c2_bitwise(nbk, ora):
+    ctx, om, D, s = make(nbk, ora, (16, 16, 16, 8, 0.0, 0, 1002))
+    hist, trace, _ = ctx.cg_solve(30, "fp32s")
+    ref = ora.cg(om, D, s["G"], s["f"], 30, "fp32s")
+    assert bits_equal(hist, ref.hist) and bits_equal(trace, ref.trace)
+    ctx.close()
+
+
+def test_single_glsc3_bitwise(nbk, ora):
+    ctx, om, D, s = make(nbk, ora, (4, 3, 5, 8, 0.0, 0, 0))
+    c = ora.multiplicity_weight(om)
+    for seed in range(6):
+        a = inputs.uniform_field((om.E, 8, 8, 8), seed, np.float32, -3.0, 3.0)
+        b = inputs.uniform_field((om.E, 8, 8, 8), seed + 50, np.float32)
+        got = ctx.glsc3(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), single=True)
+        assert got == ora.glsc3_single(a, b, c)
+        assert np.float32(got) == got
+    ctx.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_single_solver_virtual_slabs(nbk, ora, P):
+    ex, ey, ez, N, jit, sg, sr = (3, 2, 8, 6, 0.15, 21, 22)
+    grp = nbk.Group(nbk.MeshSpec(ex, ey, ez, N, jit, sg, sr), P, "fp32")
+    om = ora.Mesh(ex, ey, ez, N, jit, sg, sr)
+    _, _, D = ora.gll(N)
+    s = ora.setup(om, want=("G", "f"))
+    El = om.E // P
+    grp.load_arrays(D, [s["G"][r * El:(r + 1) * El] for r in range(P)],
+                    [s["f"][r * El:(r + 1) * El] for r in range(P)])
+    hist, trace, _ = grp.cg_solve(50, "fp32s")
+    ref = ora.cg(om, D, s["G"], s["f"], 50, "fp32s")
+    assert bits_equal(hist, ref.hist) and bits_equal(trace, ref.trace)
+    assert bits_equal(grp.solution(), ref.x.astype(np.float64))
+    grp.close()
+
+
+def test_accuracy_report_shapes(nbk, ora):
+    """AE/MAE of the two single-precision solvers against the FP64
+    solver on C1: both small and finite; reported by bench.py."""
+    ctx, om, D, s = make(nbk, ora, (2, 2, 2, 8, 0.0, 0, 1001))
+    h64, _, _ = ctx.cg_solve(100, "fp64")
+    h32, _, r32 = ctx.cg_solve(100, "fp32")
+    h1, _, r1 = ctx.cg_solve(100, "fp32s")
+    ae32 = np.abs(h32[1:] - h64[1:])
+    ae1 = np.abs(h1[1:] - h64[1:])
+    assert np.isfinite(ae32).all() and np.isfinite(ae1).all()
+    assert ae32.mean() < 1e-2 * h64[0] and ae1.mean() < 1e-2 * h64[0]
+    assert 0 < r32["true_res_rel"] < 1e-3 and 0 < r1["true_res_rel"] < 1e-3
+    ctx.close()
