@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, *NCCL_DEF, "-c", os.path.join(CSRC, src), "-o", obj]
+        extra = os.environ.get("NBK_EXTRA_FLAGS", "").split()  # tuning experiments only
+        cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, *NCCL_DEF, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

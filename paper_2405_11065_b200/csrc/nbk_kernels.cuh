@@ -85,9 +85,15 @@ __device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t)
 // slots of g1/g2 once consumed, so smem = 7*EPB*N^3 values.  Without STAGE_G
 // (only N=16 FP64, > 227 KB) G is read from global memory per k-slice.
 template <typename T>
+#ifndef NBK_EPB8_F32
+#define NBK_EPB8_F32 2
+#endif
+#ifndef NBK_EPB8_F64
+#define NBK_EPB8_F64 1
+#endif
 __host__ __device__ constexpr int ax_epb(int N)
 {
-    if (N == 8) return sizeof(T) == 4 ? 3 : 2;
+    if (N == 8) return sizeof(T) == 4 ? NBK_EPB8_F32 : NBK_EPB8_F64;
     if (N == 10) return sizeof(T) == 4 ? 2 : 1;
     if (N == 12) return 1;
     int by_thr = 256 / (N * N) > 0 ? 256 / (N * N) : 1;
