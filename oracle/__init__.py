@@ -84,6 +84,10 @@ def lib():
         L.ora_glsc3_32s.argtypes = [c_i64, _p, _p, _p]
         L.ora_fsum32.restype = ctypes.c_float
         L.ora_fsum32.argtypes = [c_i64, _p]
+        L.ora_vprec_round.restype = c_dbl
+        L.ora_vprec_round.argtypes = [c_dbl, ctypes.c_int]
+        L.ora_cgvp.restype = ctypes.c_int
+        L.ora_cgvp.argtypes = [ctypes.c_int] * 4 + [_p] * 3 + [ctypes.c_int] * 2 + [_p] * 3
         L.ora_jacobi_dinv.restype = None
         L.ora_jacobi_dinv.argtypes = [ctypes.c_int] * 4 + [_p] * 4
         L.ora_true_residual.restype = c_dbl
@@ -245,6 +249,25 @@ class CgResult:
     hist: np.ndarray   # h_0..h_niter
     trace: np.ndarray  # (niter, 5): rtz1, beta, alpha, pap, rtr
     defect: int
+
+
+def vprec_round(x: float, t: int) -> float:
+    """VPREC rounding of a binary64 value to t mantissa bits (RN, ties to even)."""
+    return float(lib().ora_vprec_round(float(x), int(t)))
+
+
+def cg_vprec(mesh: Mesh, D, G, f, niter: int, t: int) -> CgResult:
+    """VPREC-emulated CG (NEXT-4): binary64 loop, every
+    operation of the CG kernels rounded to t mantissa bits."""
+    D = np.ascontiguousarray(D, np.float64)
+    G = np.ascontiguousarray(G, np.float64)
+    f = np.ascontiguousarray(f, np.float64)
+    hist = np.zeros(niter + 1)
+    trace = np.zeros((niter, 5))
+    x = np.zeros_like(f)
+    rc = lib().ora_cgvp(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), int(t), niter, _ptr(x), _ptr(hist),
+                        _ptr(trace))
+    return CgResult(x=x, hist=hist, trace=trace, defect=int(rc))
 
 
 def jacobi_dinv(mesh: Mesh, D, G):

@@ -350,7 +350,7 @@ int ora_setup(int ex, int ey, int ez, int N, double jitter, uint64_t seed_geom, 
 /* Local operator ax_e = D^T G D u_e, canonical order CEO-1 (C1-C3)     */
 /* (T1 line 5 P:147; F2 P:215-243 local_grad3 / local_grad3_t)*/
 /* ------------------------------------------------------------------ */
-#define DEFINE_AX_LOCAL(NAME, T, FMA)                                                         \
+#define DEFINE_AX_LOCAL(NAME, T, FMA, MUL, ADD)                                               \
     void NAME(int64_t E, int N, const T* D, const T* G, const T* u, T* w)                     \
     {                                                                                         \
         const int64_t nn = (int64_t)N * N * N;                                                \
@@ -376,9 +376,9 @@ int ora_setup(int ex, int ey, int ez, int N, double jitter, uint64_t seed_geom, 
                         T g1 = Ge[0 * nn + pt], g2 = Ge[1 * nn + pt], g3 = Ge[2 * nn + pt];   \
                         T g4 = Ge[3 * nn + pt], g5 = Ge[4 * nn + pt], g6 = Ge[5 * nn + pt];   \
                         T a; /* C2 metric */                                                  \
-                        a = g1 * ur; a = FMA(g2, us, a); a = FMA(g3, ut, a); wr[pt] = a;      \
-                        a = g2 * ur; a = FMA(g4, us, a); a = FMA(g5, ut, a); ws[pt] = a;      \
-                        a = g3 * ur; a = FMA(g5, us, a); a = FMA(g6, ut, a); wt[pt] = a;      \
+                        a = MUL(g1, ur); a = FMA(g2, us, a); a = FMA(g3, ut, a); wr[pt] = a;  \
+                        a = MUL(g2, ur); a = FMA(g4, us, a); a = FMA(g5, ut, a); ws[pt] = a;  \
+                        a = MUL(g3, ur); a = FMA(g5, us, a); a = FMA(g6, ut, a); wt[pt] = a;  \
                     }                                                                         \
             for (int k = 0; k < N; ++k)                                                       \
                 for (int j = 0; j < N; ++j)                                                   \
@@ -390,14 +390,51 @@ int ora_setup(int ex, int ey, int ez, int N, double jitter, uint64_t seed_geom, 
                             a = FMA(D[l * N + j], ws[((int64_t)k * N + l) * N + i], a);       \
                         for (int l = 0; l < N; ++l)                                           \
                             b = FMA(D[l * N + k], wt[((int64_t)l * N + j) * N + i], b);       \
-                        we[((int64_t)k * N + j) * N + i] = a + b;                             \
+                        we[((int64_t)k * N + j) * N + i] = ADD(a, b);                         \
                     }                                                                         \
             free(wr);                                                                         \
         }                                                                                     \
     }
 
-DEFINE_AX_LOCAL(ora_ax_local64, double, fma)
-DEFINE_AX_LOCAL(ora_ax_local32, float, fmaf)
+#define PLAIN_MUL(a, b) ((a) * (b))
+#define PLAIN_ADD(a, b) ((a) + (b))
+#define PLAIN_DIV(a, b) ((a) / (b))
+DEFINE_AX_LOCAL(ora_ax_local64, double, fma, PLAIN_MUL, PLAIN_ADD)
+DEFINE_AX_LOCAL(ora_ax_local32, float, fmaf, PLAIN_MUL, PLAIN_ADD)
+
+/* ------------------------------------------------------------------ */
+/* VPREC emulation ("VPREC intercepts each  */
+/* FP operation, performs the computation in double precision and      */
+/* rounds the result to the emulated precision", t in       */
+/* [3, 52], CG-loop scope).  vp(x) rounds a binary64 value to t         */
+/* explicit mantissa bits, round to nearest, ties to even, on the bit  */
+/* pattern (binary64 exponent range; a carry into the exponent is the  */
+/* correct rounding up; subnormals are rounded at the same absolute bit*/
+/* position).  t >= 52 is the identity.                                 */
+/* ------------------------------------------------------------------ */
+static int g_vp_t = 52;
+
+double ora_vprec_round(double x, int t)
+{
+    if (t >= 52 || !isfinite(x)) return x;
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    const int drop = 52 - t;
+    const uint64_t mask = ((uint64_t)1 << drop) - 1, half = (uint64_t)1 << (drop - 1);
+    const uint64_t low = b & mask;
+    b &= ~mask;
+    if (low > half || (low == half && ((b >> drop) & 1))) b += (uint64_t)1 << drop;
+    double y;
+    memcpy(&y, &b, 8);
+    return y;
+}
+static double vp(double x) { return ora_vprec_round(x, g_vp_t); }
+static double vp_fma(double a, double b, double c) { return vp(fma(a, b, c)); }
+static double vp_mul(double a, double b) { return vp(a * b); }
+static double vp_add(double a, double b) { return vp(a + b); }
+static double vp_div(double a, double b) { return vp(a / b); }
+static double vp_sqrt(double a) { return vp(sqrt(a)); }
+DEFINE_AX_LOCAL(ora_ax_local_vp, double, vp_fma, vp_mul, vp_add)
 
 /* ------------------------------------------------------------------ */
 /* dssum (C4): for every global node, sum its copies in ascending local */
@@ -406,7 +443,7 @@ DEFINE_AX_LOCAL(ora_ax_local32, float, fmaf)
 /* Operates on the full mesh (all elements).                            */
 /* mask (C5): masked points are assigned +0.                            */
 /* ------------------------------------------------------------------ */
-#define DEFINE_DSSUM(NAME, T)                                                                 \
+#define DEFINE_DSSUM(NAME, T, ADD)                                                            \
     void NAME(int ex, int ey, int ez, int N, T* w, int apply_mask)                            \
     {                                                                                         \
         ora_mesh m = {ex, ey, ez, N};                                                         \
@@ -417,7 +454,7 @@ DEFINE_AX_LOCAL(ora_ax_local32, float, fmaf)
         for (int64_t L = 0; L < n; ++L) {                                                     \
             int64_t g = point_gid(&m, L);                                                     \
             if (!seen[g]) { s[g] = w[L]; seen[g] = 1; }                                       \
-            else s[g] = s[g] + w[L];                                                          \
+            else s[g] = ADD(s[g], w[L]);                                                      \
         }                                                                                     \
         for (int64_t L = 0; L < n; ++L) {                                                     \
             int64_t g = point_gid(&m, L);                                                     \
@@ -427,8 +464,8 @@ DEFINE_AX_LOCAL(ora_ax_local32, float, fmaf)
         free(seen);                                                                           \
     }
 
-DEFINE_DSSUM(ora_dssum64, double)
-DEFINE_DSSUM(ora_dssum32, float)
+DEFINE_DSSUM(ora_dssum64, double, PLAIN_ADD)
+DEFINE_DSSUM(ora_dssum32, float, PLAIN_ADD)
 
 #define DEFINE_MASK(NAME, T)                                                                  \
     void NAME(int ex, int ey, int ez, int N, T* w)                                            \
@@ -691,7 +728,7 @@ void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const doubl
 /* Returns the first iteration with pap <= 0 or a non-finite scalar     */
 /* (defect) or 0.                                                */
 /* ------------------------------------------------------------------ */
-#define DEFINE_CG(NAME, T, S, FMA, SQRT, AXLOCAL, DSSUM, GLSC3)                                          \
+#define DEFINE_CG(NAME, T, S, FMA, SQRT, DIV, AXLOCAL, DSSUM, GLSC3)                                          \
     int NAME(int ex, int ey, int ez, int N, const T* D, const T* G, const T* f, const T* dinv,  \
              int niter, T* x, double* hist, double* trace)                                      \
     {                                                                                           \
@@ -715,13 +752,13 @@ void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const doubl
         for (int k = 1; k <= niter; ++k) {                                                      \
             S rtz1 = rtz, beta = 0, alpha = 0, pap;                                             \
             if (rtz1 == 0.0) zero = 1;                                                          \
-            if (!zero && k > 1) beta = rtz1 / rtz2;                                             \
+            if (!zero && k > 1) beta = DIV(rtz1, rtz2);                                         \
             T betaT = (T)beta;                                                                  \
             for (int64_t L = 0; L < n; ++L) p[L] = FMA(betaT, p[L], z[L]);                      \
             AXLOCAL(E, N, D, G, p, w);                                                          \
             DSSUM(ex, ey, ez, N, w, 1);                                                         \
             pap = GLSC3(n, w, p, c);                                                            \
-            if (!zero) alpha = rtz1 / pap;                                                      \
+            if (!zero) alpha = DIV(rtz1, pap);                                                  \
             T alphaT = (T)alpha, alphmT = -alphaT;                                              \
             for (int64_t L = 0; L < n; ++L) x[L] = FMA(alphaT, p[L], x[L]);                     \
             for (int64_t L = 0; L < n; ++L) r[L] = FMA(alphmT, w[L], r[L]);                     \
@@ -746,11 +783,46 @@ void ora_jacobi_dinv(int ex, int ey, int ez, int N, const double* D, const doubl
         return defect;                                                                          \
     }
 
-DEFINE_CG(ora_cg64_core, double, double, fma, sqrt, ora_ax_local64, ora_dssum64, ora_glsc3_64)
-DEFINE_CG(ora_cg32_core, float, double, fmaf, sqrt, ora_ax_local32, ora_dssum32, ora_glsc3_32)
+DEFINE_CG(ora_cg64_core, double, double, fma, sqrt, PLAIN_DIV, ora_ax_local64, ora_dssum64, ora_glsc3_64)
+DEFINE_CG(ora_cg32_core, float, double, fmaf, sqrt, PLAIN_DIV, ora_ax_local32, ora_dssum32, ora_glsc3_32)
 /* paper-literal single precision: binary32 inner products (above) and binary32
  * scalars: beta = rtz1/rtz2, alpha = rtz1/pap, sqrt in binary32 (NEXT-2) */
-DEFINE_CG(ora_cg32s_core, float, float, fmaf, sqrtf, ora_ax_local32, ora_dssum32, ora_glsc3_32s)
+DEFINE_CG(ora_cg32s_core, float, float, fmaf, sqrtf, PLAIN_DIV, ora_ax_local32, ora_dssum32, ora_glsc3_32s)
+
+/* VPREC CG loop (NEXT-4): binary64 loop with every operation of the CG
+ * kernels rounded to t bits (ax: every fma / mul / add; dssum adds; the
+ * p, x, r updates; glsc3 terms vp(a b) c and the glsc3 result vp(RN64(sum));
+ * alpha, beta, sqrt).  Set-up data (D, G, f) are not rounded (CG scope). */
+static double ora_glsc3_vp(int64_t n, const double* a, const double* b, const double* c)
+{
+    int64_t nch = (n + CHUNK - 1) / CHUNK;
+    xsum* part = (xsum*)malloc(sizeof(xsum) * (nch > 0 ? nch : 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        xsum_init(&part[ch]);
+        int64_t lo = ch * CHUNK, hi = lo + CHUNK < n ? lo + CHUNK : n;
+        for (int64_t L = lo; L < hi; ++L) xsum_add(&part[ch], vp(a[L] * b[L]) * c[L]);
+    }
+    xsum tot;
+    xsum_init(&tot);
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        if (part[ch].has_special) { tot.special += part[ch].special; tot.has_special = 1; }
+        for (int q = 0; q < part[ch].n; ++q) xsum_add(&tot, part[ch].p[q]);
+    }
+    free(part);
+    return vp(xsum_round(&tot));
+}
+DEFINE_DSSUM(ora_dssum_vp, double, vp_add)
+DEFINE_CG(ora_cgvp_core, double, double, vp_fma, vp_sqrt, vp_div, ora_ax_local_vp, ora_dssum_vp, ora_glsc3_vp)
+
+int ora_cgvp(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f, int t,
+             int niter, double* x, double* hist, double* trace)
+{
+    g_vp_t = t;
+    int rc = ora_cgvp_core(ex, ey, ez, N, D, G, f, NULL, niter, x, hist, trace);
+    g_vp_t = 52;
+    return rc;
+}
 
 int ora_cg64(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,
              int niter, double* x, double* hist, double* trace)

@@ -624,3 +624,60 @@ def test_single_solver_plausibility(ora):
     assert 1e-9 < tr / h0 < 1e-3
     z = ora.cg(m, D, s["G"], np.zeros_like(s["f"]), 5, "fp32s")
     assert (z.hist == 0).all() and (z.x == 0).all()
+
+
+# --------------------------------------------------- VPREC emulation (NEXT-4)
+def _vprec_exact(x, t):
+    """Round a binary64 value to t explicit mantissa bits, ties to even, with
+    rational arithmetic (independent of the oracle's bit manipulation)."""
+    from fractions import Fraction
+    if x == 0.0 or t >= 52:
+        return x
+    m, e = math.frexp(abs(x))           # |x| = m 2^e, m in [0.5, 1)
+    e = max(e, -1021)                   # subnormals: same absolute bit position
+    ulp = Fraction(2) ** (e - 1 - t)    # weight of the last kept bit
+    q = Fraction(abs(x)) / ulp
+    fl = q.numerator // q.denominator
+    rem = q - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    return math.copysign(float(fl * ulp), x)
+
+
+def test_vprec_round_matches_rational_rounding(ora):
+    g = inputs.rng(8)
+    for trial in range(3000):
+        t = int(g.integers(1, 53))
+        if trial % 4 == 0:   # exact ties: a t+1-bit value with its last bit set
+            m = (2 * int(g.integers(1 << t, 1 << (t + 1)))) + 1
+            x = math.ldexp(m, int(g.integers(-60, 60)) - (t + 1))
+        else:
+            x = float(g.standard_normal() * 2.0 ** int(g.integers(-80, 80)))
+        assert ora.vprec_round(x, t) == _vprec_exact(x, t), (x, t)
+    assert ora.vprec_round(3 * 2.0 ** -1074, 52) == 3 * 2.0 ** -1074  # subnormal, t = 52: exact
+    assert ora.vprec_round(1.0 + 2.0 ** -30, 23) == 1.0 and ora.vprec_round(1.75, 1) == 2.0
+
+
+def test_vprec_cg_t52_is_fp64_and_precision_sweep(ora):
+    """t = 52 leaves every operation unchanged: the VPREC loop IS the FP64 solver
+    bit for bit.  Lower t: the true residual of the solution degrades as the
+    emulated precision drops (P:367-372 'residual becomes smaller as precision
+    grows', F4)."""
+    m = ora.Mesh(2, 2, 2, 6, jitter=0.1, seed_geom=4, seed_rhs=3)
+    _, _, D = ora.gll(6)
+    s = ora.setup(m, want=("G", "f"))
+    a = ora.cg(m, D, s["G"], s["f"], 80, "fp64")
+    b = ora.cg_vprec(m, D, s["G"], s["f"], 80, 52)
+    np.testing.assert_array_equal(a.hist, b.hist)
+    np.testing.assert_array_equal(a.trace, b.trace)
+    np.testing.assert_array_equal(a.x, b.x)
+    res = {}
+    for t in (6, 10, 16, 23, 36, 52):
+        r = ora.cg_vprec(m, D, s["G"], s["f"], 80, t)
+        tr, h0 = ora.true_residual(m, D, s["G"], s["f"], r.x)
+        res[t] = tr / h0
+        # every scalar is a t-bit value
+        for v in np.concatenate([r.trace.reshape(-1), r.hist]):
+            assert ora.vprec_round(v, t) == v
+    assert res[6] > res[16] > res[36] and res[52] < 1e-8
+    assert res[23] < 1e-3
