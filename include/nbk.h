@@ -48,9 +48,13 @@ typedef enum {
     NBK_FP64 = 0, /* FP64 CG solver (Nekbone's reference precision)                        */
     NBK_FP32 = 1, /* mixed: FP64 set-up, FP32 CG loop with FP64 inner-product accumulation
                      (north_star; reading R11), FP64 final residual check (C12)          */
-    NBK_FP32S = 2 /* paper-literal single: as
+    NBK_FP32S = 2, /* paper-literal single: as
                      NBK_FP32 but inner products RN32(sum RN32(a b) c) and the scalars
                      alpha, beta, sqrt in binary32 (cg_solve and glsc3 only)           */
+    NBK_VPREC = 3  /* VPREC emulation (NEXT-4): binary64 CG loop with
+                     every operation's result rounded to t mantissa bits (nbk_set_vprec;
+                     glsc3 terms vp(a b) c, the sum vp(RN64(sum)); alpha, beta, sqrt);
+                     set-up data and the final FP64 check are not rounded (cg_solve only) */
 } nbk_precision;
 
 /* Box mesh (reading R5): cubic elements of edge h = 1/ex on
@@ -207,6 +211,10 @@ nbk_status nbk_get_solution(nbk_ctx* ctx, double* x_host);
 
 /* Device pointer of the last solution in its native precision (do not free). */
 nbk_status nbk_solution_ptr(nbk_ctx* ctx, nbk_precision precision, void** x_dev);
+
+/* Mantissa bits t in [1, 52] of the following NBK_VPREC solves (default 23;
+ * t = 52 reproduces the NBK_FP64 solver bit for bit).  Unpreconditioned CG. */
+nbk_status nbk_set_vprec(nbk_ctx* ctx, int32_t t);
 
 /* Select the preconditioner of the following solves (default NBK_PRECOND_NONE).
  * Jacobi: K_A forms z = RN_T(r * dinv_T) for p = beta p + z, K_C reduces

@@ -46,21 +46,22 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    extra = os.environ.get("NBK_EXTRA_FLAGS", "").split()  # tuning experiments only
+    for src in SOURCES:  # the translation units compile in parallel
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        extra = os.environ.get("NBK_EXTRA_FLAGS", "").split()  # tuning experiments only
         cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, *NCCL_DEF, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+        objs.append(obj)
+    for src, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
-            sys.stderr.write(r.stderr)
-        log = os.path.join(CSRC, src.replace(".cu", ".ptxas.log"))
-        with open(log, "w") as fh:
-            fh.write(r.stderr)
-        objs.append(obj)
+            sys.stderr.write(err)
+        with open(os.path.join(CSRC, src.replace(".cu", ".ptxas.log")), "w") as fh:
+            fh.write(err)
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]
     subprocess.check_call(cmd)

@@ -74,17 +74,17 @@ static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned bloc
 }
 // attr_only: set the dynamic shared-memory limit (done once at set-up, never
 // under stream capture).
-template <typename T, int N, int FUSED>
+template <typename T, int N, int FUSED, bool VP = false>
 static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
                                bool pdl = false)
 {
     constexpr int EPB = ax_epb<T>(N);
     const size_t smem = (size_t)ax_smem_bytes<T>(N);
     if (attr_only)
-        return cudaFuncSetAttribute(k_ax<T, N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        return cudaFuncSetAttribute(k_ax<T, N, FUSED, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem);
     const unsigned grid = (unsigned)((a.mesh.E + EPB - 1) / EPB);
-    return launch_k(k_ax<T, N, FUSED>, grid, ax_threads<T>(N), smem, s, pdl, a);
+    return launch_k(k_ax<T, N, FUSED, VP>, grid, ax_threads<T>(N), smem, s, pdl, a);
 }
 
 #define NBK_SWITCH_N(N, CALL)                 \
@@ -107,12 +107,29 @@ static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_onl
     default: return cudaErrorInvalidValue;    \
     }
 
-template <typename T, int FUSED>
+template <typename T, int FUSED, bool VP = false>
 static cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
                              bool pdl = false)
 {
-#define AXN(n) launch_ax_n<T, n, FUSED>(a, s, attr_only, pdl)
-    NBK_SWITCH_N(a.mesh.N, AXN)
+#define AXN(n) launch_ax_n<T, n, FUSED, VP>(a, s, attr_only, pdl)
+    if constexpr (VP) {  // VPREC emulation kernels: N <= NBK_VPREC_MAXN (compile time)
+        switch (a.mesh.N) {
+        case 2: return AXN(2);
+        case 3: return AXN(3);
+        case 4: return AXN(4);
+        case 5: return AXN(5);
+        case 6: return AXN(6);
+        case 7: return AXN(7);
+        case 8: return AXN(8);
+        case 9: return AXN(9);
+        case 10: return AXN(10);
+        case 11: return AXN(11);
+        case 12: return AXN(12);
+        default: return cudaErrorNotSupported;
+        }
+    } else {
+        NBK_SWITCH_N(a.mesh.N, AXN)
+    }
 #undef AXN
 }
 
@@ -133,35 +150,35 @@ static int resident_grid(const void* kern, int block, size_t smem)
     return g;
 }
 
-template <typename T, int N, int MODE>
-static cudaError_t launch_vec_n(const VecArgs<T>& a, cudaStream_t s, bool pdl)
+template <typename T, int V, int MODE, bool VP>
+static cudaError_t launch_vec_v(const VecArgs<T>& a, cudaStream_t s, bool pdl)
 {
-    const int cap = resident_grid((const void*)k_vec<T, N, MODE>, 256, 0);
+    const int cap = resident_grid((const void*)k_vec<T, V, MODE, VP>, 256, 0);
     int64_t g = (a.n / 4 + 511) / 512;  // >= 2 chunks of 4 points per thread
     if (g < 1) g = 1;
     if (g > cap) g = cap;
-    return launch_k(k_vec<T, N, MODE>, (unsigned)g, 256, 0, s, pdl, a);
+    return launch_k(k_vec<T, V, MODE, VP>, (unsigned)g, 256, 0, s, pdl, a);
 }
 
-template <typename T, int MODE>
+// one vector kernel for every N: chunks of 4 points (even N) or 1 (odd N)
+template <typename T, int MODE, bool VP = false>
 static cudaError_t launch_vec(const VecArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
-#define VECN(n) launch_vec_n<T, n, MODE>(a, s, pdl)
-    NBK_SWITCH_N(a.mesh.N, VECN)
-#undef VECN
+    if (a.mesh.N < 2 || a.mesh.N > 16) return cudaErrorInvalidValue;
+    return a.mesh.N % 2 == 0 ? launch_vec_v<T, 4, MODE, VP>(a, s, pdl) : launch_vec_v<T, 1, MODE, VP>(a, s, pdl);
 }
 
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool VP = false>
 static int dssum_grid_t(int ntiles)
 {
-    const int cap = resident_grid((const void*)k_dssum<T, FUSED>, 256, 0);
+    const int cap = resident_grid((const void*)k_dssum<T, FUSED, VP>, 256, 0);
     return ntiles < 1 ? 1 : (ntiles > cap ? cap : ntiles);
 }
 
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool VP = false>
 static cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
-    return launch_k(k_dssum<T, FUSED>, dssum_grid_t<T, FUSED>(a.ntiles), 256, 0, s, pdl, a);
+    return launch_k(k_dssum<T, FUSED, VP>, dssum_grid_t<T, FUSED, VP>(a.ntiles), 256, 0, s, pdl, a);
 }
 
 // ------------------------------------------------------------ NCCL (dlopen)
@@ -340,9 +357,10 @@ static dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - 2 * NBK_VEC_GRI
 // One rank: K_B (its last block forms alpha).  Several: K_B (publish only) and
 // the face pack, exchange, face merge (reduces this rank's pap), all-gather,
 // k_fin (rank-ordered combination, alpha).
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool VP = false>
 static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std::vector<const T*>& p,
-                              int mask, bool pdl, std::string& err, int rev = 0, int single = 0)
+                              int mask, bool pdl, std::string& err, int rev = 0, int single = 0,
+                              int vp_t = 0)
 {
     cudaError_t e;
     const cudaStream_t s = t.s;
@@ -352,13 +370,14 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         d.mask = mask;
         d.rev = rev;
         d.single = single;
+        d.vp_t = vp_t;
         if (FUSED) {
             d.p = p[q];
             d.parts = c->parts;
             d.nA = ax_blocks_n<T>(c->E, c->N);
             d.fin = t.multi ? 0 : 1;
         }
-        if ((e = launch_dssum<T, FUSED>(d, s, pdl && !t.multi)) != cudaSuccess) return e;
+        if ((e = launch_dssum<T, FUSED, VP>(d, s, pdl && !t.multi)) != cudaSuccess) return e;
         if (t.multi) {
             FaceArgs<T> f = face_args<T>(c, w[q]);
             k_face_pack<T><<<vec_grid(2 * c->nlayer), 256, 0, s>>>(f);
@@ -374,7 +393,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         f.single = single;
         if (FUSED) {
             f.p = p[q];
-            f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED>((int)c->ntiles);
+            f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED, VP>((int)c->ntiles);
         }
         const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
         k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);
@@ -383,7 +402,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
     if (FUSED) {
         if ((e = xchg_gather(t, s, err)) != cudaSuccess) return e;
         for (nbk_ctx* c : t.m) {
-            k_fin<0><<<1, 32, 0, s>>>(c->gather, c->nranks, c->st, c->hist, c->trace, single);
+            k_fin<0><<<1, 32, 0, s>>>(c->gather, c->nranks, c->st, c->hist, c->trace, single, vp_t);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
     }
@@ -392,7 +411,7 @@ static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
 
 // Vector kernel (K_C and the other modes) over a team: one rank finalises in
 // its last block; several publish per-rank partials, all-gather, k_fin.
-template <typename T, int MODE>
+template <typename T, int MODE, bool VP = false>
 static cudaError_t vec_team(const Team& t, const std::vector<VecArgs<T>>& args, bool pdl,
                             std::string& err)
 {
@@ -400,14 +419,14 @@ static cudaError_t vec_team(const Team& t, const std::vector<VecArgs<T>>& args, 
     for (size_t q = 0; q < t.m.size(); ++q) {
         VecArgs<T> a = args[q];
         a.slot = t.multi ? t.m[q]->gather + 2 * t.m[q]->rank : nullptr;
-        if ((e = launch_vec<T, MODE>(a, t.s, pdl && !t.multi)) != cudaSuccess) return e;
+        if ((e = launch_vec<T, MODE, VP>(a, t.s, pdl && !t.multi)) != cudaSuccess) return e;
     }
     if (!t.multi) return cudaSuccess;
     if ((e = xchg_gather(t, t.s, err)) != cudaSuccess) return e;
     for (size_t q = 0; q < t.m.size(); ++q) {
         nbk_ctx* c = t.m[q];
         k_fin<1 + MODE><<<1, 32, 0, t.s>>>(c->gather, c->nranks, c->st, c->hist, c->trace,
-                                          args[q].single);
+                                          args[q].single, args[q].vp_t);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -440,7 +459,7 @@ static cudaError_t ax_team(const Team& t, const std::vector<const T*>& u, const 
 }
 
 // Enqueue one CG solve (T1 loop, fixed niter) for the team; used under capture.
-template <typename T>
+template <typename T, bool VP = false>
 static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp32, bool profiling,
                                  std::string& err, int single = 0)
 {
@@ -459,17 +478,19 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
     const int64_t nface = t.multi ? 2 : 0;    // pack + merge per dssum and member
 
     // Jacobi PCG (NEXT-1): z = r * dinv formed in K_A and K_C, rtz reduced beside rtr
-    const bool jac = t.m[0]->precond == NBK_PRECOND_JACOBI;
+    const bool jac = !VP && t.m[0]->precond == NBK_PRECOND_JACOBI;
+    const int vp_t = VP ? t.m[0]->vp_t : 0;  // VPREC emulation (NEXT-4)
     std::vector<VecArgs<T>> vi(P), vr(P);
     for (size_t q = 0; q < P; ++q) {
         vi[q] = vec_args<T>(t.m[q]);
         vi[q].r = r[q]; vi[q].x = x[q]; vi[q].p = p[q]; vi[q].f = t.m[q]->f64;
         vi[q].dinv = fld<T>(t.m[q], 4, fp32);
         vi[q].single = single;
+        vi[q].vp_t = vp_t;
         vr[q] = vi[q];
         vr[q].w = w[q];
     }
-    e = jac ? vec_team<T, VEC_INIT_J>(t, vi, false, err) : vec_team<T, VEC_INIT>(t, vi, false, err);
+    e = jac ? vec_team<T, VEC_INIT_J>(t, vi, false, err) : vec_team<T, VEC_INIT, VP>(t, vi, false, err);
     if (e != cudaSuccess) return e;
     launches += (int64_t)P * (1 + per_fin);
 
@@ -487,14 +508,16 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             aa.rev = rev;
             aa.dinv = fld<T>(c, 4, fp32);
             aa.single = single;
-            e = jac ? launch_ax<T, 2>(aa, s, false, pdl) : launch_ax<T, 1>(aa, s, false, pdl);
+            aa.vp_t = vp_t;
+            e = jac ? launch_ax<T, 2>(aa, s, false, pdl) : launch_ax<T, 1, VP>(aa, s, false, pdl);
             if (e != cudaSuccess) return e;
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = dssum_team<T, true>(t, w, pc, 0, pdl, err, !rev, single)) != cudaSuccess) return e;
+        if ((e = dssum_team<T, true, VP>(t, w, pc, 0, pdl, err, !rev, single, vp_t)) != cudaSuccess)
+            return e;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 2], s, cudaEventRecordExternal);
         for (size_t q = 0; q < P; ++q) vr[q].rev = rev;
-        e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pdl, err) : vec_team<T, VEC_RUPD>(t, vr, pdl, err);
+        e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pdl, err) : vec_team<T, VEC_RUPD, VP>(t, vr, pdl, err);
         if (e != cudaSuccess) return e;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 3], s, cudaEventRecordExternal);
         rev = !rev;
@@ -502,7 +525,7 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
     }
     for (size_t q = 0; q < P; ++q) {
         nbk_ctx* c = t.m[q];
-        k_tail_x<T><<<vec_grid(c->n), 256, 0, s>>>(x[q], p[q], c->st, c->n);
+        k_tail_x<T, VP><<<vec_grid(c->n), 256, 0, s>>>(x[q], p[q], c->st, c->n, vp_t);
         ++launches;
         // final FP64 residual check (C12): x64 = (double)x ; r_true = f - A x64
         if (fp32) {
@@ -530,7 +553,8 @@ static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
 static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_graph** out)
 {
     nbk_ctx* c = t.m[0];
-    auto key = std::make_tuple((int)prec, niter, c->profiling * 2 + c->precond);
+    auto key = std::make_tuple((int)prec + 4 * (prec == NBK_VPREC ? c->vp_t : 0), niter,
+                               c->profiling * 2 + c->precond);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) { *out = &it->second; return NBK_OK; }
     nbk_graph g;
@@ -540,9 +564,10 @@ static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_gr
     }
     NBK_CUDA(c, cudaStreamBeginCapture(t.s, cudaStreamCaptureModeThreadLocal));
     std::string err;
-    cudaError_t e = prec == NBK_FP64 ? enqueue_solve<double>(t, niter, &g, false, c->profiling, err)
-                                     : enqueue_solve<float>(t, niter, &g, true, c->profiling, err,
-                                                            prec == NBK_FP32S ? 1 : 0);
+    cudaError_t e = prec == NBK_FP64    ? enqueue_solve<double>(t, niter, &g, false, c->profiling, err)
+                    : prec == NBK_VPREC ? enqueue_solve<double, true>(t, niter, &g, false, c->profiling, err)
+                                        : enqueue_solve<float>(t, niter, &g, true, c->profiling, err,
+                                                               prec == NBK_FP32S ? 1 : 0);
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(t.s, &graph);
     if (e != cudaSuccess) {
@@ -577,6 +602,8 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
     cudaError_t e;
 
     if ((e = launch_ax<double, 0>(a64, c->stream, true)) != cudaSuccess) return e;
+    if (c->N <= NBK_VPREC_MAXN && (e = launch_ax<double, 1, true>(a64, c->stream, true)) != cudaSuccess)
+        return e;
     if ((e = launch_ax<double, 1>(a64, c->stream, true)) != cudaSuccess) return e;
     if ((e = launch_ax<double, 2>(a64, c->stream, true)) != cudaSuccess) return e;
     if ((e = launch_ax<float, 0>(a32, c->stream, true)) != cudaSuccess) return e;
@@ -673,9 +700,14 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
 {
     nbk_ctx* c = t.m[0];
     if (niter < 1 || niter > NBK_MAX_NITER) return fail(c, NBK_EINVAL, "niter out of range");
-    if (prec != NBK_FP64 && prec != NBK_FP32 && prec != NBK_FP32S) return fail(c, NBK_EINVAL, "bad precision");
-    for (nbk_ctx* m : t.m)
-        if (prec != NBK_FP64 && !m->G32) return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
+    if (prec != NBK_FP64 && prec != NBK_FP32 && prec != NBK_FP32S && prec != NBK_VPREC)
+        return fail(c, NBK_EINVAL, "bad precision");
+    for (nbk_ctx* m : t.m) {
+        if ((prec == NBK_FP32 || prec == NBK_FP32S) && !m->G32)
+            return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
+        if (prec == NBK_VPREC && m->vp_t != c->vp_t) return fail(c, NBK_EINVAL, "members differ in VPREC t");
+        if (prec == NBK_VPREC && m->N > NBK_VPREC_MAXN) return fail(c, NBK_EINVAL, "VPREC emulation supports N <= 12");
+    }
     nbk_status st = refresh_h0(t);
     if (st != NBK_OK) return st;
     if (c->precond == NBK_PRECOND_JACOBI) {
@@ -1021,6 +1053,14 @@ nbk_status nbk_glsc3(nbk_ctx* c, const void* a_dev, const void* b_dev, nbk_preci
     return glsc3_team_abi(t, &a_dev, &b_dev, prec, out);
 }
 
+nbk_status nbk_set_vprec(nbk_ctx* c, int32_t t)
+{
+    if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
+    if (t < 1 || t > 52) return fail(c, NBK_EINVAL, "VPREC mantissa bits must lie in [1, 52]");
+    c->vp_t = t;
+    return NBK_OK;
+}
+
 nbk_status nbk_set_precond(nbk_ctx* c, int32_t precond)
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
@@ -1137,7 +1177,8 @@ nbk_status nbk_solve_launches(const nbk_ctx* c, int32_t niter, nbk_precision pre
     const int64_t multi = c->nranks > 1 ? 1 : 0;
     // init (+fin), per iteration K_A, K_B, K_C (+ pack, merge, 2 fin), tail_x, [upcast],
     // final check K_A, K_B, K_C (+ pack, merge, fin)
-    *launches = (1 + multi) + (3 + 4 * multi) * (int64_t)niter + 1 + (prec != NBK_FP64 ? 1 : 0) +
+    *launches = (1 + multi) + (3 + 4 * multi) * (int64_t)niter + 1 +
+                ((prec == NBK_FP32 || prec == NBK_FP32S) ? 1 : 0) +
                 (3 + 3 * multi);
     return NBK_OK;
 }

@@ -162,8 +162,9 @@ struct MeshView {
     int ezg;             // global element layers
     int N;
     int64_t E;           // local elements
-    // magic numbers for division by ex and ex*ey (uint32 fast division)
+    // magic numbers for division by ex, ex*ey, N and N^3 (uint32 fast division)
     uint32_t ex_mul, ex_shr, exy_mul, exy_shr;
+    uint32_t n_mul, n_shr, n3_mul, n3_shr;
 };
 
 // q = floor(n / d) with (mul, shr) from make_fast_div (round-up method of
@@ -231,6 +232,33 @@ __device__ __forceinline__ double dot_term(float a, float b, double c, bool sing
 __device__ __forceinline__ double dot_term(double a, double b, double c, bool)
 {
     return dot_term(a, b, c);
+}
+
+// VPREC emulation (NEXT-4): a binary64 value rounded to t explicit
+// mantissa bits, round to nearest, ties to even, on the bit pattern (binary64
+// exponent range; subnormals rounded at the same absolute bit position).
+__device__ __forceinline__ double vprec_round(double x, int t)
+{
+    if (t >= 52 || !isfinite(x)) return x;
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const int drop = 52 - t;
+    const unsigned long long mask = (1ull << drop) - 1ull, half = 1ull << (drop - 1);
+    const unsigned long long low = b & mask;
+    b &= ~mask;
+    if (low > half || (low == half && ((b >> drop) & 1ull))) b += 1ull << drop;
+    return __longlong_as_double((long long)b);
+}
+// VP: round an operation's result (compiled away when VP is false)
+template <bool VP>
+__device__ __forceinline__ double vr(double x, int t)
+{
+    if constexpr (VP) return vprec_round(x, t); else return x;
+}
+template <bool VP>
+__device__ __forceinline__ float vr(float x, int)
+{
+    static_assert(!VP, "VPREC emulation runs in binary64");
+    return x;
 }
 
 // RN32 of the sum represented by a double-double (hi = RN64(hi + lo)): RN32(hi)
@@ -340,7 +368,7 @@ struct CgState {
     int it;            // current iteration k (1-based)
     int zero;          // rtz1 == 0 reached (rule C9): alpha = beta = 0 from then on
     int defect;        // first iteration with pap <= 0 or a non-finite scalar
-    int pad1;
+    int vp_t;          // VPREC emulation: mantissa bits of the running solve (0 = off)
     unsigned int cnt[4];  // last-block counters (reset by the finaliser)
 };
 

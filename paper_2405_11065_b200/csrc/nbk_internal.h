@@ -13,6 +13,7 @@
 #define NBK_MAX_NITER 10000
 #define NBK_VEC_GRID_MAX (148 * 8)
 #define NBK_MAX_RANKS 64
+#define NBK_VPREC_MAXN 12  // VPREC emulation kernels are built for N <= 12
 
 struct nbk_graph {
     cudaGraph_t graph = nullptr;
@@ -41,6 +42,7 @@ struct nbk_ctx {
     double* dinv64 = nullptr;             // Jacobi: 1 / assembled diag(A) (masked: 1)
     float* dinv32 = nullptr;              // RN32(dinv64) (C11)
     int precond = NBK_PRECOND_NONE;
+    int vp_t = 23;                        // VPREC emulation: mantissa bits (NBK_VPREC solves)
     int dinv_dirty = 1;                   // own diagonal to be (re)assembled
     double *hist = nullptr, *trace = nullptr;
     nbk::dd* parts = nullptr;

@@ -59,10 +59,13 @@ __device__ __forceinline__ void lds_row(T (&dst)[N], const T* src)
 
 // b[kk] = fma(d[kk], t, b[kk]) for kk = 0..N-1 (packed FFMA2 for FP32: per-lane
 // numerics identical to __fmaf_rn, so the canonical order is unchanged).
-template <typename T, int N>
-__device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t)
+template <typename T, int N, bool VP = false>
+__device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t, int vt = 0)
 {
-    if constexpr (sizeof(T) == 4 && N % 2 == 0) {
+    if constexpr (VP) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) b[q] = vr<VP>(fma_t<T>(d[q], t, b[q]), vt);
+    } else if constexpr (sizeof(T) == 4 && N % 2 == 0) {
         const float2 tt = make_float2(t, t);
 #pragma unroll
         for (int q = 0; q < N / 2; ++q) {
@@ -75,6 +78,14 @@ __device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t)
 #pragma unroll
         for (int q = 0; q < N; ++q) b[q] = fma_t<T>(d[q], t, b[q]);
     }
+}
+
+// glsc3 term with the VPREC rounding of the product (NEXT-4): vp(a b) c
+template <bool VP, typename T>
+__device__ __forceinline__ double dot_term_vp(T a, T b, double c, bool single, int vt)
+{
+    if constexpr (VP) return __dmul_rn(vr<VP>(mul_t<T>(a, b), vt), c);
+    else return dot_term(a, b, c, single);
 }
 
 // ------------------------------------------------------------ K_A config
@@ -138,6 +149,7 @@ struct AxArgs {
     const CgState* st; // fused: beta, alpha_prev
     const T* dinv;     // fused Jacobi PCG: z = r * dinv replaces r in the p update
     int single;        // paper-literal single mode: pap terms RN32(w p) (NEXT-2)
+    int vp_t;          // VPREC emulation (NEXT-4): mantissa bits (kernels instantiated with VP)
     dd* parts;         // fused: pap partial per block
     MeshView mesh;
     int mask;          // assign +0 to Dirichlet points of w
@@ -147,10 +159,11 @@ struct AxArgs {
 // ---------------------------------------------------------------- K_A
 // FUSED: 0 = plain ax (u -> w); 1 = CG step (p = beta p + r); 2 = Jacobi PCG
 // step (p = beta p + z, z = RN(r * dinv) formed here: S:376-384, T1 line 2).
-template <typename T, int N, int FUSED>
+template <typename T, int N, int FUSED, bool VP = false>
 __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     k_ax(AxArgs<T> a)
 {
+    const int vt = a.vp_t;  // VP: every operation's result rounded to vt bits (NEXT-4)
     constexpr int N2 = N * N, N3 = N * N * N, EPB = ax_epb<T>(N);
     constexpr bool STAGE = ax_stage_g<T>(N);
     constexpr bool TMA = STAGE && (N % 2 == 0);
@@ -236,8 +249,8 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 const T po = v;
                 T zk = rreg[k];
                 if constexpr (FUSED == 2) zk = mul_t<T>(rreg[k], dreg[k]);  // solveM (Jacobi)
-                v = fma_t<T>(betaT, po, zk);
-                a.x[base + k * N2] = fma_t<T>(alphaT, po, xreg[k]);
+                v = vr<VP>(fma_t<T>(betaT, po, zk), vt);
+                a.x[base + k * N2] = vr<VP>(fma_t<T>(alphaT, po, xreg[k]), vt);
                 a.p[base + k * N2] = v;
                 ue[k * N2 + ij] = v;
             }
@@ -272,26 +285,26 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             lds_row<T, N>(Dk, sD + k * N);              // D[k][:] (broadcast)
             T ur = 0, us = 0, ut = 0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) ur = fma_t<T>(Dri[l], urow[l], ur);
+            for (int l = 0; l < N; ++l) ur = vr<VP>(fma_t<T>(Dri[l], urow[l], ur), vt);
 #pragma unroll
-            for (int l = 0; l < N; ++l) us = fma_t<T>(Drj[l], ue[k * N2 + l * N + i], us);
+            for (int l = 0; l < N; ++l) us = vr<VP>(fma_t<T>(Drj[l], ue[k * N2 + l * N + i], us), vt);
 #pragma unroll
-            for (int l = 0; l < N; ++l) ut = fma_t<T>(Dk[l], ureg[l], ut);
+            for (int l = 0; l < N; ++l) ut = vr<VP>(fma_t<T>(Dk[l], ureg[l], ut), vt);
             const T g1 = Ge[0 * N3 + k * N2], g2 = Ge[1 * N3 + k * N2], g3 = Ge[2 * N3 + k * N2];
             const T g4 = Ge[3 * N3 + k * N2], g5 = Ge[4 * N3 + k * N2], g6 = Ge[5 * N3 + k * N2];
-            T wr = mul_t<T>(g1, ur);
-            wr = fma_t<T>(g2, us, wr);
-            wr = fma_t<T>(g3, ut, wr);
-            T ws = mul_t<T>(g2, ur);
-            ws = fma_t<T>(g4, us, ws);
-            ws = fma_t<T>(g5, ut, ws);
-            T wt = mul_t<T>(g3, ur);
-            wt = fma_t<T>(g5, us, wt);
-            wt = fma_t<T>(g6, ut, wt);
+            T wr = vr<VP>(mul_t<T>(g1, ur), vt);
+            wr = vr<VP>(fma_t<T>(g2, us, wr), vt);
+            wr = vr<VP>(fma_t<T>(g3, ut, wr), vt);
+            T ws = vr<VP>(mul_t<T>(g2, ur), vt);
+            ws = vr<VP>(fma_t<T>(g4, us, ws), vt);
+            ws = vr<VP>(fma_t<T>(g5, ut, ws), vt);
+            T wt = vr<VP>(mul_t<T>(g3, ur), vt);
+            wt = vr<VP>(fma_t<T>(g5, us, wt), vt);
+            wt = vr<VP>(fma_t<T>(g6, ut, wt), vt);
             // own (i,j,k) slot of g1/g2 is dead after the reads above
             wre[k * N2 + ij] = wr;
             wse[k * N2 + ij] = ws;
-            fma_row<T, N>(b, Dk, wt);   // b[kk] = fma(D[k][kk], wt, b[kk])
+            fma_row<T, N, VP>(b, Dk, wt, vt);   // b[kk] = fma(D[k][kk], wt, b[kk])
         }
     }
     __syncthreads();
@@ -321,10 +334,10 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             lds_row<T, N>(wrow, wre + k * N2 + j * N);  // wr[k][j][:]
             T s = 0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) s = fma_t<T>(Dci[l], wrow[l], s);
+            for (int l = 0; l < N; ++l) s = vr<VP>(fma_t<T>(Dci[l], wrow[l], s), vt);
 #pragma unroll
-            for (int l = 0; l < N; ++l) s = fma_t<T>(Dcj[l], wse[k * N2 + l * N + i], s);
-            T wv = add_t<T>(s, b[k]);
+            for (int l = 0; l < N; ++l) s = vr<VP>(fma_t<T>(Dcj[l], wse[k * N2 + l * N + i], s), vt);
+            T wv = vr<VP>(add_t<T>(s, b[k]), vt);
             const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
             if (a.mask && masked) wv = 0;   // C5: assign +0
             a.w[base + k * N2] = wv;
@@ -332,7 +345,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 // element-interior points (m == 1) contribute w p c here; shared
                 // nodes contribute once per node in K_B (bitwise-equal exact sum).
                 const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
-                if (!sxy && !sz) acc.add(dot_term(wv, ureg[k], 1.0, a.single));
+                if (!sxy && !sz) acc.add(dot_term_vp<VP>(wv, ureg[k], 1.0, a.single, vt));
             }
         }
     }
@@ -347,12 +360,16 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
 // CG scalars from the globally reduced inner products (rules C7, C9); run by
 // one thread: the last block of the reducing kernel (1 rank) or k_fin after
 // the rank-ordered combination of the per-rank partials (several ranks).
-__device__ __forceinline__ void fin_alpha(CgState* st, dd pap_dd, double* trace, bool single)
+__device__ __forceinline__ void fin_alpha(CgState* st, dd pap_dd, double* trace, bool single,
+                                          int vp_t = 0)
 {
     const int k = st->it;
     const double rtz1 = st->rtr;
     double alpha = 0.0, pap;
-    if (single) {  // NEXT-2: binary32 scalars (rtz1 already a binary32 value)
+    if (vp_t) {  // NEXT-4: the reduction and the division rounded to vp_t bits
+        pap = vprec_round(pap_dd.hi, vp_t);
+        if (!st->zero) alpha = vprec_round(rtz1 / pap, vp_t);
+    } else if (single) {  // NEXT-2: binary32 scalars (rtz1 already a binary32 value)
         const float pap32 = dd_to_float_rn(pap_dd.hi, pap_dd.lo);
         pap = pap32;
         if (!st->zero) alpha = __fdiv_rn((float)rtz1, pap32);
@@ -384,12 +401,18 @@ __host__ __device__ constexpr bool vec_jacobi(int mode) { return mode == VEC_INI
 // st->rtr holds the current rtz1.
 template <int MODE>
 __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, double* hist, double* trace,
-                                        bool single)
+                                        bool single, int vp_t = 0)
 {
-    // single mode (NEXT-2): binary32 sums, sqrt and division
-    const double rtr = single ? (double)dd_to_float_rn(rtr_dd.hi, rtr_dd.lo) : rtr_dd.hi;
-    const double rtz = single ? (double)dd_to_float_rn(rtz_dd.hi, rtz_dd.lo) : rtz_dd.hi;
-    const double h = single ? (double)__fsqrt_rn((float)rtr) : sqrt(rtr);
+    // single mode (NEXT-2): binary32 sums, sqrt and division; VPREC (NEXT-4): every
+    // result rounded to vp_t bits
+    double rtr = single ? (double)dd_to_float_rn(rtr_dd.hi, rtr_dd.lo) : rtr_dd.hi;
+    double rtz = single ? (double)dd_to_float_rn(rtz_dd.hi, rtz_dd.lo) : rtz_dd.hi;
+    if (vp_t) {
+        rtr = vprec_round(rtr, vp_t);
+        rtz = vprec_round(rtz, vp_t);
+    }
+    const double h = single ? (double)__fsqrt_rn((float)rtr)
+                            : (vp_t ? vprec_round(sqrt(rtr), vp_t) : sqrt(rtr));
     if constexpr (MODE == VEC_INIT || MODE == VEC_INIT_J) {
         st->rtr = rtz;
         st->rtz2 = 0.0;
@@ -415,7 +438,8 @@ __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, doubl
         double beta = 0.0;
         if (!st->zero)
             beta = single ? (double)__fdiv_rn((float)rtz1_next, (float)rtz2_next)
-                          : rtz1_next / rtz2_next;  // C7
+                          : (vp_t ? vprec_round(rtz1_next / rtz2_next, vp_t)
+                                  : rtz1_next / rtz2_next);  // C7
         st->beta = beta;
         st->beta32 = (float)beta;
         st->it = k + 1;
@@ -453,6 +477,7 @@ struct DssumArgs {
     int fin;                  // fused: 1 = last block forms alpha (1 rank); 0 = publish only
     int rev;                  // visit the tiles in reverse order
     int single;               // paper-literal single mode (NEXT-2)
+    int vp_t;                 // VPREC emulation (NEXT-4)
     MeshView mesh;
 };
 
@@ -494,7 +519,7 @@ __device__ __forceinline__ int tile_seg_load(const int32_t* g2, const int32_t* g
 // The tiles of this block (grid-stride), node by node (all multiplicities of
 // a tile in one loop, two nodes per thread per step, every load of both
 // issued before use; p by the read-only path).
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool VP = false>
 __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
 {
     for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x) {
@@ -525,23 +550,23 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
                 T sum = v[h][0];                          // C4: ascending local index
 #pragma unroll
                 for (int c = 1; c < 8; ++c)
-                    if (c < m[h]) sum = add_t<T>(sum, v[h][c]);
+                    if (c < m[h]) sum = vr<VP>(add_t<T>(sum, v[h][c]), a.vp_t);
                 if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[h][0])) sum = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) a.w[ix[h][c]] = sum;
-                if constexpr (FUSED) acc.add(dot_term(sum, p0[h], 1.0, a.single));  // one term per node
+                if constexpr (FUSED) acc.add(dot_term_vp<VP>(sum, p0[h], 1.0, a.single, a.vp_t));  // one term per node
             }
         }
     }
 }
 
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool VP = false>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
     pdl_wait();
-    dssum_tiles<T, FUSED>(a, acc);
+    dssum_tiles<T, FUSED, VP>(a, acc);
     pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
@@ -555,7 +580,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_dssum(DssumArgs
         if (publish_and_check_last(a.parts, a.nA + blockIdx.x, v, &a.st->cnt[0], total)) {
             dd pap_dd = reduce_partials(a.parts, a.nA + (int)gridDim.x);
             if (threadIdx.x == 0) {
-                fin_alpha(a.st, pap_dd, a.trace, a.single);
+                fin_alpha(a.st, pap_dd, a.trace, a.single, a.vp_t);
                 a.st->cnt[0] = 0;
             }
         }
@@ -581,6 +606,7 @@ struct VecArgs {
     double* trace;
     dd* slot;           // multi-rank: this rank's reduced partial (NULL: finalise here)
     int single;         // paper-literal single mode: RN32(a b) terms, binary32 scalars
+    int vp_t;           // VPREC emulation (NEXT-4)
     int rev;            // visit the chunks in reverse order
     MeshView mesh;
 };
@@ -628,19 +654,23 @@ struct VecT {
 };
 
 // c = 1/m (R8) of the V consecutive points L..L+V-1 (one element, N3 % V == 0),
-// stepping (i, j, k) incrementally from one division.
-template <int N, int V>
+// stepping (i, j, k) incrementally from one division (fast division by the
+// runtime N and N^3; one vector kernel serves every N).
+template <int V>
 __device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, double (&c)[V])
 {
-    constexpr int N2 = N * N, N3 = N * N * N, n1 = N - 1;
-    const uint32_t e = (uint32_t)(L / N3);
-    const int rem = (int)(L - (int64_t)e * N3);
+    const int N = m.N, n1 = N - 1;
+    const uint32_t Lu = (uint32_t)L;  // n_local < 2^31 (validated at set-up)
+    const uint32_t e = fast_div(Lu, m.n3_mul, m.n3_shr);
+    const uint32_t rem = Lu - e * (uint32_t)(N * N * N);
+    const uint32_t q1 = fast_div(rem, m.n_mul, m.n_shr);
+    const uint32_t q2 = fast_div(q1, m.n_mul, m.n_shr);
+    int i = (int)(rem - q1 * (uint32_t)N), j = (int)(q1 - q2 * (uint32_t)N), k = (int)q2;
     const ElemCoord ec = elem_coord(m, e);
-    int i = rem % N, j = (rem / N) % N, k = rem / N2;
     const bool xl = ec.ax > 0, xh = ec.ax < m.ex - 1, yl = ec.ay > 0, yh = ec.ay < m.ey - 1;
     const bool zl = ec.azg > 0, zh = ec.azg < m.ezg - 1;
     int myz = (((j == 0 && yl) || (j == n1 && yh)) ? 2 : 1) * (((k == 0 && zl) || (k == n1 && zh)) ? 2 : 1);
-    if constexpr (N % V == 0) {  // the chunk lies in one (j, k) row
+    if (N % V == 0) {  // the chunk lies in one (j, k) row
 #pragma unroll
         for (int t = 0; t < V; ++t) {
             const int ii = i + t;
@@ -665,7 +695,7 @@ __device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, doub
 // (N^3 % 4 == 0) in one element, 16-byte loads/stores; structural c = 1/m.
 // Per-chunk loads and arithmetic of each mode (split so that the loads of two
 // chunks can be issued before either is used).
-template <typename T, int V, int MODE>
+template <typename T, int V, int MODE, bool VP = false>
 struct VecChunk {
     VecT<T, V> A, B, C;
     VecT<double, V> F;
@@ -705,21 +735,21 @@ struct VecChunk {
             z.store(a.x + L);
             z.store(a.p + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
+            for (int t = 0; t < V; ++t) acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
         } else if constexpr (MODE == VEC_RUPD) {
             VecT<T, V> r;
 #pragma unroll
-            for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>(am, A.v[t], B.v[t]);  // C8
+            for (int t = 0; t < V; ++t) r.v[t] = vr<VP>(fma_t<T>(am, A.v[t], B.v[t]), a.vp_t);  // C8
             r.store(a.r + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
+            for (int t = 0; t < V; ++t) acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
         } else if constexpr (MODE == VEC_TRUE) {
             VecT<T, V> r;
 #pragma unroll
             for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, A.v[t], (T)F.v[t]);  // C12
             r.store(a.r + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
+            for (int t = 0; t < V; ++t) acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
         } else if constexpr (MODE == VEC_INIT_J) {
             VecT<T, V> r, z;
 #pragma unroll
@@ -732,7 +762,7 @@ struct VecChunk {
             z.store(a.p + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) {
-                acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
+                acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
                 acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t], a.single));  // z = r dinv
             }
         } else if constexpr (MODE == VEC_RUPD_J) {
@@ -742,7 +772,7 @@ struct VecChunk {
             r.store(a.r + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) {
-                acc.add(dot_term(r.v[t], r.v[t], c[t], a.single));
+                acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
                 acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t], a.single));  // z = r dinv
             }
         } else {
@@ -752,43 +782,42 @@ struct VecChunk {
     }
 };
 
-// All chunks of this block (grid-stride).  The CG loop alternates the sweep
+// All chunks of this block (grid-stride).  VP: VPREC rounding (NEXT-4).  The CG loop alternates the sweep
 // direction from kernel to kernel (K_A forward, K_B backward, K_C forward, next
 // K_A backward, ...): each kernel starts where its predecessor ended, on the
 // data still resident in the 126 MB L2.
-template <typename T, int N, int MODE>
+// V = 4 consecutive points per chunk for even N (N^3 % 4 == 0), 1 for odd N.
+template <typename T, int V, int MODE, bool VP = false>
 __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, acc_t& acc2)
 {
-    constexpr int N3 = N * N * N;
-    constexpr int V = (N3 % 4 == 0) ? 4 : ((N3 % 2 == 0) ? 2 : 1);
     const int64_t nch = a.n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // two chunks of V points per thread per step; every load of both is issued
     // before any use (more bytes in flight per thread)
     for (; q0 + stride < nch; q0 += 2 * stride) {
-        VecChunk<T, V, MODE> C0, C1;
+        VecChunk<T, V, MODE, VP> C0, C1;
         const int64_t c0 = a.rev ? nch - 1 - q0 : q0, c1 = a.rev ? nch - 1 - (q0 + stride) : q0 + stride;
         const int64_t L0 = c0 * V, L1 = c1 * V;
         C0.load(a, L0);
         C1.load(a, L1);
         double c[V];
-        chunk_weights<N, V>(a.mesh, L0, c);
+        chunk_weights<V>(a.mesh, L0, c);
         C0.run(a, L0, c, am, acc, acc2);
-        chunk_weights<N, V>(a.mesh, L1, c);
+        chunk_weights<V>(a.mesh, L1, c);
         C1.run(a, L1, c, am, acc, acc2);
     }
     if (q0 < nch) {
-        VecChunk<T, V, MODE> C0;
+        VecChunk<T, V, MODE, VP> C0;
         const int64_t L0 = (a.rev ? nch - 1 - q0 : q0) * V;
         C0.load(a, L0);
         double c[V];
-        chunk_weights<N, V>(a.mesh, L0, c);
+        chunk_weights<V>(a.mesh, L0, c);
         C0.run(a, L0, c, am, acc, acc2);
     }
 }
 
-template <typename T, int N, int MODE>
+template <typename T, int V, int MODE, bool VP = false>
 __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 {
     constexpr bool J = vec_jacobi(MODE);
@@ -798,7 +827,7 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
     if constexpr (MODE == VEC_RUPD || MODE == VEC_RUPD_J) {
         if constexpr (sizeof(T) == 8) am = (T)a.st->alpham; else am = (T)a.st->alpham32;
     }
-    vec_loop<T, N, MODE>(a, am, acc, acc2);
+    vec_loop<T, V, MODE, VP>(a, am, acc, acc2);
     pdl_launch_dependents();
     dd v = block_reduce_dd(acc.get());
     dd v2 = J ? block_reduce_dd(acc2.get()) : dd{0.0, 0.0};
@@ -815,7 +844,7 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
                 a.slot[0] = tot;
                 a.slot[1] = tot2;
             } else {
-                fin_rtr<MODE>(a.st, tot, tot2, a.hist, a.trace, a.single);
+                fin_rtr<MODE>(a.st, tot, tot2, a.hist, a.trace, a.single, a.vp_t);
             }
             a.st->cnt[1] = 0;
         }
@@ -823,14 +852,14 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 }
 
 // x = fma(alphaT, p, x) after the last iteration (deferred C8 x update).
-template <typename T>
-__global__ void __launch_bounds__(256) k_tail_x(T* x, const T* p, const CgState* st, int64_t n)
+template <typename T, bool VP = false>
+__global__ void __launch_bounds__(256) k_tail_x(T* x, const T* p, const CgState* st, int64_t n, int vt)
 {
     T al;
     if constexpr (sizeof(T) == 8) al = (T)st->alpha; else al = (T)st->alpha32;
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
          L += (int64_t)gridDim.x * blockDim.x)
-        x[L] = fma_t<T>(al, p[L], x[L]);
+        x[L] = vr<VP>(fma_t<T>(al, p[L], x[L]), vt);
 }
 
 // x64 = (double)x32 (exact, C12) ; G32/D32 = RN32(G64/D64) (C11).
@@ -994,7 +1023,8 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
 // and run the scalar finaliser.  KIND: 0 = alpha (pap); 1 + VecMode = rtr etc.
 // gather holds two dd per rank: [2r] the value, [2r + 1] rtz (Jacobi modes).
 template <int KIND>
-__global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double* trace, int single)
+__global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double* trace, int single,
+                      int vp_t)
 {
     if (threadIdx.x != 0) return;
     dd t{__ldcg(&gather[0].hi), __ldcg(&gather[0].lo)};
@@ -1003,8 +1033,8 @@ __global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double
         t = dd_add(t, dd{__ldcg(&gather[2 * r].hi), __ldcg(&gather[2 * r].lo)});
         t2 = dd_add(t2, dd{__ldcg(&gather[2 * r + 1].hi), __ldcg(&gather[2 * r + 1].lo)});
     }
-    if constexpr (KIND == 0) fin_alpha(st, t, trace, single);
-    else fin_rtr<KIND - 1>(st, t, vec_jacobi(KIND - 1) ? t2 : t, hist, trace, single);
+    if constexpr (KIND == 0) fin_alpha(st, t, trace, single, vp_t);
+    else fin_rtr<KIND - 1>(st, t, vec_jacobi(KIND - 1) ? t2 : t, hist, trace, single, vp_t);
 }
 
 }  // namespace nbk

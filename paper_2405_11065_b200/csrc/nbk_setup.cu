@@ -72,6 +72,8 @@ MeshView make_view(const nbk_mesh* m, const nbk_dist* d)
     v.E = (int64_t)v.ex * v.ey * v.ez_local;
     make_fast_div((uint32_t)v.ex, v.ex_mul, v.ex_shr);
     make_fast_div((uint32_t)(v.ex * v.ey), v.exy_mul, v.exy_shr);
+    make_fast_div((uint32_t)v.N, v.n_mul, v.n_shr);
+    make_fast_div((uint32_t)(v.N * v.N * v.N), v.n3_mul, v.n3_shr);
     return v;
 }
 

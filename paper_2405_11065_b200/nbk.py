@@ -22,15 +22,15 @@ LIB_PATH = os.path.join(HERE, "csrc", "libnbk.so")
 NBK_OK, NBK_EINVAL, NBK_EDEFECT, NBK_ECUDA, NBK_ENCCL, NBK_ENOMEM, NBK_ESTATE = 0, 2, 3, 4, 5, 6, 7
 NBK_FP64, NBK_FP32 = 0, 1
 AX_LOCAL, AX_DSSUM, AX_MASK = 0, 1, 2
-NBK_FP32S = 2
-PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32, "fp32s": NBK_FP32S}
+NBK_FP32S, NBK_VPREC = 2, 3
+PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32, "fp32s": NBK_FP32S, "vprec": NBK_VPREC}
 PRECOND = {"none": 0, "jacobi": 1}
 
 # every symbol include/nbk.h declares
 SYMBOLS = ["nbk_workspace_bytes", "nbk_partition", "nbk_nccl_unique_id", "nbk_cg_setup",
            "nbk_load_arrays", "nbk_get_arrays", "nbk_ax_apply", "nbk_dssum", "nbk_glsc3",
            "nbk_cg_solve", "nbk_cg_solve_host", "nbk_get_solution", "nbk_solution_ptr",
-           "nbk_set_precond", "nbk_load_precond", "nbk_get_precond", "nbk_set_profiling",
+           "nbk_set_vprec", "nbk_set_precond", "nbk_load_precond", "nbk_get_precond", "nbk_set_profiling",
            "nbk_query", "nbk_solve_launches", "nbk_group_link",
            "nbk_group_ax_apply", "nbk_group_dssum", "nbk_group_glsc3", "nbk_group_cg_solve",
            "nbk_last_error", "nbk_version", "nbk_destroy"]
@@ -103,6 +103,7 @@ def load() -> ctypes.CDLL:
         "nbk_solution_ptr": [vp, ctypes.c_int, P(vp)],
         "nbk_set_profiling": [vp, i32],
         "nbk_set_precond": [vp, i32],
+        "nbk_set_vprec": [vp, i32],
         "nbk_load_precond": [vp, vp],
         "nbk_get_precond": [vp, vp],
         "nbk_query": [vp, P(CInfo)],
@@ -274,6 +275,10 @@ class Context:
                                   PREC[prec], ctypes.byref(out)), self._ctx)
         return float(out.value)
 
+    def set_vprec(self, t: int):
+        """Mantissa bits of the VPREC-emulated solver (cg_solve(..., 'vprec'))."""
+        _check(self.lib.nbk_set_vprec(self._ctx, int(t)), self._ctx)
+
     def set_precond(self, precond: str):
         """'none' (z = r, the default) or 'jacobi' (z = r / diag(A))."""
         _check(self.lib.nbk_set_precond(self._ctx, PRECOND[precond]), self._ctx)
@@ -395,6 +400,10 @@ class Group:
 
     def solution(self) -> np.ndarray:
         return np.concatenate([c.solution() for c in self.ctxs], axis=0)
+
+    def set_vprec(self, t: int):
+        """Mantissa bits of the VPREC-emulated solver (cg_solve(..., 'vprec'))."""
+        _check(self.lib.nbk_set_vprec(self._ctx, int(t)), self._ctx)
 
     def set_precond(self, precond: str):
         for c in self.ctxs:
