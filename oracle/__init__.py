@@ -88,6 +88,9 @@ def lib():
         L.ora_vprec_round.argtypes = [c_dbl, ctypes.c_int]
         L.ora_cgvp.restype = ctypes.c_int
         L.ora_cgvp.argtypes = [ctypes.c_int] * 4 + [_p] * 3 + [ctypes.c_int] * 2 + [_p] * 3
+        L.ora_cgpm.restype = ctypes.c_int
+        L.ora_cgpm.argtypes = ([ctypes.c_int] * 4 + [_p] * 3 + [ctypes.c_int] * 2 + [c_u64] +
+                               [ctypes.c_int] + [_p] * 3)
         L.ora_jacobi_dinv.restype = None
         L.ora_jacobi_dinv.argtypes = [ctypes.c_int] * 4 + [_p] * 4
         L.ora_true_residual.restype = c_dbl
@@ -267,6 +270,24 @@ def cg_vprec(mesh: Mesh, D, G, f, niter: int, t: int) -> CgResult:
     x = np.zeros_like(f)
     rc = lib().ora_cgvp(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), int(t), niter, _ptr(x), _ptr(hist),
                         _ptr(trace))
+    return CgResult(x=x, hist=hist, trace=trace, defect=int(rc))
+
+
+EMU = {"vprec": 1, "rr": 2, "mca": 3}
+
+
+def cg_emulated(mesh: Mesh, D, G, f, niter: int, mode: str, t: int, seed: int = 0) -> CgResult:
+    """Precision-emulated CG (NEXT-4): 'vprec' (every operation rounded to t
+    bits), 'rr' (random rounding of every result at virtual precision t) or
+    'mca' (operands and results perturbed); seed selects the RR / MCA sample."""
+    D = np.ascontiguousarray(D, np.float64)
+    G = np.ascontiguousarray(G, np.float64)
+    f = np.ascontiguousarray(f, np.float64)
+    hist = np.zeros(niter + 1)
+    trace = np.zeros((niter, 5))
+    x = np.zeros_like(f)
+    rc = lib().ora_cgpm(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), EMU[mode], int(t),
+                        seed & (2**64 - 1), niter, _ptr(x), _ptr(hist), _ptr(trace))
     return CgResult(x=x, hist=hist, trace=trace, defect=int(rc))
 
 

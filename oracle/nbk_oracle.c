@@ -871,6 +871,192 @@ int ora_cg32s(int ex, int ey, int ez, int N, const double* D, const double* G, c
     return rc;
 }
 
+/* ------------------------------------------------------------------ */
+/* Precision-emulated CG (NEXT-4), the CG loop of   */
+/* T1 written out with every operation through an emulation op:         */
+/*   VPREC (mode 1): result rounded to t mantissa bits;                 */
+/*   RR    (mode 2): result -> x + 2^(e_x - t) xi (random rounding);    */
+/*   MCA   (mode 3): operands and result perturbed (full MCA);          */
+/* xi = SplitMix64(seed, 4 key + slot) - 1/2 in [-1/2, 1/2), e_x =       */
+/* floor(log2|x|) + 1, slot 0 = result, 1.. = operands in order.        */
+/* key = ((it*8 + phase) * 2^40 + L) * 128 + op, phases A (ax step: ops  */
+/* per output point: 0 p update, 1 x update [key of iteration it+1, the  */
+/* iteration whose step applies it], 2.. ur, 2+N.. us, 2+2N.. ut chains, */
+/* 2+3N.. metric (9), 11+3N.. r/s transpose chain (2N), 11+5N+l t chain, */
+/* 11+6N final add), B (dssum: chain add c of a node, L = first copy),   */
+/* C (r update), S (scalars, L = 0: 0 pap, 1 alpha, 2 rtr, 3 sqrt, 4     */
+/* beta of the next iteration; iteration 0 = initial rtr, h0).  Each     */
+/* correctly rounded glsc3 is one operation (VPREC also rounds the       */
+/* products of its terms).  This function shares no code with the       */
+/* macro-generated VPREC loop above (cross-checked in the pins).         */
+/* ------------------------------------------------------------------ */
+static int g_pm_mode = 0, g_pm_t = 52;
+static uint64_t g_pm_seed = 0;
+enum { ORA_PH_A = 0, ORA_PH_B = 1, ORA_PH_C = 2, ORA_PH_S = 3 };
+
+static uint64_t pm_key(int it, int ph, int64_t L, int o)
+{
+    return (((uint64_t)it * 8u + (uint64_t)ph) * ((uint64_t)1 << 40) + (uint64_t)L) * 128u + (uint64_t)o;
+}
+static double pm_inexact(double x, uint64_t key, int slot)
+{
+    if (x == 0.0 || !isfinite(x)) return x;
+    uint64_t z = ora_splitmix64(g_pm_seed, 4 * key + (uint64_t)slot);
+    double xi = (double)(z >> 11) * 0x1.0p-53 - 0.5;
+    int ex;
+    frexp(x, &ex);
+    return x + ldexp(xi, ex - g_pm_t);
+}
+static double pm_res(double r, uint64_t key)
+{
+    if (g_pm_mode == 1) return ora_vprec_round(r, g_pm_t);
+    if (g_pm_mode >= 2) return pm_inexact(r, key, 0);
+    return r;
+}
+static double pm_in(double x, uint64_t key, int slot) { return g_pm_mode == 3 ? pm_inexact(x, key, slot) : x; }
+static double P_FMA(double a, double b, double c, uint64_t k)
+{
+    return pm_res(fma(pm_in(a, k, 1), pm_in(b, k, 2), pm_in(c, k, 3)), k);
+}
+static double P_MUL(double a, double b, uint64_t k) { return pm_res(pm_in(a, k, 1) * pm_in(b, k, 2), k); }
+static double P_ADD(double a, double b, uint64_t k) { return pm_res(pm_in(a, k, 1) + pm_in(b, k, 2), k); }
+static double P_DIV(double a, double b, uint64_t k) { return pm_res(pm_in(a, k, 1) / pm_in(b, k, 2), k); }
+static double P_SQRT(double a, uint64_t k) { return pm_res(sqrt(pm_in(a, k, 1)), k); }
+
+static void pm_ax_local(int it, int64_t E, int N, const double* D, const double* G, const double* u,
+                        double* w)
+{
+    const int64_t nn = (int64_t)N * N * N;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+        const double* ue = u + e * nn;
+        const double* Ge = G + e * 6 * nn;
+        double* we = w + e * nn;
+        double* wr = (double*)malloc(sizeof(double) * 3 * nn);
+        double* ws = wr + nn;
+        double* wt = ws + nn;
+        for (int k = 0; k < N; ++k)
+            for (int j = 0; j < N; ++j)
+                for (int i = 0; i < N; ++i) {
+                    int64_t pt = ((int64_t)k * N + j) * N + i, L = e * nn + pt;
+                    double ur = 0, us = 0, ut = 0;
+                    for (int l = 0; l < N; ++l)
+                        ur = P_FMA(D[i * N + l], ue[((int64_t)k * N + j) * N + l], ur, pm_key(it, ORA_PH_A, L, 2 + l));
+                    for (int l = 0; l < N; ++l)
+                        us = P_FMA(D[j * N + l], ue[((int64_t)k * N + l) * N + i], us, pm_key(it, ORA_PH_A, L, 2 + N + l));
+                    for (int l = 0; l < N; ++l)
+                        ut = P_FMA(D[k * N + l], ue[((int64_t)l * N + j) * N + i], ut, pm_key(it, ORA_PH_A, L, 2 + 2 * N + l));
+                    const double g1 = Ge[0 * nn + pt], g2 = Ge[1 * nn + pt], g3 = Ge[2 * nn + pt];
+                    const double g4 = Ge[3 * nn + pt], g5 = Ge[4 * nn + pt], g6 = Ge[5 * nn + pt];
+                    const int om = 2 + 3 * N;
+                    double a;
+                    a = P_MUL(g1, ur, pm_key(it, ORA_PH_A, L, om));
+                    a = P_FMA(g2, us, a, pm_key(it, ORA_PH_A, L, om + 1));
+                    a = P_FMA(g3, ut, a, pm_key(it, ORA_PH_A, L, om + 2));
+                    wr[pt] = a;
+                    a = P_MUL(g2, ur, pm_key(it, ORA_PH_A, L, om + 3));
+                    a = P_FMA(g4, us, a, pm_key(it, ORA_PH_A, L, om + 4));
+                    a = P_FMA(g5, ut, a, pm_key(it, ORA_PH_A, L, om + 5));
+                    ws[pt] = a;
+                    a = P_MUL(g3, ur, pm_key(it, ORA_PH_A, L, om + 6));
+                    a = P_FMA(g5, us, a, pm_key(it, ORA_PH_A, L, om + 7));
+                    a = P_FMA(g6, ut, a, pm_key(it, ORA_PH_A, L, om + 8));
+                    wt[pt] = a;
+                }
+        for (int k = 0; k < N; ++k)
+            for (int j = 0; j < N; ++j)
+                for (int i = 0; i < N; ++i) {
+                    int64_t L = e * nn + ((int64_t)k * N + j) * N + i;
+                    double a = 0, b = 0;
+                    for (int l = 0; l < N; ++l)
+                        a = P_FMA(D[l * N + i], wr[((int64_t)k * N + j) * N + l], a, pm_key(it, ORA_PH_A, L, 11 + 3 * N + l));
+                    for (int l = 0; l < N; ++l)
+                        a = P_FMA(D[l * N + j], ws[((int64_t)k * N + l) * N + i], a, pm_key(it, ORA_PH_A, L, 11 + 4 * N + l));
+                    for (int l = 0; l < N; ++l)
+                        b = P_FMA(D[l * N + k], wt[((int64_t)l * N + j) * N + i], b, pm_key(it, ORA_PH_A, L, 11 + 5 * N + l));
+                    we[((int64_t)k * N + j) * N + i] = P_ADD(a, b, pm_key(it, ORA_PH_A, L, 11 + 6 * N));
+                }
+        free(wr);
+    }
+}
+
+static void pm_dssum_mask(int it, const ora_mesh* m, double* w)
+{
+    int64_t n = (int64_t)m->ex * m->ey * m->ez * n3(m);
+    int64_t ng = gnx(m) * gny(m) * gnz(m);
+    double* s = (double*)malloc(sizeof(double) * ng);
+    int64_t* first = (int64_t*)malloc(sizeof(int64_t) * ng);
+    int* cnt = (int*)calloc(ng, sizeof(int));
+    for (int64_t L = 0; L < n; ++L) {
+        int64_t g = point_gid(m, L);
+        if (cnt[g] == 0) { s[g] = w[L]; first[g] = L; }
+        else s[g] = P_ADD(s[g], w[L], pm_key(it, ORA_PH_B, first[g], cnt[g]));
+        cnt[g]++;
+    }
+    for (int64_t L = 0; L < n; ++L) {
+        int64_t g = point_gid(m, L);
+        w[L] = point_masked(m, g) ? 0.0 : s[g];
+    }
+    free(s); free(first); free(cnt);
+}
+
+/* glsc3 as one emulated operation: exact sum of the terms (VPREC rounds the
+ * products), then the result through the emulation op */
+static double pm_glsc3(int64_t n, const double* a, const double* b, const double* c, uint64_t key)
+{
+    xsum tot;
+    xsum_init(&tot);
+    for (int64_t L = 0; L < n; ++L) {
+        double ab = a[L] * b[L];
+        if (g_pm_mode == 1) ab = ora_vprec_round(ab, g_pm_t);
+        xsum_add(&tot, ab * c[L]);
+    }
+    return pm_res(xsum_round(&tot), key);
+}
+
+int ora_cgpm(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f, int mode,
+             int t, uint64_t seed, int niter, double* x, double* hist, double* trace)
+{
+    ora_mesh m = {ex, ey, ez, N};
+    int64_t E = (int64_t)ex * ey * ez, n = E * n3(&m);
+    g_pm_mode = mode;
+    g_pm_t = t;
+    g_pm_seed = seed;
+    double* c = make_c(&m);
+    double* r = (double*)malloc(sizeof(double) * n);
+    double* p = (double*)malloc(sizeof(double) * n);
+    double* w = (double*)malloc(sizeof(double) * n);
+    for (int64_t L = 0; L < n; ++L) { x[L] = 0; r[L] = f[L]; p[L] = 0; }
+    double rtr = pm_glsc3(n, r, r, c, pm_key(0, ORA_PH_S, 0, 2));
+    hist[0] = P_SQRT(rtr, pm_key(0, ORA_PH_S, 0, 3));
+    double rtz = rtr, rtz2 = 0.0;
+    int defect = 0, zero = 0;
+    for (int k = 1; k <= niter; ++k) {
+        double rtz1 = rtz, beta = 0.0, alpha = 0.0, pap;
+        if (rtz1 == 0.0) zero = 1;
+        if (!zero && k > 1) beta = P_DIV(rtz1, rtz2, pm_key(k - 1, ORA_PH_S, 0, 4));
+        for (int64_t L = 0; L < n; ++L) p[L] = P_FMA(beta, p[L], r[L], pm_key(k, ORA_PH_A, L, 0));
+        pm_ax_local(k, E, N, D, G, p, w);
+        pm_dssum_mask(k, &m, w);
+        pap = pm_glsc3(n, w, p, c, pm_key(k, ORA_PH_S, 0, 0));
+        if (!zero) alpha = P_DIV(rtz1, pap, pm_key(k, ORA_PH_S, 0, 1));
+        for (int64_t L = 0; L < n; ++L) x[L] = P_FMA(alpha, p[L], x[L], pm_key(k + 1, ORA_PH_A, L, 1));
+        for (int64_t L = 0; L < n; ++L) r[L] = P_FMA(-alpha, w[L], r[L], pm_key(k, ORA_PH_C, L, 0));
+        rtr = pm_glsc3(n, r, r, c, pm_key(k, ORA_PH_S, 0, 2));
+        hist[k] = P_SQRT(rtr, pm_key(k, ORA_PH_S, 0, 3));
+        rtz = rtr;
+        if (!zero && !defect && (!(pap > 0.0) || !isfinite(pap) || !isfinite(rtr))) defect = k;
+        if (trace) {
+            double* tr = trace + 5 * (int64_t)(k - 1);
+            tr[0] = rtz1; tr[1] = beta; tr[2] = alpha; tr[3] = pap; tr[4] = rtr;
+        }
+        rtz2 = rtz1;
+    }
+    free(c); free(r); free(p); free(w);
+    g_pm_mode = 0; g_pm_t = 52; g_pm_seed = 0;
+    return defect;
+}
+
 /* Jacobi PCG (NEXT-1): dinv is data (FP64, e.g. from ora_jacobi_dinv);
  * the FP32 loop uses dinv32 = RN32(dinv) (C11). */
 int ora_pcg64(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,

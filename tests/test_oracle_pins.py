@@ -681,3 +681,41 @@ def test_vprec_cg_t52_is_fp64_and_precision_sweep(ora):
             assert ora.vprec_round(v, t) == v
     assert res[6] > res[16] > res[36] and res[52] < 1e-8
     assert res[23] < 1e-3
+
+
+def test_emulated_loop_vprec_equals_macro_loop(ora):
+    """The explicit-key emulation loop (used for RR / MCA) and the macro-built
+    VPREC loop are separate code: in VPREC mode they must agree bit for bit."""
+    m = ora.Mesh(3, 2, 2, 5, jitter=0.15, seed_geom=6, seed_rhs=7)
+    _, _, D = ora.gll(5)
+    s = ora.setup(m, want=("G", "f"))
+    for t in (5, 12, 23, 52):
+        a = ora.cg_vprec(m, D, s["G"], s["f"], 40, t)
+        b = ora.cg_emulated(m, D, s["G"], s["f"], 40, "vprec", t)
+        np.testing.assert_array_equal(a.hist, b.hist)
+        np.testing.assert_array_equal(a.trace, b.trace)
+        np.testing.assert_array_equal(a.x, b.x)
+
+
+@pytest.mark.parametrize("mode", ["rr", "mca"])
+def test_mca_samples_statistics(ora, mode):
+    """MCA / RR samples: a sample is reproducible from its seed,
+    different seeds differ, the perturbation is at the virtual precision: at
+    t = 23 the early iterations keep ~t significant bits (s2 = -log2|sigma/mu|,
+    P:380), the sample mean tracks the FP64 history, and t = 40 perturbs far
+    less than t = 23."""
+    m = ora.Mesh(2, 2, 2, 6, jitter=0.1, seed_geom=4, seed_rhs=3)
+    _, _, D = ora.gll(6)
+    s = ora.setup(m, want=("G", "f"))
+    a = ora.cg_emulated(m, D, s["G"], s["f"], 30, mode, 23, 11)
+    b = ora.cg_emulated(m, D, s["G"], s["f"], 30, mode, 23, 11)
+    np.testing.assert_array_equal(a.hist, b.hist)
+    hs = np.array([ora.cg_emulated(m, D, s["G"], s["f"], 30, mode, 23, sd).hist for sd in range(8)])
+    assert len({h.tobytes() for h in hs}) == 8
+    r64 = ora.cg(m, D, s["G"], s["f"], 30, "fp64")
+    mu, sg = hs.mean(0), hs.std(0)
+    s2 = -np.log2(sg[1:6] / np.abs(mu[1:6]))
+    assert (s2 > 17).all() and (s2 < 30).all(), s2
+    assert np.abs(mu[:10] / r64.hist[:10] - 1).max() < 1e-5
+    h40 = np.array([ora.cg_emulated(m, D, s["G"], s["f"], 30, mode, 40, sd).hist for sd in range(4)])
+    assert h40.std(0)[1:10].max() < 1e-3 * sg[1:10].max()
