@@ -212,8 +212,21 @@ nbk_status nbk_get_solution(nbk_ctx* ctx, double* x_host);
 /* Device pointer of the last solution in its native precision (do not free). */
 nbk_status nbk_solution_ptr(nbk_ctx* ctx, nbk_precision precision, void** x_dev);
 
-/* Mantissa bits t in [1, 52] of the following NBK_VPREC solves (default 23;
- * t = 52 reproduces the NBK_FP64 solver bit for bit).  Unpreconditioned CG. */
+/* Precision emulation of the following NBK_VPREC solves (SURVEY 8(f) NEXT-4,
+ * P:58-68; unpreconditioned CG, N <= 12, CG-loop scope):
+ *   NBK_EMU_VPREC: every operation's result rounded to t mantissa bits (t = 52
+ *     reproduces the NBK_FP64 solver bit for bit);
+ *   NBK_EMU_RR: Monte Carlo random rounding of every result, inexact(x) =
+ *     x + 2^(e_x - t) xi, xi ~ U[-1/2, 1/2) (Verificarlo "rr" mode);
+ *   NBK_EMU_MCA: inexact() on the operands and on the result ("mca" mode).
+ * xi = SplitMix64(seed, 4 key + slot) with key = (iteration, phase, global
+ * local index, operation number): one seed = one sample, reproducible and
+ * identical to the oracle's.  Each correctly rounded glsc3 counts as one
+ * operation.  nbk_set_vprec(ctx, t) = nbk_set_emulation(ctx, VPREC, t, 0). */
+#define NBK_EMU_VPREC 1
+#define NBK_EMU_RR 2
+#define NBK_EMU_MCA 3
+nbk_status nbk_set_emulation(nbk_ctx* ctx, int32_t mode, int32_t t, uint64_t seed);
 nbk_status nbk_set_vprec(nbk_ctx* ctx, int32_t t);
 
 /* Select the preconditioner of the following solves (default NBK_PRECOND_NONE).

@@ -15,8 +15,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(CSRC, "libnbk.so")
-SOURCES = ["nbk_capi.cu", "nbk_setup.cu"]
-HEADERS = ["nbk_common.cuh", "nbk_kernels.cuh", "nbk_internal.h", "../../include/nbk.h"]
+# (source, object, extra flags): nbk_emu.cu is compiled once per emulation mode
+SOURCES = [("nbk_capi.cu", "nbk_capi", []), ("nbk_setup.cu", "nbk_setup", []),
+           ("nbk_emu.cu", "nbk_emu1", ["-DNBK_EMU_MODE=1"]),
+           ("nbk_emu.cu", "nbk_emu2", ["-DNBK_EMU_MODE=2"]),
+           ("nbk_emu.cu", "nbk_emu3", ["-DNBK_EMU_MODE=3"])]
+HEADERS = ["nbk_common.cuh", "nbk_kernels.cuh", "nbk_launch.cuh", "nbk_internal.h",
+           "../../include/nbk.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NCCL_DIR = None
@@ -35,7 +40,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = SOURCES + HEADERS + [os.path.basename(__file__)]
+    deps = [src for src, _, _ in SOURCES] + HEADERS + [os.path.basename(__file__)]
     for f in deps:
         p = os.path.join(CSRC, f) if not f.endswith(".py") else os.path.join(HERE, f)
         if os.path.exists(p) and os.path.getmtime(p) > t:
@@ -48,19 +53,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs, procs = [], []
     extra = os.environ.get("NBK_EXTRA_FLAGS", "").split()  # tuning experiments only
-    for src in SOURCES:  # the translation units compile in parallel
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, *NCCL_DEF, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
-        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    for src, stem, defs in SOURCES:  # the translation units compile in parallel
+        obj = os.path.join(CSRC, stem + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, *NCCL_DEF, *defs, *extra, "-c", os.path.join(CSRC, src),
+               "-o", obj]
+        procs.append((stem, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
-    for src, pr in procs:
+    for stem, pr in procs:
         out, err = pr.communicate()
         if pr.returncode != 0:
             sys.stderr.write(out + err)
-            raise RuntimeError(f"nvcc failed on {src}")
+            raise RuntimeError(f"nvcc failed on {stem}")
         if verbose:
             sys.stderr.write(err)
-        with open(os.path.join(CSRC, src.replace(".cu", ".ptxas.log")), "w") as fh:
+        with open(os.path.join(CSRC, stem + ".ptxas.log"), "w") as fh:
             fh.write(err)
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]

@@ -15,8 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
-#include "nbk_internal.h"
-#include "nbk_kernels.cuh"
+#include "nbk_launch.cuh"
 
 using namespace nbk;
 
@@ -38,522 +37,39 @@ static nbk_status fail(nbk_ctx* ctx, nbk_status st, const std::string& msg)
     return st;
 }
 
-static int vec_grid(int64_t n)
+namespace nbk {
+cudaError_t enqueue_emulated_1(const Team&, int, nbk_graph*, bool, std::string&);
+cudaError_t enqueue_emulated_2(const Team&, int, nbk_graph*, bool, std::string&);
+cudaError_t enqueue_emulated_3(const Team&, int, nbk_graph*, bool, std::string&);
+cudaError_t emulated_attrs_1(nbk_ctx*);
+cudaError_t emulated_attrs_2(nbk_ctx*);
+cudaError_t emulated_attrs_3(nbk_ctx*);
+
+cudaError_t enqueue_emulated(const Team& t, int niter, nbk_graph* g, bool profiling, std::string& err,
+                             int mode)
 {
-    int64_t g = (n + 255) / 256;
-    if (g < 1) g = 1;
-    return (int)(g > NBK_VEC_GRID_MAX ? NBK_VEC_GRID_MAX : g);
-}
-
-
-// ------------------------------------------------------------ dispatchers
-// Launch with the programmatic-stream-serialization attribute (PDL) when pdl:
-// the kernel may start while its predecessor drains; it calls griddepcontrol.wait
-// before touching the predecessor's results.
-static bool g_pdl_enabled = [] {
-    const char* e = getenv("NBK_PDL");  // opt-in: measured no gain on C2
-    return e && e[0] == '1';
-}();
-
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
-                            cudaStream_t s, bool pdl, Args... args)
-{
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    const bool on = pdl && g_pdl_enabled;
-    cfg.attrs = on ? attr : nullptr;
-    cfg.numAttrs = on ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, args...);
-}
-// attr_only: set the dynamic shared-memory limit (done once at set-up, never
-// under stream capture).
-template <typename T, int N, int FUSED, bool VP = false>
-static cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
-                               bool pdl = false)
-{
-    constexpr int EPB = ax_epb<T>(N);
-    const size_t smem = (size_t)ax_smem_bytes<T>(N);
-    if (attr_only)
-        return cudaFuncSetAttribute(k_ax<T, N, FUSED, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem);
-    const unsigned grid = (unsigned)((a.mesh.E + EPB - 1) / EPB);
-    return launch_k(k_ax<T, N, FUSED, VP>, grid, ax_threads<T>(N), smem, s, pdl, a);
-}
-
-#define NBK_SWITCH_N(N, CALL)                 \
-    switch (N) {                              \
-    case 2: return CALL(2);                   \
-    case 3: return CALL(3);                   \
-    case 4: return CALL(4);                   \
-    case 5: return CALL(5);                   \
-    case 6: return CALL(6);                   \
-    case 7: return CALL(7);                   \
-    case 8: return CALL(8);                   \
-    case 9: return CALL(9);                   \
-    case 10: return CALL(10);                 \
-    case 11: return CALL(11);                 \
-    case 12: return CALL(12);                 \
-    case 13: return CALL(13);                 \
-    case 14: return CALL(14);                 \
-    case 15: return CALL(15);                 \
-    case 16: return CALL(16);                 \
-    default: return cudaErrorInvalidValue;    \
+    switch (mode) {
+    case PM_VPREC: return enqueue_emulated_1(t, niter, g, profiling, err);
+    case PM_RR: return enqueue_emulated_2(t, niter, g, profiling, err);
+    case PM_MCA: return enqueue_emulated_3(t, niter, g, profiling, err);
+    default: return cudaErrorInvalidValue;
     }
-
-template <typename T, int FUSED, bool VP = false>
-static cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
-                             bool pdl = false)
-{
-#define AXN(n) launch_ax_n<T, n, FUSED, VP>(a, s, attr_only, pdl)
-    if constexpr (VP) {  // VPREC emulation kernels: N <= NBK_VPREC_MAXN (compile time)
-        switch (a.mesh.N) {
-        case 2: return AXN(2);
-        case 3: return AXN(3);
-        case 4: return AXN(4);
-        case 5: return AXN(5);
-        case 6: return AXN(6);
-        case 7: return AXN(7);
-        case 8: return AXN(8);
-        case 9: return AXN(9);
-        case 10: return AXN(10);
-        case 11: return AXN(11);
-        case 12: return AXN(12);
-        default: return cudaErrorNotSupported;
-        }
-    } else {
-        NBK_SWITCH_N(a.mesh.N, AXN)
-    }
-#undef AXN
 }
 
-// Resident CTAs of a kernel on the whole device (SM count x occupancy), cached
-// per kernel: grids of the streaming kernels are sized to exactly one wave.
-static int resident_grid(const void* kern, int block, size_t smem)
-{
-    static std::map<const void*, int> cache;
-    auto it = cache.find(kern);
-    if (it != cache.end()) return it->second;
-    int dev = 0, sms = 148, nb = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, block, smem) != cudaSuccess || nb < 1) nb = 1;
-    int g = nb * sms;
-    if (g > NBK_VEC_GRID_MAX) g = NBK_VEC_GRID_MAX;
-    cache[kern] = g;
-    return g;
-}
-
-template <typename T, int V, int MODE, bool VP>
-static cudaError_t launch_vec_v(const VecArgs<T>& a, cudaStream_t s, bool pdl)
-{
-    const int cap = resident_grid((const void*)k_vec<T, V, MODE, VP>, 256, 0);
-    int64_t g = (a.n / 4 + 511) / 512;  // >= 2 chunks of 4 points per thread
-    if (g < 1) g = 1;
-    if (g > cap) g = cap;
-    return launch_k(k_vec<T, V, MODE, VP>, (unsigned)g, 256, 0, s, pdl, a);
-}
-
-// one vector kernel for every N: chunks of 4 points (even N) or 1 (odd N)
-template <typename T, int MODE, bool VP = false>
-static cudaError_t launch_vec(const VecArgs<T>& a, cudaStream_t s, bool pdl = false)
-{
-    if (a.mesh.N < 2 || a.mesh.N > 16) return cudaErrorInvalidValue;
-    return a.mesh.N % 2 == 0 ? launch_vec_v<T, 4, MODE, VP>(a, s, pdl) : launch_vec_v<T, 1, MODE, VP>(a, s, pdl);
-}
-
-template <typename T, bool FUSED, bool VP = false>
-static int dssum_grid_t(int ntiles)
-{
-    const int cap = resident_grid((const void*)k_dssum<T, FUSED, VP>, 256, 0);
-    return ntiles < 1 ? 1 : (ntiles > cap ? cap : ntiles);
-}
-
-template <typename T, bool FUSED, bool VP = false>
-static cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl = false)
-{
-    return launch_k(k_dssum<T, FUSED, VP>, dssum_grid_t<T, FUSED, VP>(a.ntiles), 256, 0, s, pdl, a);
-}
-
-// ------------------------------------------------------------ NCCL (dlopen)
-// NCCL is loaded at run time only when a context has nranks > 1 and a unique
-// id, so that the process uses the one libnccl.so.2 torch has already loaded
-// (dlopen by soname returns the loaded copy) and 1-rank use needs no NCCL.
-struct NcclApi {
-    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
-    decltype(&ncclCommInitRank) commInitRank = nullptr;
-    decltype(&ncclCommDestroy) commDestroy = nullptr;
-    decltype(&ncclGroupStart) groupStart = nullptr;
-    decltype(&ncclGroupEnd) groupEnd = nullptr;
-    decltype(&ncclSend) send = nullptr;
-    decltype(&ncclRecv) recv = nullptr;
-    decltype(&ncclAllGather) allGather = nullptr;
-    decltype(&ncclGetErrorString) errorString = nullptr;
-};
-
-static const NcclApi* nccl_api(std::string& why)
-{
-    static NcclApi api;
-    static int state = 0;  // 0 untried, 1 ok, -1 failed
-    static std::string err;
-    if (state == 0) {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-#ifdef NBK_NCCL_LIB
-        if (!h) h = dlopen(NBK_NCCL_LIB, RTLD_NOW | RTLD_GLOBAL);
-#endif
-        if (!h) {
-            err = std::string("cannot load libnccl.so.2: ") + dlerror();
-            state = -1;
-        } else {
-#define NBK_SYM(f, n) api.f = (decltype(api.f))dlsym(h, n)
-            NBK_SYM(getUniqueId, "ncclGetUniqueId");
-            NBK_SYM(commInitRank, "ncclCommInitRank");
-            NBK_SYM(commDestroy, "ncclCommDestroy");
-            NBK_SYM(groupStart, "ncclGroupStart");
-            NBK_SYM(groupEnd, "ncclGroupEnd");
-            NBK_SYM(send, "ncclSend");
-            NBK_SYM(recv, "ncclRecv");
-            NBK_SYM(allGather, "ncclAllGather");
-            NBK_SYM(errorString, "ncclGetErrorString");
-#undef NBK_SYM
-            const bool ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.groupStart &&
-                            api.groupEnd && api.send && api.recv && api.allGather && api.errorString;
-            state = ok ? 1 : -1;
-            if (!ok) err = "libnccl.so.2 lacks a required symbol";
-        }
-    }
-    if (state < 0) { why = err; return nullptr; }
-    return &api;
-}
-
-// ------------------------------------------------------------ teams
-// The contexts whose work one call enqueues: {self} for a 1-rank or an NCCL
-// rank context, or all P contexts of an in-process virtual-slab group (every
-// slab on this device; faces and partials are shared by pointer aliasing and
-// the phases of all slabs are enqueued in order on the first member's stream).
-struct Team {
-    std::vector<nbk_ctx*> m;
-    bool multi = false;   // nranks > 1: face exchange + rank-ordered reductions
-    cudaStream_t s = nullptr;
-};
-
-static Team team_self(nbk_ctx* c)
-{
-    Team t;
-    t.m.push_back(c);
-    t.multi = c->nranks > 1;
-    t.s = c->stream;
-    return t;
-}
-
-template <typename T>
-static T* fld(nbk_ctx* c, int which, bool fp32)
-{
-    // which: 0 x, 1 r, 2 p, 3 w, 4 dinv
-    void* v64[5] = {c->x64, c->r64, c->p64, c->w64, c->dinv64};
-    void* v32[5] = {c->x32, c->r32, c->p32, c->w32, c->dinv32};
-    return (T*)(fp32 ? v32[which] : v64[which]);
-}
-
-// Exchange the packed face layers with the neighbour ranks (NCCL mode).  In a
-// virtual group the receive buffers alias the neighbours' send buffers.
-template <typename T>
-static cudaError_t xchg_faces(const Team& t, cudaStream_t s, std::string& err)
-{
-    for (nbk_ctx* c : t.m) {
-        if (!c->comm) continue;
-        std::string why;
-        const NcclApi* A = nccl_api(why);
-        if (!A) { err = why; return cudaErrorUnknown; }
-        ncclComm_t comm = (ncclComm_t)c->comm;
-        const ncclDataType_t ty = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-        const size_t cnt = (size_t)c->nlayer;
-        ncclResult_t r = A->groupStart();
-        if (c->has_lo && r == ncclSuccess) r = A->send(c->send_lo, cnt, ty, c->rank - 1, comm, s);
-        if (c->has_lo && r == ncclSuccess) r = A->recv(c->recv_lo, cnt, ty, c->rank - 1, comm, s);
-        if (c->has_hi && r == ncclSuccess) r = A->send(c->send_hi, cnt, ty, c->rank + 1, comm, s);
-        if (c->has_hi && r == ncclSuccess) r = A->recv(c->recv_hi, cnt, ty, c->rank + 1, comm, s);
-        ncclResult_t r2 = A->groupEnd();
-        if (r != ncclSuccess || r2 != ncclSuccess) {
-            err = std::string("NCCL face exchange: ") + A->errorString(r != ncclSuccess ? r : r2);
-            return cudaErrorUnknown;
-        }
-    }
-    return cudaSuccess;
-}
-
-// All-gather of the per-rank dd partials, in place (slot = gather + rank).
-static cudaError_t xchg_gather(const Team& t, cudaStream_t s, std::string& err)
-{
-    for (nbk_ctx* c : t.m) {
-        if (!c->comm) continue;
-        std::string why;
-        const NcclApi* A = nccl_api(why);
-        if (!A) { err = why; return cudaErrorUnknown; }
-        ncclResult_t r = A->allGather(c->gather + 2 * c->rank, c->gather, 4, ncclFloat64,
-                                      (ncclComm_t)c->comm, s);
-        if (r != ncclSuccess) {
-            err = std::string("NCCL allgather: ") + A->errorString(r);
-            return cudaErrorUnknown;
-        }
-    }
-    return cudaSuccess;
-}
-
-// ------------------------------------------------------------ helpers
-template <typename T>
-static AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
-{
-    AxArgs<T> a{};
-    a.D = D;
-    a.G = G;
-    a.mesh = c->view;
-    a.st = c->st;
-    a.parts = c->parts;
-    return a;
-}
-
-template <typename T>
-static int ax_blocks_n(int64_t E, int N)
-{
-#define EPBN(n) (int)((E + ax_epb<T>(n) - 1) / ax_epb<T>(n))
-    NBK_SWITCH_N(N, EPBN)
-#undef EPBN
-}
-
-template <typename T>
-static DssumArgs<T> dssum_args(nbk_ctx* c, T* w)
-{
-    DssumArgs<T> d{};
-    d.w = w;
-    d.g2 = c->g2; d.g4 = c->g4; d.g8 = c->g8;
-    d.toff = c->toff; d.ntiles = (int)c->ntiles;
-    d.st = c->st; d.trace = c->trace; d.mesh = c->view; d.mask = 0; d.fin = 1;
-    return d;
-}
-
-template <typename T>
-static FaceArgs<T> face_args(nbk_ctx* c, T* w)
-{
-    FaceArgs<T> f{};
-    f.w = w;
-    f.send_lo = (T*)c->send_lo; f.send_hi = (T*)c->send_hi;
-    f.recv_lo = (const T*)c->recv_lo; f.recv_hi = (const T*)c->recv_hi;
-    f.has_lo = c->has_lo; f.has_hi = c->has_hi;
-    f.parts = c->parts; f.st = c->st; f.slot = c->gather + 2 * c->rank; f.mesh = c->view;
-    return f;
-}
-
-// vector kernels: two banks of NBK_VEC_GRID_MAX partials (rtr, rtz) at the end
-static dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - 2 * NBK_VEC_GRID_MAX; }
-
-// dssum (+ mask) of w over a team.  fused: shared-node pap terms, alpha.
-// One rank: K_B (its last block forms alpha).  Several: K_B (publish only) and
-// the face pack, exchange, face merge (reduces this rank's pap), all-gather,
-// k_fin (rank-ordered combination, alpha).
-template <typename T, bool FUSED, bool VP = false>
-static cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std::vector<const T*>& p,
-                              int mask, bool pdl, std::string& err, int rev = 0, int single = 0,
-                              int vp_t = 0)
+cudaError_t emulated_attrs(nbk_ctx* c)
 {
     cudaError_t e;
-    const cudaStream_t s = t.s;
-    for (size_t q = 0; q < t.m.size(); ++q) {
-        nbk_ctx* c = t.m[q];
-        DssumArgs<T> d = dssum_args<T>(c, w[q]);
-        d.mask = mask;
-        d.rev = rev;
-        d.single = single;
-        d.vp_t = vp_t;
-        if (FUSED) {
-            d.p = p[q];
-            d.parts = c->parts;
-            d.nA = ax_blocks_n<T>(c->E, c->N);
-            d.fin = t.multi ? 0 : 1;
-        }
-        if ((e = launch_dssum<T, FUSED, VP>(d, s, pdl && !t.multi)) != cudaSuccess) return e;
-        if (t.multi) {
-            FaceArgs<T> f = face_args<T>(c, w[q]);
-            k_face_pack<T><<<vec_grid(2 * c->nlayer), 256, 0, s>>>(f);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-    }
-    if (!t.multi) return cudaSuccess;
-    if ((e = xchg_faces<T>(t, s, err)) != cudaSuccess) return e;
-    for (size_t q = 0; q < t.m.size(); ++q) {
-        nbk_ctx* c = t.m[q];
-        FaceArgs<T> f = face_args<T>(c, w[q]);
-        f.mask = mask;
-        f.single = single;
-        if (FUSED) {
-            f.p = p[q];
-            f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED, VP>((int)c->ntiles);
-        }
-        const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
-        k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    if (FUSED) {
-        if ((e = xchg_gather(t, s, err)) != cudaSuccess) return e;
-        for (nbk_ctx* c : t.m) {
-            k_fin<0><<<1, 32, 0, s>>>(c->gather, c->nranks, c->st, c->hist, c->trace, single, vp_t);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-    }
-    return cudaSuccess;
+    if ((e = emulated_attrs_1(c)) != cudaSuccess) return e;
+    if ((e = emulated_attrs_2(c)) != cudaSuccess) return e;
+    return emulated_attrs_3(c);
 }
-
-// Vector kernel (K_C and the other modes) over a team: one rank finalises in
-// its last block; several publish per-rank partials, all-gather, k_fin.
-template <typename T, int MODE, bool VP = false>
-static cudaError_t vec_team(const Team& t, const std::vector<VecArgs<T>>& args, bool pdl,
-                            std::string& err)
-{
-    cudaError_t e;
-    for (size_t q = 0; q < t.m.size(); ++q) {
-        VecArgs<T> a = args[q];
-        a.slot = t.multi ? t.m[q]->gather + 2 * t.m[q]->rank : nullptr;
-        if ((e = launch_vec<T, MODE, VP>(a, t.s, pdl && !t.multi)) != cudaSuccess) return e;
-    }
-    if (!t.multi) return cudaSuccess;
-    if ((e = xchg_gather(t, t.s, err)) != cudaSuccess) return e;
-    for (size_t q = 0; q < t.m.size(); ++q) {
-        nbk_ctx* c = t.m[q];
-        k_fin<1 + MODE><<<1, 32, 0, t.s>>>(c->gather, c->nranks, c->st, c->hist, c->trace,
-                                          args[q].single, args[q].vp_t);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-}
-
-template <typename T>
-static VecArgs<T> vec_args(nbk_ctx* c)
-{
-    VecArgs<T> v{};
-    v.n = c->n; v.parts = vec_parts(c); v.st = c->st; v.hist = c->hist; v.trace = c->trace;
-    v.mesh = c->view;
-    return v;
-}
-
-// ax (+ dssum + mask) of per-member fields over a team (standalone / final check).
-template <typename T>
-static cudaError_t ax_team(const Team& t, const std::vector<const T*>& u, const std::vector<T*>& w,
-                           int flags, bool fp32, std::string& err)
-{
-    cudaError_t e;
-    for (size_t q = 0; q < t.m.size(); ++q) {
-        nbk_ctx* c = t.m[q];
-        AxArgs<T> a = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
-                           : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
-        a.u = u[q]; a.w = w[q]; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
-        if ((e = launch_ax<T, 0>(a, t.s)) != cudaSuccess) return e;
-    }
-    if (flags & NBK_AX_DSSUM) return dssum_team<T, false>(t, w, {}, 0, false, err);
-    return cudaSuccess;
-}
-
-// Enqueue one CG solve (T1 loop, fixed niter) for the team; used under capture.
-template <typename T, bool VP = false>
-static cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp32, bool profiling,
-                                 std::string& err, int single = 0)
-{
-    const cudaStream_t s = t.s;
-    const size_t P = t.m.size();
-    cudaError_t e;
-    int64_t launches = 0;
-    std::vector<T*> x(P), r(P), p(P), w(P);
-    std::vector<const T*> pc(P);
-    for (size_t q = 0; q < P; ++q) {
-        x[q] = fld<T>(t.m[q], 0, fp32); r[q] = fld<T>(t.m[q], 1, fp32);
-        p[q] = fld<T>(t.m[q], 2, fp32); w[q] = fld<T>(t.m[q], 3, fp32);
-        pc[q] = p[q];
-    }
-    const int64_t per_fin = t.multi ? 1 : 0;  // k_fin launches per reduction and member
-    const int64_t nface = t.multi ? 2 : 0;    // pack + merge per dssum and member
-
-    // Jacobi PCG (NEXT-1): z = r * dinv formed in K_A and K_C, rtz reduced beside rtr
-    const bool jac = !VP && t.m[0]->precond == NBK_PRECOND_JACOBI;
-    const int vp_t = VP ? t.m[0]->vp_t : 0;  // VPREC emulation (NEXT-4)
-    std::vector<VecArgs<T>> vi(P), vr(P);
-    for (size_t q = 0; q < P; ++q) {
-        vi[q] = vec_args<T>(t.m[q]);
-        vi[q].r = r[q]; vi[q].x = x[q]; vi[q].p = p[q]; vi[q].f = t.m[q]->f64;
-        vi[q].dinv = fld<T>(t.m[q], 4, fp32);
-        vi[q].single = single;
-        vi[q].vp_t = vp_t;
-        vr[q] = vi[q];
-        vr[q].w = w[q];
-    }
-    e = jac ? vec_team<T, VEC_INIT_J>(t, vi, false, err) : vec_team<T, VEC_INIT, VP>(t, vi, false, err);
-    if (e != cudaSuccess) return e;
-    launches += (int64_t)P * (1 + per_fin);
-
-    // sweep directions alternate kernel by kernel: K_A f, K_B b, K_C f, K_A b, ...
-    int rev = 0;
-    for (int k = 1; k <= niter; ++k) {
-        const bool prof = g && profiling && P == 1;
-        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1)], s, cudaEventRecordExternal);
-        const bool pdl = !prof;  // events between kernels break PDL edges
-        for (size_t q = 0; q < P; ++q) {
-            nbk_ctx* c = t.m[q];
-            AxArgs<T> aa = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
-                                : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
-            aa.u = nullptr; aa.w = w[q]; aa.p = p[q]; aa.r = r[q]; aa.x = x[q]; aa.mask = 1;
-            aa.rev = rev;
-            aa.dinv = fld<T>(c, 4, fp32);
-            aa.single = single;
-            aa.vp_t = vp_t;
-            e = jac ? launch_ax<T, 2>(aa, s, false, pdl) : launch_ax<T, 1, VP>(aa, s, false, pdl);
-            if (e != cudaSuccess) return e;
-        }
-        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = dssum_team<T, true, VP>(t, w, pc, 0, pdl, err, !rev, single, vp_t)) != cudaSuccess)
-            return e;
-        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 2], s, cudaEventRecordExternal);
-        for (size_t q = 0; q < P; ++q) vr[q].rev = rev;
-        e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pdl, err) : vec_team<T, VEC_RUPD, VP>(t, vr, pdl, err);
-        if (e != cudaSuccess) return e;
-        if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 3], s, cudaEventRecordExternal);
-        rev = !rev;
-        launches += (int64_t)P * (3 + nface + 2 * per_fin);
-    }
-    for (size_t q = 0; q < P; ++q) {
-        nbk_ctx* c = t.m[q];
-        k_tail_x<T, VP><<<vec_grid(c->n), 256, 0, s>>>(x[q], p[q], c->st, c->n, vp_t);
-        ++launches;
-        // final FP64 residual check (C12): x64 = (double)x ; r_true = f - A x64
-        if (fp32) {
-            k_upcast<<<vec_grid(c->n), 256, 0, s>>>(c->x64, (const float*)x[q], c->n);
-            ++launches;
-        }
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    std::vector<const double*> x64(P);
-    std::vector<double*> w64(P);
-    std::vector<VecArgs<double>> vt(P);
-    for (size_t q = 0; q < P; ++q) {
-        nbk_ctx* c = t.m[q];
-        x64[q] = c->x64; w64[q] = c->w64;
-        vt[q] = vec_args<double>(c);
-        vt[q].r = c->r64; vt[q].w = c->w64; vt[q].f = c->f64;
-    }
-    if ((e = ax_team<double>(t, x64, w64, NBK_AX_DSSUM | NBK_AX_MASK, false, err)) != cudaSuccess) return e;
-    if ((e = vec_team<double, VEC_TRUE>(t, vt, false, err)) != cudaSuccess) return e;
-    launches += (int64_t)P * (3 + nface + per_fin);
-    if (g) g->launches = launches;
-    return cudaSuccess;
-}
+}  // namespace nbk
 
 static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_graph** out)
 {
     nbk_ctx* c = t.m[0];
-    auto key = std::make_tuple((int)prec + 4 * (prec == NBK_VPREC ? c->vp_t : 0), niter,
+    // emulated solves: one graph per (mode, t, seed) -- the seed is a kernel argument
+    auto key = std::make_tuple((int)prec + (prec == NBK_VPREC ? 4 * (c->vp_t + 64 * c->pm_mode) : 0), niter,
                                c->profiling * 2 + c->precond);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) { *out = &it->second; return NBK_OK; }
@@ -565,7 +81,7 @@ static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_gr
     NBK_CUDA(c, cudaStreamBeginCapture(t.s, cudaStreamCaptureModeThreadLocal));
     std::string err;
     cudaError_t e = prec == NBK_FP64    ? enqueue_solve<double>(t, niter, &g, false, c->profiling, err)
-                    : prec == NBK_VPREC ? enqueue_solve<double, true>(t, niter, &g, false, c->profiling, err)
+                    : prec == NBK_VPREC ? enqueue_emulated(t, niter, &g, c->profiling, err, c->pm_mode)
                                         : enqueue_solve<float>(t, niter, &g, true, c->profiling, err,
                                                                prec == NBK_FP32S ? 1 : 0);
     cudaGraph_t graph = nullptr;
@@ -602,8 +118,7 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
     cudaError_t e;
 
     if ((e = launch_ax<double, 0>(a64, c->stream, true)) != cudaSuccess) return e;
-    if (c->N <= NBK_VPREC_MAXN && (e = launch_ax<double, 1, true>(a64, c->stream, true)) != cudaSuccess)
-        return e;
+    if (c->N <= NBK_VPREC_MAXN && (e = emulated_attrs(c)) != cudaSuccess) return e;
     if ((e = launch_ax<double, 1>(a64, c->stream, true)) != cudaSuccess) return e;
     if ((e = launch_ax<double, 2>(a64, c->stream, true)) != cudaSuccess) return e;
     if ((e = launch_ax<float, 0>(a32, c->stream, true)) != cudaSuccess) return e;
@@ -707,6 +222,7 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
             return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
         if (prec == NBK_VPREC && m->vp_t != c->vp_t) return fail(c, NBK_EINVAL, "members differ in VPREC t");
         if (prec == NBK_VPREC && m->N > NBK_VPREC_MAXN) return fail(c, NBK_EINVAL, "VPREC emulation supports N <= 12");
+        if (prec == NBK_VPREC && t.multi) return fail(c, NBK_EINVAL, "precision emulation runs on one rank");
     }
     nbk_status st = refresh_h0(t);
     if (st != NBK_OK) return st;
@@ -1055,9 +571,30 @@ nbk_status nbk_glsc3(nbk_ctx* c, const void* a_dev, const void* b_dev, nbk_preci
 
 nbk_status nbk_set_vprec(nbk_ctx* c, int32_t t)
 {
+    return nbk_set_emulation(c, NBK_EMU_VPREC, t, 0);
+}
+
+nbk_status nbk_set_emulation(nbk_ctx* c, int32_t mode, int32_t t, uint64_t seed)
+{
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
-    if (t < 1 || t > 52) return fail(c, NBK_EINVAL, "VPREC mantissa bits must lie in [1, 52]");
+    if (mode != NBK_EMU_VPREC && mode != NBK_EMU_RR && mode != NBK_EMU_MCA)
+        return fail(c, NBK_EINVAL, "bad emulation mode");
+    if (t < 1 || t > 52) return fail(c, NBK_EINVAL, "virtual precision t must lie in [1, 52]");
+    c->pm_mode = mode;
     c->vp_t = t;
+    if (c->pm_seed != seed) {  // the seed is baked into the captured kernel arguments
+        for (auto it = c->graphs.begin(); it != c->graphs.end();) {
+            if (std::get<0>(it->first) % 4 == NBK_VPREC) {
+                if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+                if (it->second.graph) cudaGraphDestroy(it->second.graph);
+                for (auto ev : it->second.prof_events) cudaEventDestroy(ev);
+                it = c->graphs.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    c->pm_seed = seed;
     return NBK_OK;
 }
 

@@ -248,18 +248,90 @@ __device__ __forceinline__ double vprec_round(double x, int t)
     if (low > half || (low == half && ((b >> drop) & 1ull))) b += 1ull << drop;
     return __longlong_as_double((long long)b);
 }
-// VP: round an operation's result (compiled away when VP is false)
-template <bool VP>
-__device__ __forceinline__ double vr(double x, int t)
+// ---------------------------------------------------------- precision tools
+// Emulation modes of the CG-loop operations:
+//   PM_NONE  plain IEEE binary64 / binary32;
+//   PM_VPREC every result rounded to t mantissa bits (VPREC);
+//   PM_RR    Monte Carlo random rounding of the result: inexact(x) = x + 2^(e_x - t) xi,
+//            e_x = floor(log2|x|) + 1, xi ~ U[-1/2, 1/2), then RN64 (MCA "rr" mode);
+//   PM_MCA   inexact() on the operands and on the result (full MCA).
+// The random xi of an operation comes from SplitMix64(seed, 4 key + slot), key =
+// (iteration, phase, global local index, op number) -- the oracle numbers the
+// operations identically, so emulated runs are bitwise comparable.
+enum { PM_NONE = 0, PM_VPREC = 1, PM_RR = 2, PM_MCA = 3 };
+struct PmArgs {
+    int t;                    // virtual precision (mantissa bits)
+    unsigned long long seed;  // RR / MCA sample seed
+};
+__device__ __forceinline__ unsigned long long pm_key(int it, int phase, long long Lg, int o)
 {
-    if constexpr (VP) return vprec_round(x, t); else return x;
+    return (((unsigned long long)it * 8ull + (unsigned long long)phase) * (1ull << 40) +
+            (unsigned long long)Lg) * 128ull + (unsigned long long)o;
 }
-template <bool VP>
-__device__ __forceinline__ float vr(float x, int)
+__device__ __forceinline__ double pm_inexact(double x, const PmArgs& P, unsigned long long key, int slot)
 {
-    static_assert(!VP, "VPREC emulation runs in binary64");
-    return x;
+    if (x == 0.0 || !isfinite(x)) return x;
+    unsigned long long z = P.seed + (4ull * key + (unsigned long long)slot + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const double xi = __dsub_rn(__dmul_rn((double)(z >> 11), 0x1.0p-53), 0.5);
+    int ex;
+    frexp(x, &ex);  // x = m 2^ex, m in [0.5, 1): e_x = floor(log2|x|) + 1 = ex
+    return __dadd_rn(x, scalbn(xi, ex - P.t));
 }
+template <int PM>
+__device__ __forceinline__ double pm_res(double r, const PmArgs& P, unsigned long long key)
+{
+    if constexpr (PM == PM_VPREC) return vprec_round(r, P.t);
+    else if constexpr (PM == PM_RR || PM == PM_MCA) return pm_inexact(r, P, key, 0);
+    else return r;
+}
+template <int PM>
+__device__ __forceinline__ double pm_opnd(double x, const PmArgs& P, unsigned long long key, int slot)
+{
+    if constexpr (PM == PM_MCA) return pm_inexact(x, P, key, slot); else return x;
+}
+template <int PM>
+__device__ __forceinline__ double pfma(double a, double b, double c, const PmArgs& P, unsigned long long key)
+{
+    if constexpr (PM == PM_NONE) return __fma_rn(a, b, c);
+    else return pm_res<PM>(__fma_rn(pm_opnd<PM>(a, P, key, 1), pm_opnd<PM>(b, P, key, 2),
+                                    pm_opnd<PM>(c, P, key, 3)), P, key);
+}
+template <int PM>
+__device__ __forceinline__ double pmul(double a, double b, const PmArgs& P, unsigned long long key)
+{
+    if constexpr (PM == PM_NONE) return __dmul_rn(a, b);
+    else return pm_res<PM>(__dmul_rn(pm_opnd<PM>(a, P, key, 1), pm_opnd<PM>(b, P, key, 2)), P, key);
+}
+template <int PM>
+__device__ __forceinline__ double padd(double a, double b, const PmArgs& P, unsigned long long key)
+{
+    if constexpr (PM == PM_NONE) return __dadd_rn(a, b);
+    else return pm_res<PM>(__dadd_rn(pm_opnd<PM>(a, P, key, 1), pm_opnd<PM>(b, P, key, 2)), P, key);
+}
+// binary32 kernels are never emulated
+template <int PM>
+__device__ __forceinline__ float pfma(float a, float b, float c, const PmArgs&, unsigned long long)
+{
+    static_assert(PM == PM_NONE, "precision emulation runs in binary64");
+    return __fmaf_rn(a, b, c);
+}
+template <int PM>
+__device__ __forceinline__ float pmul(float a, float b, const PmArgs&, unsigned long long)
+{
+    static_assert(PM == PM_NONE, "precision emulation runs in binary64");
+    return __fmul_rn(a, b);
+}
+template <int PM>
+__device__ __forceinline__ float padd(float a, float b, const PmArgs&, unsigned long long)
+{
+    static_assert(PM == PM_NONE, "precision emulation runs in binary64");
+    return __fadd_rn(a, b);
+}
+// key phases
+enum { PH_A = 0, PH_B = 1, PH_C = 2, PH_S = 3 };
 
 // RN32 of the sum represented by a double-double (hi = RN64(hi + lo)): RN32(hi)
 // unless hi lies exactly half-way between two binary32 neighbours, where the
@@ -368,7 +440,7 @@ struct CgState {
     int it;            // current iteration k (1-based)
     int zero;          // rtz1 == 0 reached (rule C9): alpha = beta = 0 from then on
     int defect;        // first iteration with pap <= 0 or a non-finite scalar
-    int vp_t;          // VPREC emulation: mantissa bits of the running solve (0 = off)
+    int pm;            // precision emulation of the running solve (PM_*; 0 = off)
     unsigned int cnt[4];  // last-block counters (reset by the finaliser)
 };
 

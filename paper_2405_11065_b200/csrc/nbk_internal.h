@@ -42,7 +42,9 @@ struct nbk_ctx {
     double* dinv64 = nullptr;             // Jacobi: 1 / assembled diag(A) (masked: 1)
     float* dinv32 = nullptr;              // RN32(dinv64) (C11)
     int precond = NBK_PRECOND_NONE;
-    int vp_t = 23;                        // VPREC emulation: mantissa bits (NBK_VPREC solves)
+    int vp_t = 23;                        // emulation: virtual precision t (NBK_VPREC solves)
+    int pm_mode = 1;                      // NBK_EMU_VPREC / NBK_EMU_RR / NBK_EMU_MCA
+    unsigned long long pm_seed = 0;       // RR / MCA sample
     int dinv_dirty = 1;                   // own diagonal to be (re)assembled
     double *hist = nullptr, *trace = nullptr;
     nbk::dd* parts = nullptr;

@@ -59,12 +59,14 @@ __device__ __forceinline__ void lds_row(T (&dst)[N], const T* src)
 
 // b[kk] = fma(d[kk], t, b[kk]) for kk = 0..N-1 (packed FFMA2 for FP32: per-lane
 // numerics identical to __fmaf_rn, so the canonical order is unchanged).
-template <typename T, int N, bool VP = false>
-__device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t, int vt = 0)
+// PM != PM_NONE: b[q] is the t-chain of the point at key kbase + q kstride.
+template <typename T, int N, int PM = PM_NONE>
+__device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t, const PmArgs* P = nullptr,
+                                        unsigned long long kbase = 0, unsigned long long kstride = 0)
 {
-    if constexpr (VP) {
+    if constexpr (PM != PM_NONE) {
 #pragma unroll
-        for (int q = 0; q < N; ++q) b[q] = vr<VP>(fma_t<T>(d[q], t, b[q]), vt);
+        for (int q = 0; q < N; ++q) b[q] = pfma<PM>(d[q], t, b[q], *P, kbase + q * kstride);
     } else if constexpr (sizeof(T) == 4 && N % 2 == 0) {
         const float2 tt = make_float2(t, t);
 #pragma unroll
@@ -80,11 +82,23 @@ __device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t, int vt 
     }
 }
 
-// glsc3 term with the VPREC rounding of the product (NEXT-4): vp(a b) c
-template <bool VP, typename T>
-__device__ __forceinline__ double dot_term_vp(T a, T b, double c, bool single, int vt)
+// Global node id of local point (e, i, j, k): the emulation key of the pointwise
+// vector updates, so that every copy of a node draws the same perturbation and
+// the fields stay continuous (the fused per-node pap stays exact).
+__device__ __forceinline__ long long node_gid(const MeshView& m, uint32_t e, int i, int j, int k)
 {
-    if constexpr (VP) return __dmul_rn(vr<VP>(mul_t<T>(a, b), vt), c);
+    const ElemCoord ec = elem_coord(m, e);
+    const long long n1 = m.N - 1;
+    const long long Gx = (long long)m.ex * n1 + 1, Gy = (long long)m.ey * n1 + 1;
+    return (ec.ax * n1 + i) + Gx * ((ec.ay * n1 + j) + Gy * (ec.azg * n1 + k));
+}
+
+// glsc3 term: VPREC rounds the product, vp(a b) c (NEXT-4); RR / MCA treat the
+// whole correctly rounded glsc3 as one operation (its result is perturbed).
+template <int PM, typename T>
+__device__ __forceinline__ double dot_term_pm(T a, T b, double c, bool single, const PmArgs& P)
+{
+    if constexpr (PM == PM_VPREC) return __dmul_rn(vprec_round(mul_t<T>(a, b), P.t), c);
     else return dot_term(a, b, c, single);
 }
 
@@ -149,7 +163,8 @@ struct AxArgs {
     const CgState* st; // fused: beta, alpha_prev
     const T* dinv;     // fused Jacobi PCG: z = r * dinv replaces r in the p update
     int single;        // paper-literal single mode: pap terms RN32(w p) (NEXT-2)
-    int vp_t;          // VPREC emulation (NEXT-4): mantissa bits (kernels instantiated with VP)
+    PmArgs pm;         // precision emulation (NEXT-4; kernels instantiated with PM)
+    int it;            // CG iteration (emulation keys)
     dd* parts;         // fused: pap partial per block
     MeshView mesh;
     int mask;          // assign +0 to Dirichlet points of w
@@ -159,11 +174,14 @@ struct AxArgs {
 // ---------------------------------------------------------------- K_A
 // FUSED: 0 = plain ax (u -> w); 1 = CG step (p = beta p + r); 2 = Jacobi PCG
 // step (p = beta p + z, z = RN(r * dinv) formed here: S:376-384, T1 line 2).
-template <typename T, int N, int FUSED, bool VP = false>
+template <typename T, int N, int FUSED, int PM = PM_NONE>
 __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     k_ax(AxArgs<T> a)
 {
-    const int vt = a.vp_t;  // VP: every operation's result rounded to vt bits (NEXT-4)
+    // PM: every operation goes through the emulation (NEXT-4); op numbers per point:
+    // 0 p, 1 x (these two keyed by the global node), 2.. ur, 2+N.. us, 2+2N.. ut,
+    // 2+3N.. metric (9), 11+3N.. r/s transpose (2N), 11+5N.. t transpose (N), 11+6N add
+    const PmArgs& P = a.pm;
     constexpr int N2 = N * N, N3 = N * N * N, EPB = ax_epb<T>(N);
     constexpr bool STAGE = ax_stage_g<T>(N);
     constexpr bool TMA = STAGE && (N % 2 == 0);
@@ -213,6 +231,9 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     }
 
     const int64_t base = e * N3 + ij;
+    const long long goff = (long long)a.mesh.z0 * a.mesh.ex * a.mesh.ey * N3;  // global local index
+    auto key = [&](int kk, int o) { return pm_key(a.it, PH_A, goff + base + (long long)kk * N2, o); };
+    (void)key;
     T betaT = 0, alphaT = 0;
     T rreg[FUSED ? N : 1], xreg[FUSED ? N : 1], dreg[FUSED == 2 ? N : 1];
     if constexpr (FUSED) {
@@ -249,8 +270,10 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 const T po = v;
                 T zk = rreg[k];
                 if constexpr (FUSED == 2) zk = mul_t<T>(rreg[k], dreg[k]);  // solveM (Jacobi)
-                v = vr<VP>(fma_t<T>(betaT, po, zk), vt);
-                a.x[base + k * N2] = vr<VP>(fma_t<T>(alphaT, po, xreg[k]), vt);
+                long long gk = 0;  // emulation: pointwise updates keyed by the global node
+                if constexpr (PM != PM_NONE) gk = node_gid(a.mesh, (uint32_t)e, i, j, k);
+                v = pfma<PM>(betaT, po, zk, P, pm_key(a.it, PH_A, gk, 0));
+                a.x[base + k * N2] = pfma<PM>(alphaT, po, xreg[k], P, pm_key(a.it, PH_A, gk, 1));
                 a.p[base + k * N2] = v;
                 ue[k * N2 + ij] = v;
             }
@@ -285,26 +308,28 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             lds_row<T, N>(Dk, sD + k * N);              // D[k][:] (broadcast)
             T ur = 0, us = 0, ut = 0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) ur = vr<VP>(fma_t<T>(Dri[l], urow[l], ur), vt);
+            for (int l = 0; l < N; ++l) ur = pfma<PM>(Dri[l], urow[l], ur, P, key(k, 2 + l));
 #pragma unroll
-            for (int l = 0; l < N; ++l) us = vr<VP>(fma_t<T>(Drj[l], ue[k * N2 + l * N + i], us), vt);
+            for (int l = 0; l < N; ++l) us = pfma<PM>(Drj[l], ue[k * N2 + l * N + i], us, P, key(k, 2 + N + l));
 #pragma unroll
-            for (int l = 0; l < N; ++l) ut = vr<VP>(fma_t<T>(Dk[l], ureg[l], ut), vt);
+            for (int l = 0; l < N; ++l) ut = pfma<PM>(Dk[l], ureg[l], ut, P, key(k, 2 + 2 * N + l));
             const T g1 = Ge[0 * N3 + k * N2], g2 = Ge[1 * N3 + k * N2], g3 = Ge[2 * N3 + k * N2];
             const T g4 = Ge[3 * N3 + k * N2], g5 = Ge[4 * N3 + k * N2], g6 = Ge[5 * N3 + k * N2];
-            T wr = vr<VP>(mul_t<T>(g1, ur), vt);
-            wr = vr<VP>(fma_t<T>(g2, us, wr), vt);
-            wr = vr<VP>(fma_t<T>(g3, ut, wr), vt);
-            T ws = vr<VP>(mul_t<T>(g2, ur), vt);
-            ws = vr<VP>(fma_t<T>(g4, us, ws), vt);
-            ws = vr<VP>(fma_t<T>(g5, ut, ws), vt);
-            T wt = vr<VP>(mul_t<T>(g3, ur), vt);
-            wt = vr<VP>(fma_t<T>(g5, us, wt), vt);
-            wt = vr<VP>(fma_t<T>(g6, ut, wt), vt);
+            const int om = 2 + 3 * N;
+            T wr = pmul<PM>(g1, ur, P, key(k, om));
+            wr = pfma<PM>(g2, us, wr, P, key(k, om + 1));
+            wr = pfma<PM>(g3, ut, wr, P, key(k, om + 2));
+            T ws = pmul<PM>(g2, ur, P, key(k, om + 3));
+            ws = pfma<PM>(g4, us, ws, P, key(k, om + 4));
+            ws = pfma<PM>(g5, ut, ws, P, key(k, om + 5));
+            T wt = pmul<PM>(g3, ur, P, key(k, om + 6));
+            wt = pfma<PM>(g5, us, wt, P, key(k, om + 7));
+            wt = pfma<PM>(g6, ut, wt, P, key(k, om + 8));
             // own (i,j,k) slot of g1/g2 is dead after the reads above
             wre[k * N2 + ij] = wr;
             wse[k * N2 + ij] = ws;
-            fma_row<T, N, VP>(b, Dk, wt, vt);   // b[kk] = fma(D[k][kk], wt, b[kk])
+            // b[kk] = fma(D[k][kk], wt, b[kk]): op 11+5N+k of point (i, j, kk)
+            fma_row<T, N, PM>(b, Dk, wt, &P, key(0, 11 + 5 * N + k), key(1, 0) - key(0, 0));
         }
     }
     __syncthreads();
@@ -334,10 +359,11 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             lds_row<T, N>(wrow, wre + k * N2 + j * N);  // wr[k][j][:]
             T s = 0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) s = vr<VP>(fma_t<T>(Dci[l], wrow[l], s), vt);
+            for (int l = 0; l < N; ++l) s = pfma<PM>(Dci[l], wrow[l], s, P, key(k, 11 + 3 * N + l));
 #pragma unroll
-            for (int l = 0; l < N; ++l) s = vr<VP>(fma_t<T>(Dcj[l], wse[k * N2 + l * N + i], s), vt);
-            T wv = vr<VP>(add_t<T>(s, b[k]), vt);
+            for (int l = 0; l < N; ++l)
+                s = pfma<PM>(Dcj[l], wse[k * N2 + l * N + i], s, P, key(k, 11 + 4 * N + l));
+            T wv = padd<PM>(s, b[k], P, key(k, 11 + 6 * N));
             const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
             if (a.mask && masked) wv = 0;   // C5: assign +0
             a.w[base + k * N2] = wv;
@@ -345,7 +371,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 // element-interior points (m == 1) contribute w p c here; shared
                 // nodes contribute once per node in K_B (bitwise-equal exact sum).
                 const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
-                if (!sxy && !sz) acc.add(dot_term_vp<VP>(wv, ureg[k], 1.0, a.single, vt));
+                if (!sxy && !sz) acc.add(dot_term_pm<PM>(wv, ureg[k], 1.0, a.single, P));
             }
         }
     }
@@ -360,15 +386,37 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
 // CG scalars from the globally reduced inner products (rules C7, C9); run by
 // one thread: the last block of the reducing kernel (1 rank) or k_fin after
 // the rank-ordered combination of the per-rank partials (several ranks).
+// Scalar operations under an emulation mode (NEXT-4): glsc3 results, division,
+// sqrt -- each one operation (keys: iteration, PH_S, 0, op).
+__device__ __forceinline__ double pm_scalar(int pm, double r, const PmArgs& P, int it, int o)
+{
+    const unsigned long long key = pm_key(it, PH_S, 0, o);
+    if (pm == PM_VPREC) return vprec_round(r, P.t);
+    if (pm == PM_RR || pm == PM_MCA) return pm_inexact(r, P, key, 0);
+    return r;
+}
+__device__ __forceinline__ double pm_opnd_rt(int pm, double x, const PmArgs& P, int it, int o, int slot)
+{
+    return pm == PM_MCA ? pm_inexact(x, P, pm_key(it, PH_S, 0, o), slot) : x;
+}
+__device__ __forceinline__ double pm_div(int pm, double a, double b, const PmArgs& P, int it, int o)
+{
+    return pm_scalar(pm, pm_opnd_rt(pm, a, P, it, o, 1) / pm_opnd_rt(pm, b, P, it, o, 2), P, it, o);
+}
+__device__ __forceinline__ double pm_sqrt(int pm, double a, const PmArgs& P, int it, int o)
+{
+    return pm_scalar(pm, sqrt(pm_opnd_rt(pm, a, P, it, o, 1)), P, it, o);
+}
+
 __device__ __forceinline__ void fin_alpha(CgState* st, dd pap_dd, double* trace, bool single,
-                                          int vp_t = 0)
+                                          int pm = PM_NONE, PmArgs P = PmArgs{52, 0})
 {
     const int k = st->it;
     const double rtz1 = st->rtr;
     double alpha = 0.0, pap;
-    if (vp_t) {  // NEXT-4: the reduction and the division rounded to vp_t bits
-        pap = vprec_round(pap_dd.hi, vp_t);
-        if (!st->zero) alpha = vprec_round(rtz1 / pap, vp_t);
+    if (pm != PM_NONE) {  // NEXT-4: the reduction and the division are emulated operations
+        pap = pm_scalar(pm, pap_dd.hi, P, k, 0);
+        if (!st->zero) alpha = pm_div(pm, rtz1, pap, P, k, 1);
     } else if (single) {  // NEXT-2: binary32 scalars (rtz1 already a binary32 value)
         const float pap32 = dd_to_float_rn(pap_dd.hi, pap_dd.lo);
         pap = pap32;
@@ -401,18 +449,19 @@ __host__ __device__ constexpr bool vec_jacobi(int mode) { return mode == VEC_INI
 // st->rtr holds the current rtz1.
 template <int MODE>
 __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, double* hist, double* trace,
-                                        bool single, int vp_t = 0)
+                                        bool single, int pm = PM_NONE, PmArgs P = PmArgs{52, 0})
 {
-    // single mode (NEXT-2): binary32 sums, sqrt and division; VPREC (NEXT-4): every
-    // result rounded to vp_t bits
+    // single mode (NEXT-2): binary32 sums, sqrt and division; emulation (NEXT-4):
+    // rtr, sqrt and beta are emulated operations (unpreconditioned: rtz = rtr)
+    const int it = (MODE == VEC_INIT || MODE == VEC_INIT_J) ? 0 : st->it;
     double rtr = single ? (double)dd_to_float_rn(rtr_dd.hi, rtr_dd.lo) : rtr_dd.hi;
     double rtz = single ? (double)dd_to_float_rn(rtz_dd.hi, rtz_dd.lo) : rtz_dd.hi;
-    if (vp_t) {
-        rtr = vprec_round(rtr, vp_t);
-        rtz = vprec_round(rtz, vp_t);
+    if (pm != PM_NONE) {
+        rtr = pm_scalar(pm, rtr, P, it, 2);
+        rtz = rtr;
     }
     const double h = single ? (double)__fsqrt_rn((float)rtr)
-                            : (vp_t ? vprec_round(sqrt(rtr), vp_t) : sqrt(rtr));
+                            : (pm != PM_NONE ? pm_sqrt(pm, rtr, P, it, 3) : sqrt(rtr));
     if constexpr (MODE == VEC_INIT || MODE == VEC_INIT_J) {
         st->rtr = rtz;
         st->rtz2 = 0.0;
@@ -438,8 +487,8 @@ __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, doubl
         double beta = 0.0;
         if (!st->zero)
             beta = single ? (double)__fdiv_rn((float)rtz1_next, (float)rtz2_next)
-                          : (vp_t ? vprec_round(rtz1_next / rtz2_next, vp_t)
-                                  : rtz1_next / rtz2_next);  // C7
+                          : (pm != PM_NONE ? pm_div(pm, rtz1_next, rtz2_next, P, k, 4)
+                                           : rtz1_next / rtz2_next);  // C7
         st->beta = beta;
         st->beta32 = (float)beta;
         st->it = k + 1;
@@ -477,7 +526,8 @@ struct DssumArgs {
     int fin;                  // fused: 1 = last block forms alpha (1 rank); 0 = publish only
     int rev;                  // visit the tiles in reverse order
     int single;               // paper-literal single mode (NEXT-2)
-    int vp_t;                 // VPREC emulation (NEXT-4)
+    PmArgs pm;                // precision emulation (NEXT-4)
+    int it;                   // CG iteration (emulation keys)
     MeshView mesh;
 };
 
@@ -519,7 +569,7 @@ __device__ __forceinline__ int tile_seg_load(const int32_t* g2, const int32_t* g
 // The tiles of this block (grid-stride), node by node (all multiplicities of
 // a tile in one loop, two nodes per thread per step, every load of both
 // issued before use; p by the read-only path).
-template <typename T, bool FUSED, bool VP = false>
+template <typename T, bool FUSED, int PM = PM_NONE>
 __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
 {
     for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x) {
@@ -550,23 +600,26 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
                 T sum = v[h][0];                          // C4: ascending local index
 #pragma unroll
                 for (int c = 1; c < 8; ++c)
-                    if (c < m[h]) sum = vr<VP>(add_t<T>(sum, v[h][c]), a.vp_t);
+                    if (c < m[h])  // chain add c of the node (key: its first copy)
+                        sum = padd<PM>(sum, v[h][c], a.pm,
+                                       pm_key(a.it, PH_B, (long long)a.mesh.z0 * a.mesh.ex * a.mesh.ey *
+                                                          a.mesh.N * a.mesh.N * a.mesh.N + ix[h][0], c));
                 if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[h][0])) sum = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) a.w[ix[h][c]] = sum;
-                if constexpr (FUSED) acc.add(dot_term_vp<VP>(sum, p0[h], 1.0, a.single, a.vp_t));  // one term per node
+                if constexpr (FUSED) acc.add(dot_term_pm<PM>(sum, p0[h], 1.0, a.single, a.pm));  // one term per node
             }
         }
     }
 }
 
-template <typename T, bool FUSED, bool VP = false>
+template <typename T, bool FUSED, int PM = PM_NONE>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
     pdl_wait();
-    dssum_tiles<T, FUSED, VP>(a, acc);
+    dssum_tiles<T, FUSED, PM>(a, acc);
     pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
@@ -580,7 +633,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_dssum(DssumArgs
         if (publish_and_check_last(a.parts, a.nA + blockIdx.x, v, &a.st->cnt[0], total)) {
             dd pap_dd = reduce_partials(a.parts, a.nA + (int)gridDim.x);
             if (threadIdx.x == 0) {
-                fin_alpha(a.st, pap_dd, a.trace, a.single, a.vp_t);
+                fin_alpha(a.st, pap_dd, a.trace, a.single, PM, a.pm);
                 a.st->cnt[0] = 0;
             }
         }
@@ -606,7 +659,8 @@ struct VecArgs {
     double* trace;
     dd* slot;           // multi-rank: this rank's reduced partial (NULL: finalise here)
     int single;         // paper-literal single mode: RN32(a b) terms, binary32 scalars
-    int vp_t;           // VPREC emulation (NEXT-4)
+    PmArgs pm;          // precision emulation (NEXT-4)
+    int it;             // CG iteration (emulation keys)
     int rev;            // visit the chunks in reverse order
     MeshView mesh;
 };
@@ -695,7 +749,7 @@ __device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, doub
 // (N^3 % 4 == 0) in one element, 16-byte loads/stores; structural c = 1/m.
 // Per-chunk loads and arithmetic of each mode (split so that the loads of two
 // chunks can be issued before either is used).
-template <typename T, int V, int MODE, bool VP = false>
+template <typename T, int V, int MODE, int PM = PM_NONE>
 struct VecChunk {
     VecT<T, V> A, B, C;
     VecT<double, V> F;
@@ -735,21 +789,31 @@ struct VecChunk {
             z.store(a.x + L);
             z.store(a.p + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
+            for (int t = 0; t < V; ++t) acc.add(dot_term_pm<PM>(r.v[t], r.v[t], c[t], a.single, a.pm));
         } else if constexpr (MODE == VEC_RUPD) {
             VecT<T, V> r;
 #pragma unroll
-            for (int t = 0; t < V; ++t) r.v[t] = vr<VP>(fma_t<T>(am, A.v[t], B.v[t]), a.vp_t);  // C8
+            for (int t = 0; t < V; ++t) {  // C8 (emulation key: the point's global node, phase C)
+                long long g = 0;
+                if constexpr (PM != PM_NONE) {
+                    const int N = a.mesh.N, N3 = N * N * N;
+                    const int64_t Lt = L + t;
+                    const uint32_t e = (uint32_t)(Lt / N3);
+                    const int rem = (int)(Lt - (int64_t)e * N3);
+                    g = node_gid(a.mesh, e, rem % N, (rem / N) % N, rem / (N * N));
+                }
+                r.v[t] = pfma<PM>(am, A.v[t], B.v[t], a.pm, pm_key(a.it, PH_C, g, 0));
+            }
             r.store(a.r + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
+            for (int t = 0; t < V; ++t) acc.add(dot_term_pm<PM>(r.v[t], r.v[t], c[t], a.single, a.pm));
         } else if constexpr (MODE == VEC_TRUE) {
             VecT<T, V> r;
 #pragma unroll
             for (int t = 0; t < V; ++t) r.v[t] = fma_t<T>((T)-1, A.v[t], (T)F.v[t]);  // C12
             r.store(a.r + L);
 #pragma unroll
-            for (int t = 0; t < V; ++t) acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
+            for (int t = 0; t < V; ++t) acc.add(dot_term_pm<PM>(r.v[t], r.v[t], c[t], a.single, a.pm));
         } else if constexpr (MODE == VEC_INIT_J) {
             VecT<T, V> r, z;
 #pragma unroll
@@ -762,7 +826,7 @@ struct VecChunk {
             z.store(a.p + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) {
-                acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
+                acc.add(dot_term_pm<PM>(r.v[t], r.v[t], c[t], a.single, a.pm));
                 acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t], a.single));  // z = r dinv
             }
         } else if constexpr (MODE == VEC_RUPD_J) {
@@ -772,7 +836,7 @@ struct VecChunk {
             r.store(a.r + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) {
-                acc.add(dot_term_vp<VP>(r.v[t], r.v[t], c[t], a.single, a.vp_t));
+                acc.add(dot_term_pm<PM>(r.v[t], r.v[t], c[t], a.single, a.pm));
                 acc2.add(dot_term(r.v[t], mul_t<T>(r.v[t], C.v[t]), c[t], a.single));  // z = r dinv
             }
         } else {
@@ -787,7 +851,7 @@ struct VecChunk {
 // K_A backward, ...): each kernel starts where its predecessor ended, on the
 // data still resident in the 126 MB L2.
 // V = 4 consecutive points per chunk for even N (N^3 % 4 == 0), 1 for odd N.
-template <typename T, int V, int MODE, bool VP = false>
+template <typename T, int V, int MODE, int PM = PM_NONE>
 __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, acc_t& acc2)
 {
     const int64_t nch = a.n / V;
@@ -796,7 +860,7 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, 
     // two chunks of V points per thread per step; every load of both is issued
     // before any use (more bytes in flight per thread)
     for (; q0 + stride < nch; q0 += 2 * stride) {
-        VecChunk<T, V, MODE, VP> C0, C1;
+        VecChunk<T, V, MODE, PM> C0, C1;
         const int64_t c0 = a.rev ? nch - 1 - q0 : q0, c1 = a.rev ? nch - 1 - (q0 + stride) : q0 + stride;
         const int64_t L0 = c0 * V, L1 = c1 * V;
         C0.load(a, L0);
@@ -808,7 +872,7 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, 
         C1.run(a, L1, c, am, acc, acc2);
     }
     if (q0 < nch) {
-        VecChunk<T, V, MODE, VP> C0;
+        VecChunk<T, V, MODE, PM> C0;
         const int64_t L0 = (a.rev ? nch - 1 - q0 : q0) * V;
         C0.load(a, L0);
         double c[V];
@@ -817,7 +881,7 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, 
     }
 }
 
-template <typename T, int V, int MODE, bool VP = false>
+template <typename T, int V, int MODE, int PM = PM_NONE>
 __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 {
     constexpr bool J = vec_jacobi(MODE);
@@ -827,7 +891,7 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
     if constexpr (MODE == VEC_RUPD || MODE == VEC_RUPD_J) {
         if constexpr (sizeof(T) == 8) am = (T)a.st->alpham; else am = (T)a.st->alpham32;
     }
-    vec_loop<T, V, MODE, VP>(a, am, acc, acc2);
+    vec_loop<T, V, MODE, PM>(a, am, acc, acc2);
     pdl_launch_dependents();
     dd v = block_reduce_dd(acc.get());
     dd v2 = J ? block_reduce_dd(acc2.get()) : dd{0.0, 0.0};
@@ -844,7 +908,7 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
                 a.slot[0] = tot;
                 a.slot[1] = tot2;
             } else {
-                fin_rtr<MODE>(a.st, tot, tot2, a.hist, a.trace, a.single, a.vp_t);
+                fin_rtr<MODE>(a.st, tot, tot2, a.hist, a.trace, a.single, PM, a.pm);
             }
             a.st->cnt[1] = 0;
         }
@@ -852,24 +916,34 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 }
 
 // x = fma(alphaT, p, x) after the last iteration (deferred C8 x update).
-template <typename T, bool VP = false>
-__global__ void __launch_bounds__(256) k_tail_x(T* x, const T* p, const CgState* st, int64_t n, int vt)
+// PM: the x update of "iteration niter + 1" (emulation key: op 1 of phase A, global node)
+template <typename T, int PM = PM_NONE>
+__global__ void __launch_bounds__(256) k_tail_x(T* x, const T* p, const CgState* st, int64_t n,
+                                                PmArgs P, int it, MeshView m)
 {
     T al;
     if constexpr (sizeof(T) == 8) al = (T)st->alpha; else al = (T)st->alpha32;
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
-         L += (int64_t)gridDim.x * blockDim.x)
-        x[L] = vr<VP>(fma_t<T>(al, p[L], x[L]), vt);
+         L += (int64_t)gridDim.x * blockDim.x) {
+        long long g = 0;
+        if constexpr (PM != PM_NONE) {
+            const int N = m.N, N3 = N * N * N;
+            const uint32_t e = (uint32_t)(L / N3);
+            const int rem = (int)(L - (int64_t)e * N3);
+            g = node_gid(m, e, rem % N, (rem / N) % N, rem / (N * N));
+        }
+        x[L] = pfma<PM>(al, p[L], x[L], P, pm_key(it, PH_A, g, 1));
+    }
 }
 
 // x64 = (double)x32 (exact, C12) ; G32/D32 = RN32(G64/D64) (C11).
-__global__ void __launch_bounds__(256) k_upcast(double* dst, const float* src, int64_t n)
+static __global__ void __launch_bounds__(256) k_upcast(double* dst, const float* src, int64_t n)
 {
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
          L += (int64_t)gridDim.x * blockDim.x)
         dst[L] = (double)src[L];
 }
-__global__ void __launch_bounds__(256) k_downcast(float* dst, const double* src, int64_t n)
+static __global__ void __launch_bounds__(256) k_downcast(float* dst, const double* src, int64_t n)
 {
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
          L += (int64_t)gridDim.x * blockDim.x)
@@ -1024,7 +1098,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
 // gather holds two dd per rank: [2r] the value, [2r + 1] rtz (Jacobi modes).
 template <int KIND>
 __global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double* trace, int single,
-                      int vp_t)
+                      int pm, PmArgs pa)
 {
     if (threadIdx.x != 0) return;
     dd t{__ldcg(&gather[0].hi), __ldcg(&gather[0].lo)};
@@ -1033,8 +1107,8 @@ __global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double
         t = dd_add(t, dd{__ldcg(&gather[2 * r].hi), __ldcg(&gather[2 * r].lo)});
         t2 = dd_add(t2, dd{__ldcg(&gather[2 * r + 1].hi), __ldcg(&gather[2 * r + 1].lo)});
     }
-    if constexpr (KIND == 0) fin_alpha(st, t, trace, single, vp_t);
-    else fin_rtr<KIND - 1>(st, t, vec_jacobi(KIND - 1) ? t2 : t, hist, trace, single, vp_t);
+    if constexpr (KIND == 0) fin_alpha(st, t, trace, single, pm, pa);
+    else fin_rtr<KIND - 1>(st, t, vec_jacobi(KIND - 1) ? t2 : t, hist, trace, single, pm, pa);
 }
 
 }  // namespace nbk

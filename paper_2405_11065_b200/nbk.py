@@ -25,12 +25,13 @@ AX_LOCAL, AX_DSSUM, AX_MASK = 0, 1, 2
 NBK_FP32S, NBK_VPREC = 2, 3
 PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32, "fp32s": NBK_FP32S, "vprec": NBK_VPREC}
 PRECOND = {"none": 0, "jacobi": 1}
+EMU = {"vprec": 1, "rr": 2, "mca": 3}
 
 # every symbol include/nbk.h declares
 SYMBOLS = ["nbk_workspace_bytes", "nbk_partition", "nbk_nccl_unique_id", "nbk_cg_setup",
            "nbk_load_arrays", "nbk_get_arrays", "nbk_ax_apply", "nbk_dssum", "nbk_glsc3",
            "nbk_cg_solve", "nbk_cg_solve_host", "nbk_get_solution", "nbk_solution_ptr",
-           "nbk_set_vprec", "nbk_set_precond", "nbk_load_precond", "nbk_get_precond", "nbk_set_profiling",
+           "nbk_set_emulation", "nbk_set_vprec", "nbk_set_precond", "nbk_load_precond", "nbk_get_precond", "nbk_set_profiling",
            "nbk_query", "nbk_solve_launches", "nbk_group_link",
            "nbk_group_ax_apply", "nbk_group_dssum", "nbk_group_glsc3", "nbk_group_cg_solve",
            "nbk_last_error", "nbk_version", "nbk_destroy"]
@@ -104,6 +105,7 @@ def load() -> ctypes.CDLL:
         "nbk_set_profiling": [vp, i32],
         "nbk_set_precond": [vp, i32],
         "nbk_set_vprec": [vp, i32],
+        "nbk_set_emulation": [vp, i32, i32, ctypes.c_uint64],
         "nbk_load_precond": [vp, vp],
         "nbk_get_precond": [vp, vp],
         "nbk_query": [vp, P(CInfo)],
@@ -279,6 +281,12 @@ class Context:
         """Mantissa bits of the VPREC-emulated solver (cg_solve(..., 'vprec'))."""
         _check(self.lib.nbk_set_vprec(self._ctx, int(t)), self._ctx)
 
+    def set_emulation(self, mode: str, t: int, seed: int = 0):
+        """Emulation of cg_solve(..., 'vprec'): mode 'vprec', 'rr' or 'mca' at
+        virtual precision t; seed selects the RR / MCA sample."""
+        _check(self.lib.nbk_set_emulation(self._ctx, EMU[mode], int(t), seed & (2**64 - 1)),
+               self._ctx)
+
     def set_precond(self, precond: str):
         """'none' (z = r, the default) or 'jacobi' (z = r / diag(A))."""
         _check(self.lib.nbk_set_precond(self._ctx, PRECOND[precond]), self._ctx)
@@ -404,6 +412,12 @@ class Group:
     def set_vprec(self, t: int):
         """Mantissa bits of the VPREC-emulated solver (cg_solve(..., 'vprec'))."""
         _check(self.lib.nbk_set_vprec(self._ctx, int(t)), self._ctx)
+
+    def set_emulation(self, mode: str, t: int, seed: int = 0):
+        """Emulation of cg_solve(..., 'vprec'): mode 'vprec', 'rr' or 'mca' at
+        virtual precision t; seed selects the RR / MCA sample."""
+        _check(self.lib.nbk_set_emulation(self._ctx, EMU[mode], int(t), seed & (2**64 - 1)),
+               self._ctx)
 
     def set_precond(self, precond: str):
         for c in self.ctxs:

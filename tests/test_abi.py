@@ -54,8 +54,8 @@ def test_kernels_are_sm100a_and_use_no_contraction(lib):
             funcs[cur] = []
         elif cur:
             funcs[cur].append(line)
-    fused64 = "\n".join(funcs["_ZN3nbk4k_axIdLi8ELi1EEEvNS_6AxArgsIT_EE"])
-    fused32 = "\n".join(funcs["_ZN3nbk4k_axIfLi8ELi1EEEvNS_6AxArgsIT_EE"])
+    fused64 = "\n".join(funcs["_ZN3nbk4k_axIdLi8ELi1ELi0EEEvNS_6AxArgsIT_EE"])
+    fused32 = "\n".join(funcs["_ZN3nbk4k_axIfLi8ELi1ELi0EEEvNS_6AxArgsIT_EE"])
     assert "DFMA" in fused64 and "FFMA" in fused32
     # TMA 1-D bulk copies (cp.async.bulk -> UBLKCP) stage G and p in shared memory
     assert "UBLKCP" in fused64 and "UBLKCP" in fused32

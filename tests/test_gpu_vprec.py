@@ -71,3 +71,41 @@ def test_vprec_rejects_large_n(nbk, ora):
     with pytest.raises(nbk.NbkError):
         ctx.set_vprec(60)
     ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["rr", "mca"])
+@pytest.mark.parametrize("args", [(2, 2, 2, 8, 0.0, 0, 1001), (3, 2, 2, 6, 0.15, 4, 5)])
+def test_mca_samples_bitwise(nbk, ora, mode, args):
+    """Monte Carlo random rounding / full MCA samples: the library
+    draws the same xi for the same operation as the oracle (counter-based
+    SplitMix64 over (iteration, phase, global index, operation)), so each
+    sample is bitwise reproducible and equal to the oracle's."""
+    ctx, om, D, s = make(nbk, ora, args)
+    for seed in (1, 2):
+        ctx.set_emulation(mode, 23, seed)
+        hist, trace, res = ctx.cg_solve(40, "vprec")
+        ref = ora.cg_emulated(om, D, s["G"], s["f"], 40, mode, 23, seed)
+        assert bits_equal(hist, ref.hist)
+        assert bits_equal(trace, ref.trace)
+        assert bits_equal(ctx.solution(), ref.x)
+    ctx.close()
+
+
+def test_emulation_vprec_mode_matches_set_vprec(nbk, ora):
+    ctx, om, D, s = make(nbk, ora, (2, 2, 2, 8, 0.0, 0, 1001))
+    ctx.set_vprec(16)
+    a = ctx.cg_solve(30, "vprec")[0]
+    ctx.set_emulation("vprec", 16, 99)
+    b = ctx.cg_solve(30, "vprec")[0]
+    assert bits_equal(a, b)
+    ctx.close()
+
+
+def test_emulation_is_single_rank(nbk, ora):
+    """The slab-face merge is not emulated: emulated solves need one rank."""
+    grp = nbk.Group(nbk.MeshSpec(2, 2, 4, 6), 2, "fp64")
+    for c in grp.ctxs:
+        c.set_emulation("rr", 23, 5)
+    with pytest.raises(nbk.NbkError):
+        grp.cg_solve(5, "vprec")
+    grp.close()
