@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-fp64", action="store_true")
     ap.add_argument("--no-accuracy", dest="accuracy", action="store_false",
                     help="skip the FP32 / paper-literal single accuracy report")
+    ap.add_argument("--no-precision-study", dest="precision_study", action="store_false",
+                    help="skip the VPREC sweep / MCA ensembles (NEXT-4) on C1")
     ap.add_argument("--no-jacobi", dest="jacobi", action="store_false",
                     help="skip the Jacobi-PCG measurement beside the headline")
     ap.add_argument("--others", default="C3,C4,C5",
@@ -249,6 +251,44 @@ def time_solves(ctx, torch, cfg, precision, steps, warmup, flush, profile):
     ms = [a.elapsed_time(b) for a, b in ev]
     time_solves.kBC = kBC
     return ms, kA, graph_ms, res, hist
+
+
+def precision_study(nbk, torch, stream, niter=100, samples=20):
+    """SURVEY 8(f) NEXT-4 on the GPU path (F4-F6), CG-loop scope, on
+    the C1 mesh: VPREC sweep of the virtual precision t (final recursive and
+    true residual), and `samples`-run Monte Carlo ensembles (rr and mca modes)
+    at t = 23: per-iteration mean / min / max of the residual history and the
+    significant bits s2 = -log2|sigma/mu|."""
+    import numpy as np
+    cfg = nbk.CONFIGS["C1"]
+    ctx = nbk.cg_setup(nbk.MeshSpec(**cfg.mesh_args(1)), "fp64", stream=stream)
+    h64, _, r64 = ctx.cg_solve(niter, "fp64", trace=False)
+    out = {"workload": "C1 (2x2x2, N=8), %d iterations, unpreconditioned" % niter,
+           "fp64": {"h_final_rel": float(h64[-1] / h64[0]), "true_res_rel": r64["true_res_rel"]}}
+    t0 = time.perf_counter()
+    sweep = {}
+    for t in (3, 4, 6, 8, 10, 12, 16, 20, 23, 28, 36, 44, 52):
+        ctx.set_emulation("vprec", t, 0)
+        h, _, r = ctx.cg_solve(niter, "vprec", trace=False)
+        sweep[t] = {"h_final_rel": float(h[-1] / h[0]), "true_res_rel": r["true_res_rel"]}
+    out["vprec_sweep"] = sweep
+    for mode in ("rr", "mca"):
+        H = []
+        for sd in range(samples):
+            ctx.set_emulation(mode, 23, 1000 + sd)
+            h, _, _ = ctx.cg_solve(niter, "vprec", trace=False)
+            H.append(h)
+        H = np.array(H)
+        mu, sg = H.mean(0), H.std(0)
+        s2 = -np.log2(np.maximum(sg, 1e-300) / np.abs(mu))
+        ks = [k for k in (1, 10, 25, 50, 75, niter) if k <= niter]
+        out[mode] = {"t": 23, "samples": samples,
+                     "rel_spread_at": {k: float((H[:, k].max() - H[:, k].min()) / abs(mu[k])) for k in ks},
+                     "s2_at": {k: float(s2[k]) for k in ks},
+                     "mean_over_fp64_at": {k: float(mu[k] / h64[k]) for k in ks}}
+    out["seconds"] = time.perf_counter() - t0
+    ctx.close()
+    return out
 
 
 def measure_other(nbk, torch, name, flush, stream, peak, steps=3, warmup=2):
@@ -462,6 +502,10 @@ def run_gpu(args):
              "iteration_GBps": b_fused * n / t_iter / 1e9,
              "iteration_hbm_frac": b_fused * n / t_iter / 1e9 / peak}
 
+    precision = None
+    if world == 1 and args.precision_study:
+        precision = precision_study(nbk, torch, stream)
+
     others = {}
     if world == 1 and args.others:
         ctx.close()
@@ -485,7 +529,7 @@ def run_gpu(args):
             "h_final_rel": float(hist[-1] / hist[0]) if hist[0] else 0.0,
             "median_step_ms": statistics.median(ms), "iteration_model": model,
             "kernels": kernels, **extra,
-            "other_configs": others or None}
+            "other_configs": others or None, "precision_tools": precision}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

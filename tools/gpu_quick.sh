@@ -5,5 +5,5 @@ if [ -n "$3" ]; then timeout 1200 python -m pytest tests -m gpu -x -q -k "$3" > 
 else timeout 1200 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.log 2>&1; fi
 echo "pytest rc=$?" >> $out/pytest_gpu.log
 for c in $cfgs; do
-  timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --others "" > $out/bench_$c.json 2> $out/bench_$c.err
+  timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --others "" --no-precision-study > $out/bench_$c.json 2> $out/bench_$c.err
 done
