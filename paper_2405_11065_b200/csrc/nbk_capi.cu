@@ -56,6 +56,23 @@ cudaError_t enqueue_emulated(const Team& t, int niter, nbk_graph* g, bool profil
     }
 }
 
+cudaError_t enqueue_final_check(const Team& t, std::string& err)
+{
+    const size_t P = t.m.size();
+    std::vector<const double*> x64(P);
+    std::vector<double*> w64(P);
+    std::vector<VecArgs<double>> vt(P);
+    for (size_t q = 0; q < P; ++q) {
+        nbk_ctx* c = t.m[q];
+        x64[q] = c->x64; w64[q] = c->w64;
+        vt[q] = vec_args<double>(c);
+        vt[q].r = c->r64; vt[q].w = c->w64; vt[q].f = c->f64;
+    }
+    cudaError_t e;
+    if ((e = ax_team<double>(t, x64, w64, NBK_AX_DSSUM | NBK_AX_MASK, false, err)) != cudaSuccess) return e;
+    return vec_team<double, VEC_TRUE>(t, vt, false, err);
+}
+
 cudaError_t emulated_attrs(nbk_ctx* c)
 {
     cudaError_t e;

@@ -441,6 +441,10 @@ inline cudaError_t ax_team(const Team& t, const std::vector<const T*>& u, const 
 }
 
 // Enqueue one CG solve (T1 loop, fixed niter) for the team; used under capture.
+// Final FP64 residual check (C12) after the loop: w = A x64 (K_A, dssum, mask),
+// r_true = f - w, glsc3 -- plain binary64 kernels, defined once (nbk_capi.cu).
+cudaError_t enqueue_final_check(const Team& t, std::string& err);
+
 template <typename T, int PM = PM_NONE>
 inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp32, bool profiling,
                                  std::string& err, int single = 0)
@@ -521,17 +525,7 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
         }
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    std::vector<const double*> x64(P);
-    std::vector<double*> w64(P);
-    std::vector<VecArgs<double>> vt(P);
-    for (size_t q = 0; q < P; ++q) {
-        nbk_ctx* c = t.m[q];
-        x64[q] = c->x64; w64[q] = c->w64;
-        vt[q] = vec_args<double>(c);
-        vt[q].r = c->r64; vt[q].w = c->w64; vt[q].f = c->f64;
-    }
-    if ((e = ax_team<double>(t, x64, w64, NBK_AX_DSSUM | NBK_AX_MASK, false, err)) != cudaSuccess) return e;
-    if ((e = vec_team<double, VEC_TRUE>(t, vt, false, err)) != cudaSuccess) return e;
+    if ((e = enqueue_final_check(t, err)) != cudaSuccess) return e;
     launches += (int64_t)P * (3 + nface + per_fin);
     if (g) g->launches = launches;
     return cudaSuccess;
