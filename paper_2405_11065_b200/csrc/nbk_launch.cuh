@@ -31,10 +31,14 @@ inline int vec_grid(int64_t n)
 // Launch with the programmatic-stream-serialization attribute (PDL) when pdl:
 // the kernel may start while its predecessor drains; it calls griddepcontrol.wait
 // before touching the predecessor's results.
-inline bool g_pdl_enabled = [] {
-    const char* e = getenv("NBK_PDL");  // opt-in: measured no gain on C2
-    return e && e[0] == '1';
+// Edges of the CG loop that get PDL: bit 0 K_C -> K_A, bit 1 K_A -> K_B, bit 2 K_B -> K_C.
+// Measured: K_C -> K_A alone +3 % on C2, neutral on C4 (K_A issues its
+// G bulk copy while K_C's last CTA reduces); K_A -> K_B costs up to 12 %.  NBK_PDL overrides.
+inline int g_pdl_mask = [] {
+    const char* e = getenv("NBK_PDL");
+    return e ? atoi(e) : 1;
 }();
+inline bool g_pdl_enabled = true;
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
@@ -497,18 +501,21 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             aa.single = single;
             aa.pm = pm;
             aa.it = k;
-            e = jac ? launch_ax<T, 2>(aa, s, false, pdl) : launch_ax<T, 1, PM>(aa, s, false, pdl);
+            const bool pa = pdl && (g_pdl_mask & 1);
+            e = jac ? launch_ax<T, 2>(aa, s, false, pa) : launch_ax<T, 1, PM>(aa, s, false, pa);
             if (e != cudaSuccess) return e;
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = dssum_team<T, true, PM>(t, w, pc, 0, pdl, err, !rev, single, pm, k)) != cudaSuccess)
+        if ((e = dssum_team<T, true, PM>(t, w, pc, 0, pdl && (g_pdl_mask & 2), err, !rev, single, pm, k)) !=
+            cudaSuccess)
             return e;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 2], s, cudaEventRecordExternal);
         for (size_t q = 0; q < P; ++q) {
             vr[q].rev = rev;
             vr[q].it = k;
         }
-        e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pdl, err) : vec_team<T, VEC_RUPD, PM>(t, vr, pdl, err);
+        const bool pc_ = pdl && (g_pdl_mask & 4);
+        e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pc_, err) : vec_team<T, VEC_RUPD, PM>(t, vr, pc_, err);
         if (e != cudaSuccess) return e;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 3], s, cudaEventRecordExternal);
         rev = !rev;
