@@ -95,7 +95,7 @@ def main():
                     md.append(f"| {label} (`{m}`) | {v} {units[h.index(m)]} |")
             md.append("| top stalls | " + ", ".join(f"{w} {100 * f:.0f}%" for w, f in stalls(h, r)) + " |")
             md.append("")
-            if "k_ax" in name and ", 1>" in name:
+            if "k_ax" in name and (", 1>" in name or ", 1, 0>" in name):
                 def b(m):
                     u = units[h.index(m)]
                     x = float(vals[m].replace(",", ""))
