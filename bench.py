@@ -344,7 +344,7 @@ def run_gpu(args):
 
     # ---- timed region (headline precision; plain graph, PDL edges on) ----
     barrier()
-    with torch.cuda.stream(stream), ClockSampler(local) as clk, Energy(local) as en32:
+    with torch.cuda.stream(stream), ClockSampler(local) as clk:
         ms, _, graph_ms, res, hist = time_solves(ctx, torch, cfg, prec, args.steps, args.warmup,
                                                  flush, profile=False)
         ctx.sync()
@@ -389,10 +389,9 @@ def run_gpu(args):
     if not args.no_fp64 and prec == "fp32":
         barrier()
         with torch.cuda.stream(stream):
-            with Energy(local) as en64:
-                ms64, _, _, res64, _ = time_solves(ctx, torch, cfg, "fp64", args.steps,
-                                                   args.warmup, flush, profile=False)
-                ctx.sync()
+            ms64, _, _, res64, _ = time_solves(ctx, torch, cfg, "fp64", args.steps,
+                                               args.warmup, flush, profile=False)
+            ctx.sync()
             _, kA64, _, _, _ = time_solves(ctx, torch, cfg, "fp64", args.steps, args.warmup,
                                            flush, profile=True)
         barrier()
@@ -403,13 +402,27 @@ def run_gpu(args):
                          "k_ax_hbm_frac": 12 * 8 * n / (ka64 / 1e3) / 1e9 / peak,
                          "true_res_rel": res64["true_res_rel"]}
         extra["speedup_fp32_vs_fp64"] = value / v64
-        if en32.joules and en64.joules:
-            # whole timed region incl. warm-up solves and L2 flushes: per-solve energy
-            # ratio is what it compares (P:682-703 energy-to-solution gain)
-            extra["energy"] = {"fp32_J_per_region": en32.joules, "fp64_J_per_region": en64.joules,
-                               "fp64_over_fp32": en64.joules / en32.joules,
-                               "note": "NVML total energy over warm-up + timed solves of each "
-                                       "solver (same step counts)"}
+        # energy-to-solution: the NVML counter updates coarsely, so each
+        # solver runs back-to-back solves for >= 2 s and the energy per solve is taken
+        en = {}
+        with torch.cuda.stream(stream):
+            for p_ in ("fp32", "fp64"):
+                ctx.cg_solve(cfg.niter, p_, trace=False)
+                ctx.sync()
+                nsol, t0 = 0, time.perf_counter()
+                with Energy(local) as eg:
+                    while time.perf_counter() - t0 < 2.0:
+                        for _ in range(10):
+                            ctx.cg_solve(cfg.niter, p_, trace=False)
+                        nsol += 10
+                    ctx.sync()
+                    dt = time.perf_counter() - t0
+                if eg.joules:
+                    en[p_] = {"J_per_solve": eg.joules / nsol, "solves": nsol, "avg_W": eg.joules / dt}
+        if "fp32" in en and "fp64" in en:
+            extra["energy"] = {**en, "fp64_over_fp32": en["fp64"]["J_per_solve"] / en["fp32"]["J_per_solve"],
+                               "note": "NVML total-energy counter over >= 2 s of back-to-back "
+                                       "solves per solver (incl. the FP64 final check)"}
 
     # ---- accuracy of the single-precision solvers vs FP64 (P:517-522 AE / MAE; NEXT-2) ----
     if args.accuracy and world == 1:
