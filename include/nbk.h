@@ -213,7 +213,8 @@ nbk_status nbk_get_solution(nbk_ctx* ctx, double* x_host);
 nbk_status nbk_solution_ptr(nbk_ctx* ctx, nbk_precision precision, void** x_dev);
 
 /* Precision emulation of the following NBK_VPREC solves (SURVEY 8(f) NEXT-4,
- * P:58-68; unpreconditioned CG, N <= 12, CG-loop scope):
+ * P:58-68; unpreconditioned CG on one rank, CG-loop scope; N <= 12
+ * for VPREC, N <= 8 for RR / MCA):
  *   NBK_EMU_VPREC: every operation's result rounded to t mantissa bits (t = 52
  *     reproduces the NBK_FP64 solver bit for bit);
  *   NBK_EMU_RR: Monte Carlo random rounding of every result, inexact(x) =

@@ -239,6 +239,8 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
             return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
         if (prec == NBK_VPREC && m->vp_t != c->vp_t) return fail(c, NBK_EINVAL, "members differ in VPREC t");
         if (prec == NBK_VPREC && m->N > NBK_VPREC_MAXN) return fail(c, NBK_EINVAL, "VPREC emulation supports N <= 12");
+        if (prec == NBK_VPREC && m->pm_mode != PM_VPREC && m->N > NBK_MC_MAXN)
+            return fail(c, NBK_EINVAL, "RR / MCA emulation supports N <= 8");
         if (prec == NBK_VPREC && t.multi) return fail(c, NBK_EINVAL, "precision emulation runs on one rank");
     }
     nbk_status st = refresh_h0(t);

@@ -14,6 +14,7 @@
 #define NBK_VEC_GRID_MAX (148 * 8)
 #define NBK_MAX_RANKS 64
 #define NBK_VPREC_MAXN 12  // VPREC emulation kernels are built for N <= 12
+#define NBK_MC_MAXN 8      // RR / MCA emulation kernels (per-operation RNG: large code) for N <= 8
 
 struct nbk_graph {
     cudaGraph_t graph = nullptr;

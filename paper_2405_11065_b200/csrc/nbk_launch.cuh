@@ -97,7 +97,7 @@ inline cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only 
                              bool pdl = false)
 {
 #define AXN(n) launch_ax_n<T, n, FUSED, PM>(a, s, attr_only, pdl)
-    if constexpr (PM != PM_NONE) {  // emulation kernels: N <= NBK_VPREC_MAXN (compile time)
+    if constexpr (PM == PM_VPREC) {  // emulation kernels: N <= NBK_VPREC_MAXN (compile time)
         switch (a.mesh.N) {
         case 2: return AXN(2);
         case 3: return AXN(3);
@@ -110,6 +110,17 @@ inline cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only 
         case 10: return AXN(10);
         case 11: return AXN(11);
         case 12: return AXN(12);
+        default: return cudaErrorNotSupported;
+        }
+    } else if constexpr (PM != PM_NONE) {  // Monte Carlo modes: N <= NBK_MC_MAXN
+        switch (a.mesh.N) {
+        case 2: return AXN(2);
+        case 3: return AXN(3);
+        case 4: return AXN(4);
+        case 5: return AXN(5);
+        case 6: return AXN(6);
+        case 7: return AXN(7);
+        case 8: return AXN(8);
         default: return cudaErrorNotSupported;
         }
     } else {

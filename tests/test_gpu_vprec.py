@@ -68,6 +68,13 @@ def test_vprec_rejects_large_n(nbk, ora):
     ctx.set_vprec(23)
     with pytest.raises(nbk.NbkError):
         ctx.cg_solve(5, "vprec")
+    ctx.close()
+    ctx = nbk.cg_setup(nbk.MeshSpec(2, 2, 2, 10), "fp64")
+    ctx.set_emulation("mca", 23, 1)       # Monte Carlo kernels are built for N <= 8
+    with pytest.raises(nbk.NbkError):
+        ctx.cg_solve(5, "vprec")
+    ctx.set_vprec(23)                     # VPREC: N <= 12
+    ctx.cg_solve(5, "vprec")
     with pytest.raises(nbk.NbkError):
         ctx.set_vprec(60)
     ctx.close()
