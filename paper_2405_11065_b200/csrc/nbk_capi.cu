@@ -432,6 +432,12 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
         ncclResult_t r = A->commInitRank(&comm, c->nranks, id, c->rank);
         if (r != ncclSuccess) { delete c; return fail(nullptr, NBK_ENCCL, std::string("ncclCommInitRank: ") + A->errorString(r)); }
         c->comm = comm;
+        if (cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_xchg, cudaEventDisableTiming) != cudaSuccess) {
+            nbk_destroy(c);
+            return fail(nullptr, NBK_ECUDA, "cannot create the face-exchange stream");
+        }
     }
     nbk_status st = NBK_OK;
     cudaError_t e = set_ax_attrs(c);
@@ -832,6 +838,9 @@ void nbk_destroy(nbk_ctx* c)
         const NcclApi* A = nccl_api(why);
         if (A) A->commDestroy((ncclComm_t)c->comm);
     }
+    if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+    if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     // unlink from a virtual group: the others must not alias this workspace
     for (nbk_ctx* o : std::vector<nbk_ctx*>(c->group)) {
         if (o == c) continue;

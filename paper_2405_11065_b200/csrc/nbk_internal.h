@@ -67,6 +67,8 @@ struct nbk_ctx {
     nbk::dd* gather = nullptr;         // P per-rank partials (group-shared in virtual mode)
     nbk::dd* gather_own = nullptr;
     void* comm = nullptr;              // ncclComm_t (NCCL mode)
+    cudaStream_t comm_stream = nullptr;  // face exchange, overlapped with the local dssum
+    cudaEvent_t ev_pack = nullptr, ev_xchg = nullptr;  // fork / join of comm_stream
     std::vector<nbk_ctx*> group;       // virtual slabs: all P contexts of the process
     int h0_dirty = 0;
 

@@ -360,6 +360,24 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
 {
     cudaError_t e;
     const cudaStream_t s = t.s;
+    // Several ranks: pack the slab-boundary face layers first (K_B never
+    // touches plane nodes), so that the NCCL face exchange runs on the
+    // context's comm stream while K_B sums the local shared nodes; the merge
+    // waits for both.  (Virtual slabs: the exchange is pointer aliasing.)
+    if (t.multi) {
+        for (size_t q = 0; q < t.m.size(); ++q) {
+            FaceArgs<T> f = face_args<T>(t.m[q], w[q]);
+            k_face_pack<T><<<vec_grid(2 * t.m[q]->nlayer), 256, 0, s>>>(f);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+        for (nbk_ctx* c : t.m) {
+            if (!c->comm) continue;
+            if ((e = cudaEventRecord(c->ev_pack, s)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0)) != cudaSuccess) return e;
+            if ((e = xchg_faces<T>(team_self(c), c->comm_stream, err)) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(c->ev_xchg, c->comm_stream)) != cudaSuccess) return e;
+        }
+    }
     for (size_t q = 0; q < t.m.size(); ++q) {
         nbk_ctx* c = t.m[q];
         DssumArgs<T> d = dssum_args<T>(c, w[q]);
@@ -375,14 +393,10 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
             d.fin = t.multi ? 0 : 1;
         }
         if ((e = launch_dssum<T, FUSED, PM>(d, s, pdl && !t.multi)) != cudaSuccess) return e;
-        if (t.multi) {
-            FaceArgs<T> f = face_args<T>(c, w[q]);
-            k_face_pack<T><<<vec_grid(2 * c->nlayer), 256, 0, s>>>(f);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
     }
     if (!t.multi) return cudaSuccess;
-    if ((e = xchg_faces<T>(t, s, err)) != cudaSuccess) return e;
+    for (nbk_ctx* c : t.m)
+        if (c->comm && (e = cudaStreamWaitEvent(s, c->ev_xchg, 0)) != cudaSuccess) return e;
     for (size_t q = 0; q < t.m.size(); ++q) {
         nbk_ctx* c = t.m[q];
         FaceArgs<T> f = face_args<T>(c, w[q]);
