@@ -509,6 +509,12 @@ __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, doubl
 // sectors of w a tile touches (its own elements and the neighbours at +1,
 // +ex, +ex*ey) are re-used from L2 instead of being streamed from HBM once
 // per group.
+#ifndef NBK_DSSUM_H
+#define NBK_DSSUM_H 2   // nodes per thread per step
+#endif
+#ifndef NBK_DSSUM_MINB32
+#define NBK_DSSUM_MINB32 4
+#endif
 template <typename T>
 struct DssumArgs {
     T* w;
@@ -578,16 +584,19 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
         const int n2 = __ldg(&a.toff[3 * t + 3]) - s2, n4 = __ldg(&a.toff[3 * t + 4]) - s4;
         const int n8 = __ldg(&a.toff[3 * t + 5]) - s8;
         const int tot = n2 + n4 + n8;
-        for (int q = threadIdx.x; q < tot; q += 2 * blockDim.x) {
-            const int q2 = q + blockDim.x;
-            int32_t ix[2][8];
-            int m[2];
-            m[0] = tile_seg_load(a.g2, a.g4, a.g8, s2, n2, s4, n4, s8, q, ix[0]);
-            m[1] = q2 < tot ? tile_seg_load(a.g2, a.g4, a.g8, s2, n2, s4, n4, s8, q2, ix[1]) : 0;
-            T v[2][8];
-            T p0[2] = {0, 0};
+        for (int q = threadIdx.x; q < tot; q += NBK_DSSUM_H * blockDim.x) {
+            int32_t ix[NBK_DSSUM_H][8];
+            int m[NBK_DSSUM_H];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < NBK_DSSUM_H; ++h) {
+                const int qh = q + h * blockDim.x;
+                m[h] = qh < tot ? tile_seg_load(a.g2, a.g4, a.g8, s2, n2, s4, n4, s8, qh, ix[h]) : 0;
+            }
+            T v[NBK_DSSUM_H][8];
+            T p0[NBK_DSSUM_H];
+#pragma unroll
+            for (int h = 0; h < NBK_DSSUM_H; ++h) {
+                p0[h] = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) v[h][c] = a.w[ix[h][c]];
@@ -595,7 +604,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
                     if (m[h]) p0[h] = __ldg(a.p + ix[h][0]);
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < NBK_DSSUM_H; ++h) {
                 if (!m[h]) continue;
                 T sum = v[h][0];                          // C4: ascending local index
 #pragma unroll
@@ -615,7 +624,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
 }
 
 template <typename T, bool FUSED, int PM = PM_NONE>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 4 : 3) k_dssum(DssumArgs<T> a)
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : 3) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
     pdl_wait();
