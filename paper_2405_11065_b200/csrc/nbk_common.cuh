@@ -383,6 +383,23 @@ __device__ __forceinline__ float add_t<float>(float a, float b)
     return __fadd_rn(a, b);
 }
 
+// ------------------------------------------------------------ K_B tile staging
+// Byte layout of one dssum tile's index rows in shared memory: the g2 rows
+// (8 B each) from the 16-byte boundary at or below the first, rounded up to 16
+// bytes, then the g4 rows (16 B), then the g8 rows (32 B).
+#ifndef NBK_DSSUM_TILE_SMEM
+#define NBK_DSSUM_TILE_SMEM 22528   // per buffer; two buffers per CTA
+#endif
+__host__ __device__ inline int64_t dssum_g2_lead(int64_t s2) { return (8 * s2) & 15; }
+__host__ __device__ inline int64_t dssum_g2_bytes(int64_t s2, int64_t n2)
+{
+    return n2 ? ((8 * (s2 + n2) + 15) & ~(int64_t)15) - ((8 * s2) & ~(int64_t)15) : 0;
+}
+__host__ __device__ inline int64_t dssum_tile_bytes(int64_t s2, int64_t n2, int64_t n4, int64_t n8)
+{
+    return dssum_g2_bytes(s2, n2) + 16 * n4 + 32 * n8;
+}
+
 // ------------------------------------------------------------ TMA / mbarrier
 // 1-D bulk copies global -> shared through the tensor memory accelerator
 // (cp.async.bulk, SASS UBLKCP) completing on an mbarrier (transaction bytes).

@@ -56,6 +56,7 @@ struct nbk_ctx {
     int64_t n2 = 0, n4 = 0, n8 = 0, nother = 0;
     int32_t* toff = nullptr;              // dssum tiles: (ntiles + 1) x 3 offsets
     int64_t ntiles = 0, tile_elems = 1;
+    int64_t tile_smem = 0;                // max index bytes of a tile (K_B smem per buffer)
     unsigned char* scratch = nullptr;  // set-up scratch (aliases the vector region)
     size_t scratch_bytes = 0;
 

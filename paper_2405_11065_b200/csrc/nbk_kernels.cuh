@@ -534,6 +534,8 @@ struct DssumArgs {
     int single;               // paper-literal single mode (NEXT-2)
     PmArgs pm;                // precision emulation (NEXT-4)
     int it;                   // CG iteration (emulation keys)
+    int stage;                // index rows of each tile staged in smem by bulk copies
+    int tile_smem;            // bytes per staging buffer (two buffers)
     MeshView mesh;
 };
 
@@ -575,14 +577,69 @@ __device__ __forceinline__ int tile_seg_load(const int32_t* g2, const int32_t* g
 // The tiles of this block (grid-stride), node by node (all multiplicities of
 // a tile in one loop, two nodes per thread per step, every load of both
 // issued before use; p by the read-only path).
-template <typename T, bool FUSED, int PM = PM_NONE>
-__device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
+// Tile t's segment offsets.
+__device__ __forceinline__ void tile_range(const int32_t* toff, int t, int& s2, int& n2, int& s4, int& n4,
+                                           int& s8, int& n8)
 {
-    for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x) {
+    s2 = __ldg(&toff[3 * t]); s4 = __ldg(&toff[3 * t + 1]); s8 = __ldg(&toff[3 * t + 2]);
+    n2 = __ldg(&toff[3 * t + 3]) - s2; n4 = __ldg(&toff[3 * t + 4]) - s4; n8 = __ldg(&toff[3 * t + 5]) - s8;
+}
+
+// Thread 0: bulk-copy tile t's index rows into buf (layout: dssum_tile_bytes).
+__device__ __forceinline__ void tile_stage(const int32_t* g2, const int32_t* g4, const int32_t* g8,
+                                           const int32_t* toff, int t, unsigned char* buf, uint64_t* bar)
+{
+    int s2, n2, s4, n4, s8, n8;
+    tile_range(toff, t, s2, n2, s4, n4, s8, n8);
+    const uint32_t b2 = (uint32_t)dssum_g2_bytes(s2, n2), b4 = 16u * n4, b8 = 32u * n8;
+    mbar_arrive_expect_tx(bar, b2 + b4 + b8);
+    if (b2) tma_load_1d(buf, reinterpret_cast<const unsigned char*>(g2) + ((8 * (int64_t)s2) & ~(int64_t)15), b2, bar);
+    if (b4) tma_load_1d(buf + b2, g4 + 4 * (int64_t)s4, b4, bar);
+    if (b8) tma_load_1d(buf + b2 + b4, g8 + 8 * (int64_t)s8, b8, bar);
+}
+
+// The tiles of this block (grid-stride), node by node (all multiplicities of
+// a tile in one loop, NBK_DSSUM_H nodes per thread per step, every load of
+// them issued before use; p by the read-only path).  stage: the index rows of
+// the block's next tile are bulk-copied into the other shared-memory buffer
+// while this tile is processed, so the per-step dependent chain is one global
+// latency (w) instead of two (indices, then w).
+template <typename T, bool FUSED, int PM = PM_NONE>
+__device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
+                                            int tile_smem, uint64_t* bars)
+{
+    if (a.stage) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && (int)blockIdx.x < a.ntiles)
+            tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - blockIdx.x : blockIdx.x, sbuf, &bars[0]);
+    }
+    int k = 0;
+    for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x, ++k) {
         const int t = a.rev ? a.ntiles - 1 - i : i;
-        const int s2 = __ldg(&a.toff[3 * t]), s4 = __ldg(&a.toff[3 * t + 1]), s8 = __ldg(&a.toff[3 * t + 2]);
-        const int n2 = __ldg(&a.toff[3 * t + 3]) - s2, n4 = __ldg(&a.toff[3 * t + 4]) - s4;
-        const int n8 = __ldg(&a.toff[3 * t + 5]) - s8;
+        int s2, n2, s4, n4, s8, n8;
+        tile_range(a.toff, t, s2, n2, s4, n4, s8, n8);
+        const int32_t *G2 = a.g2, *G4 = a.g4, *G8 = a.g8;
+        int S2 = s2, S4 = s4, S8 = s8;
+        if (a.stage) {
+            const int b = k & 1;
+            const int inx = i + (int)gridDim.x;
+            if (threadIdx.x == 0 && inx < a.ntiles) {  // the other buffer was released by the last barrier
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - inx : inx,
+                           sbuf + (b ^ 1) * tile_smem, &bars[b ^ 1]);
+            }
+            mbar_wait(&bars[b], (k >> 1) & 1);
+            unsigned char* buf = sbuf + b * tile_smem;
+            const int b2 = (int)dssum_g2_bytes(s2, n2);
+            G2 = reinterpret_cast<const int32_t*>(buf + dssum_g2_lead(s2));
+            G4 = reinterpret_cast<const int32_t*>(buf + b2);
+            G8 = reinterpret_cast<const int32_t*>(buf + b2 + 16 * n4);
+            S2 = S4 = S8 = 0;
+        }
         const int tot = n2 + n4 + n8;
         for (int q = threadIdx.x; q < tot; q += NBK_DSSUM_H * blockDim.x) {
             int32_t ix[NBK_DSSUM_H][8];
@@ -590,7 +647,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
 #pragma unroll
             for (int h = 0; h < NBK_DSSUM_H; ++h) {
                 const int qh = q + h * blockDim.x;
-                m[h] = qh < tot ? tile_seg_load(a.g2, a.g4, a.g8, s2, n2, s4, n4, s8, qh, ix[h]) : 0;
+                m[h] = qh < tot ? tile_seg_load(G2, G4, G8, S2, n2, S4, n4, S8, qh, ix[h]) : 0;
             }
             T v[NBK_DSSUM_H][8];
             T p0[NBK_DSSUM_H];
@@ -620,6 +677,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc)
                 if constexpr (FUSED) acc.add(dot_term_pm<PM>(sum, p0[h], 1.0, a.single, a.pm));  // one term per node
             }
         }
+        if (a.stage) __syncthreads();
     }
 }
 
@@ -627,8 +685,10 @@ template <typename T, bool FUSED, int PM = PM_NONE>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : 3) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
+    extern __shared__ __align__(128) unsigned char dsm_tiles[];
+    __shared__ uint64_t dsm_bars[2];
     pdl_wait();
-    dssum_tiles<T, FUSED, PM>(a, acc);
+    dssum_tiles<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
     pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());

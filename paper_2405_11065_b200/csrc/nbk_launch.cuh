@@ -133,8 +133,8 @@ inline cudaError_t launch_ax(const AxArgs<T>& a, cudaStream_t s, bool attr_only 
 // per kernel: grids of the streaming kernels are sized to exactly one wave.
 inline int resident_grid(const void* kern, int block, size_t smem)
 {
-    static std::map<const void*, int> cache;
-    auto it = cache.find(kern);
+    static std::map<std::pair<const void*, size_t>, int> cache;
+    auto it = cache.find({kern, smem});
     if (it != cache.end()) return it->second;
     int dev = 0, sms = 148, nb = 1;
     cudaGetDevice(&dev);
@@ -142,7 +142,7 @@ inline int resident_grid(const void* kern, int block, size_t smem)
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, block, smem) != cudaSuccess || nb < 1) nb = 1;
     int g = nb * sms;
     if (g > NBK_VEC_GRID_MAX) g = NBK_VEC_GRID_MAX;
-    cache[kern] = g;
+    cache[{kern, smem}] = g;
     return g;
 }
 
@@ -164,17 +164,37 @@ inline cudaError_t launch_vec(const VecArgs<T>& a, cudaStream_t s, bool pdl = fa
     return a.mesh.N % 2 == 0 ? launch_vec_v<T, 4, MODE, PM>(a, s, pdl) : launch_vec_v<T, 1, MODE, PM>(a, s, pdl);
 }
 
-template <typename T, bool FUSED, int PM = PM_NONE>
-inline int dssum_grid_t(int ntiles)
+// K_B index staging: a block's next tile is prefetched while it processes the
+// current one, which only pays when blocks own several tiles (large meshes;
+// measured: C4 +2-4 %, C2 -2 % where every block owns one tile).
+// NBK_DSSUM_STAGE (read at every launch / graph capture): 0 off, 1 auto
+// (default: on when the tiles are >= 4 per block), 2 always (tests).
+inline int dssum_stage_mode()
 {
-    const int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 0);
+    const char* e = getenv("NBK_DSSUM_STAGE");
+    return e ? atoi(e) : 1;
+}
+
+template <typename T, bool FUSED, int PM = PM_NONE>
+inline int dssum_grid_t(int ntiles, int64_t tile_smem, int* stage_out = nullptr)
+{
+    const int mode = dssum_stage_mode();
+    int stage = 0;
+    int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 0);
+    if (mode != 0) {
+        const int cap_s = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 2 * (size_t)tile_smem);
+        if (mode == 2 || ntiles >= 4 * cap_s) { stage = 1; cap = cap_s; }
+    }
+    if (stage_out) *stage_out = stage;
     return ntiles < 1 ? 1 : (ntiles > cap ? cap : ntiles);
 }
 
 template <typename T, bool FUSED, int PM = PM_NONE>
 inline cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
-    return launch_k(k_dssum<T, FUSED, PM>, dssum_grid_t<T, FUSED, PM>(a.ntiles), 256, 0, s, pdl, a);
+    DssumArgs<T> d = a;
+    const int grid = dssum_grid_t<T, FUSED, PM>(a.ntiles, a.tile_smem, &d.stage);
+    return launch_k(k_dssum<T, FUSED, PM>, grid, 256, d.stage ? 2 * (size_t)a.tile_smem : 0, s, pdl, d);
 }
 
 // ------------------------------------------------------------ NCCL (dlopen)
@@ -329,7 +349,7 @@ inline DssumArgs<T> dssum_args(nbk_ctx* c, T* w)
     DssumArgs<T> d{};
     d.w = w;
     d.g2 = c->g2; d.g4 = c->g4; d.g8 = c->g8;
-    d.toff = c->toff; d.ntiles = (int)c->ntiles;
+    d.toff = c->toff; d.ntiles = (int)c->ntiles; d.tile_smem = (int)c->tile_smem;
     d.st = c->st; d.trace = c->trace; d.mesh = c->view; d.mask = 0; d.fin = 1;
     return d;
 }
@@ -404,7 +424,7 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         f.single = single;
         if (FUSED) {
             f.p = p[q];
-            f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED, PM>((int)c->ntiles);
+            f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED, PM>((int)c->ntiles, c->tile_smem);
         }
         const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
         k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);

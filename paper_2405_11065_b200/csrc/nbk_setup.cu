@@ -547,13 +547,29 @@ cudaError_t build_plan(nbk_ctx* ctx)
     if (const char* env = getenv("NBK_DSSUM_TILE_NODES")) tile_nodes = atol(env) > 0 ? atol(env) : tile_nodes;
     int64_t te = (tile_nodes + per_elem - 1) / per_elem;
     if (te < 1) te = 1;
-    ctx->tile_elems = te;
-    ctx->ntiles = (ctx->E + te - 1) / te;
-    k_tile_offsets<<<grid_for(3 * (ctx->ntiles + 1)), 256, 0, s>>>(ctx->g2, ctx->g4, ctx->g8, ctx->n2,
-                                                                 ctx->n4, ctx->n8, ctx->ntiles, te, N3,
-                                                                 ctx->toff);
-    err = cudaStreamSynchronize(s);
-    if (err != cudaSuccess) return err;
+    // K_B stages each tile's index rows in shared memory (double-buffered bulk
+    // copies): halve the tile until its rows fit NBK_DSSUM_TILE_SMEM bytes.
+    std::vector<int32_t> th;
+    for (;;) {
+        ctx->tile_elems = te;
+        ctx->ntiles = (ctx->E + te - 1) / te;
+        k_tile_offsets<<<grid_for(3 * (ctx->ntiles + 1)), 256, 0, s>>>(ctx->g2, ctx->g4, ctx->g8, ctx->n2,
+                                                                     ctx->n4, ctx->n8, ctx->ntiles, te, N3,
+                                                                     ctx->toff);
+        th.resize(3 * (size_t)(ctx->ntiles + 1));
+        err = cudaMemcpyAsync(th.data(), ctx->toff, th.size() * 4, cudaMemcpyDeviceToHost, s);
+        if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+        if (err != cudaSuccess) return err;
+        int64_t mx = 0;
+        for (int64_t t = 0; t < ctx->ntiles; ++t) {
+            const int64_t b = nbk::dssum_tile_bytes(th[3 * t], th[3 * t + 3] - th[3 * t],
+                                                    th[3 * t + 4] - th[3 * t + 1], th[3 * t + 5] - th[3 * t + 2]);
+            mx = b > mx ? b : mx;
+        }
+        ctx->tile_smem = mx;
+        if (mx <= NBK_DSSUM_TILE_SMEM || te == 1) break;
+        te = (te + 1) / 2;
+    }
     return cudaGetLastError();
 }
 
