@@ -169,6 +169,7 @@ struct AxArgs {
     MeshView mesh;
     int mask;          // assign +0 to Dirichlet points of w
     int rev;           // sweep the element tiles in reverse order (L2 reuse, see k_vec)
+    int p_ready;       // fused: p is final before the PDL wait (CG iterations >= 2)
 };
 
 // ---------------------------------------------------------------- K_A
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     constexpr bool TMA = STAGE && (N % 2 == 0);
     __shared__ __align__(16) T sD[N2];
     __shared__ __align__(16) T sDt[N2];
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar[2];   // TMA: p / u block, G block
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* sG = reinterpret_cast<T*>(smem_raw);                  // STAGE: EPB*6*N3
     T* sU = STAGE ? sG + EPB * 6 * N3 : sG;                  // EPB*N3
@@ -206,14 +207,27 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     // depend on the previous kernel: its bulk copy is issued before the PDL
     // wait and overlaps the previous kernel's tail.
     if constexpr (TMA) {
+        // p / u and G on their own barriers: the p update runs while G is in
+        // flight.  p (CG step) is final before this kernel starts from
+        // iteration 2 on (written by the previous K_A, which completed before
+        // K_B and K_C ran), so it is issued first and before the PDL wait when
+        // a.p_ready.
         if (tid == 0) {
-            mbar_init(&bar, 1);
-            const uint32_t gbytes = (uint32_t)(nel * 6 * N3 * sizeof(T));
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
             const uint32_t ubytes = (uint32_t)(nel * N3 * sizeof(T));
-            mbar_arrive_expect_tx(&bar, gbytes + ubytes);
-            tma_load_1d(sG, a.G + e0 * 6 * N3, gbytes, &bar);
+            const uint32_t gbytes = (uint32_t)(nel * 6 * N3 * sizeof(T));
+            if (FUSED && a.p_ready) {
+                mbar_arrive_expect_tx(&bar[0], ubytes);
+                tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
+            }
+            mbar_arrive_expect_tx(&bar[1], gbytes);
+            tma_load_1d(sG, a.G + e0 * 6 * N3, gbytes, &bar[1]);
             pdl_wait();
-            tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar);
+            if (!(FUSED && a.p_ready)) {
+                mbar_arrive_expect_tx(&bar[0], ubytes);
+                tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
+            }
         }
         pdl_wait();
     } else if constexpr (STAGE) {
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
         }
     }
     __syncthreads();  // barrier init, sD, cooperative copies visible
-    if constexpr (TMA) mbar_wait(&bar, 0);
+    if constexpr (TMA) mbar_wait(&bar[0], 0);
 
     T* ue = sU + el * N3;
     T* wre = STAGE ? sG + el * 6 * N3 : sW + el * N3;            // aliases g1 (STAGE)
@@ -299,6 +313,9 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
+            if constexpr (TMA) {
+                if (k == 0) mbar_wait(&bar[1], 0);
+            }
             if constexpr (!DREG) {
                 lds_row<T, N>(Dri, sD + i * N);
                 lds_row<T, N>(Drj, sD + j * N);

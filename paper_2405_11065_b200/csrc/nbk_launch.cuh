@@ -546,6 +546,7 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             aa.single = single;
             aa.pm = pm;
             aa.it = k;
+            aa.p_ready = k >= 2;
             const bool pa = pdl && (g_pdl_mask & 1);
             e = jac ? launch_ax<T, 2>(aa, s, false, pa) : launch_ax<T, 1, PM>(aa, s, false, pa);
             if (e != cudaSuccess) return e;
