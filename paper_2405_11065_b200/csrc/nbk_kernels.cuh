@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     const bool valid = el < nel;
     const T* src_u = FUSED ? a.p : a.u;
 
+    T rreg[FUSED ? N : 1], xreg[FUSED ? N : 1], dreg[FUSED == 2 ? N : 1];
     // ---- stage G and u/p of the CTA's elements in shared memory.  G does not
     // depend on the previous kernel: its bulk copy is issued before the PDL
     // wait and overlaps the previous kernel's tail.
@@ -229,6 +230,15 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
             }
         }
+        if constexpr (FUSED) {  // x and dinv are final too (x: previous K_A)
+            if (valid && a.p_ready) {
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    xreg[k] = a.x[e * N3 + ij + k * N2];
+                    if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + e * N3 + ij + k * N2);
+                }
+            }
+        }
         pdl_wait();
     } else if constexpr (STAGE) {
         pdl_wait();
@@ -249,7 +259,6 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     auto key = [&](int kk, int o) { return pm_key(a.it, PH_A, goff + base + (long long)kk * N2, o); };
     (void)key;
     T betaT = 0, alphaT = 0;
-    T rreg[FUSED ? N : 1], xreg[FUSED ? N : 1], dreg[FUSED == 2 ? N : 1];
     if constexpr (FUSED) {
         if constexpr (sizeof(T) == 8) {
             betaT = (T)a.st->beta;
@@ -259,11 +268,14 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             alphaT = (T)a.st->alpha32;
         }
         if (valid) {  // issued before the TMA wait: overlaps with the bulk copies
+            const bool early = TMA && a.p_ready;
 #pragma unroll
             for (int k = 0; k < N; ++k) {
                 rreg[k] = a.r[base + k * N2];
-                xreg[k] = a.x[base + k * N2];
-                if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + base + k * N2);
+                if (!early) {
+                    xreg[k] = a.x[base + k * N2];
+                    if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + base + k * N2);
+                }
             }
         }
     }

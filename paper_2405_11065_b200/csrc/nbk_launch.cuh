@@ -39,6 +39,11 @@ inline int g_pdl_mask = [] {
     return e ? atoi(e) : 1;
 }();
 inline bool g_pdl_enabled = true;
+// K_A issues p / x loads before the PDL wait from iteration 2 on (NBK_P_EARLY=0: after).
+inline int g_p_early = [] {
+    const char* e = getenv("NBK_P_EARLY");
+    return e ? atoi(e) : 1;
+}();
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
@@ -546,7 +551,7 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             aa.single = single;
             aa.pm = pm;
             aa.it = k;
-            aa.p_ready = k >= 2;
+            aa.p_ready = k >= 2 && g_p_early;
             const bool pa = pdl && (g_pdl_mask & 1);
             e = jac ? launch_ax<T, 2>(aa, s, false, pa) : launch_ax<T, 1, PM>(aa, s, false, pa);
             if (e != cudaSuccess) return e;
