@@ -111,9 +111,10 @@ def test_group_glsc3_equals_one_rank(nbk, ora, dtype):
 
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
-@pytest.mark.parametrize("P", [2, 4])
-@pytest.mark.parametrize("args", [(2, 2, 4, 8, 0.0, 0, 1001), (3, 3, 4, 10, 0.1, 2005, 1005),
-                                  (2, 2, 8, 12, 0.1, 2003, 1003)])
+@pytest.mark.parametrize("P,args", [(P, a) for P in (2, 4) for a in
+                                    [(2, 2, 4, 8, 0.0, 0, 1001), (3, 3, 4, 10, 0.1, 2005, 1005),
+                                     (2, 2, 8, 12, 0.1, 2003, 1003)]]
+                         + [(8, (2, 2, 8, 12, 0.1, 2003, 1003)), (8, (2, 3, 8, 8, 0.0, 0, 1004))])
 def test_group_cg_bitwise_vs_oracle(nbk, ora, precision, P, args):
     grp, om, D, s = make_group(nbk, ora, args, P)
     niter = 60
@@ -162,3 +163,32 @@ def test_group_misuse_is_rejected(nbk, ora):
     with pytest.raises(nbk.NbkError):
         nbk.cg_setup(nbk.MeshSpec(2, 2, 3, 4), "fp64", rank=0, nranks=2)  # ez % P != 0
     grp.close()
+
+
+@pytest.mark.parametrize("cfg,P", [("C4", 2), ("C4", 4), ("C5", 2)])
+def test_full_size_virtual_slabs_equal_one_rank(nbk, cfg, P):
+    """BASELINE's multi-GPU configurations at full size on one GPU: the global
+    problem of C4 at P GPUs (weak: 64x64x32P) and of C5 (strong: 64^3, N = 10)
+    solved by one rank and by P virtual slabs, each slab with its own set-up --
+    residual history, trace, true residual and solution bit for bit equal."""
+    import hashlib
+    c = nbk.CONFIGS[cfg]
+    spec = nbk.MeshSpec(**c.mesh_args(P))
+    niter = 20
+    one = nbk.cg_setup(spec, "fp32")
+    ref = {}
+    for prec in ("fp32", "fp64"):
+        h, t, r = one.cg_solve(niter, prec)
+        ref[prec] = (h, t, r["true_res"], hashlib.sha256(one.solution().tobytes()).hexdigest())
+    one.close()
+    del one
+    torch.cuda.empty_cache()
+    grp = nbk.Group(spec, P, "fp32")
+    for prec in ("fp32", "fp64"):
+        h, t, r = grp.cg_solve(niter, prec)
+        h1, t1, tr1, x1 = ref[prec]
+        assert bits_equal(h, h1) and bits_equal(t, t1)
+        assert r["true_res"] == tr1
+        assert hashlib.sha256(grp.solution().tobytes()).hexdigest() == x1
+    grp.close()
+    torch.cuda.empty_cache()
