@@ -375,6 +375,8 @@ def run_gpu(args):
                "K_B_alg_GBps": n * (phi0 * (2 * s_b + 4) + psi0 * (s_b + 4)) / (kb_ms / 1e3) / 1e9,
                "K_C_alg_GBps": 3 * s_b * n / (kc_ms / 1e3) / 1e9,
                "timing": "CUDA events between the kernels of every iteration (profiling replay)"}
+    kernels["K_B_frac"] = kernels["K_B_alg_GBps"] / peak
+    kernels["K_C_frac"] = kernels["K_C_alg_GBps"] / peak
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config, prec),
                 "kernel": "k_ax<fused> (p,x update + ax_e + mask + interior pap)",
@@ -510,8 +512,11 @@ def run_gpu(args):
     s_b = 4 if prec == "fp32" else 8
     b_fused = 15 * s_b + phi * (2 * s_b + 4) + psi * (s_b + 4)
     t_iter = tot_ms / args.steps / cfg.niter / 1e3
+    b_fused64 = 15 * 8 + phi * (2 * 8 + 4) + psi * (8 + 4)
     model = {"B_fused_bytes_per_local_point": b_fused,
              "bytes_per_global_dof": b_fused * n / ng,
+             "bytes_per_global_dof_fp64_solver": b_fused64 * n / ng,
+             "bytes_per_dof_ratio_fp32_over_fp64": b_fused / b_fused64 if prec == "fp32" else 1.0,
              "iteration_GBps": b_fused * n / t_iter / 1e9,
              "iteration_hbm_frac": b_fused * n / t_iter / 1e9 / peak}
 
