@@ -45,6 +45,8 @@ def parse():
                     help="skip the FP32 / paper-literal single accuracy report")
     ap.add_argument("--no-precision-study", dest="precision_study", action="store_false",
                     help="skip the VPREC sweep / MCA ensembles (NEXT-4) on C1")
+    ap.add_argument("--convergence", type=int, default=4000,
+                    help="iterations of the long convergence / true-residual-floor study (0: skip)")
     ap.add_argument("--no-jacobi", dest="jacobi", action="store_false",
                     help="skip the Jacobi-PCG measurement beside the headline")
     ap.add_argument("--others", default="C3,C4,C5",
@@ -450,6 +452,29 @@ def run_gpu(args):
         acc["fp32s_value"] = ng * cfg.niter * args.steps / (sum(ms1) / 1e3) / 1e9
         acc["note"] = ("fp32: north_star mixed solver (FP64 inner-product accumulation); fp32s: "
                        "paper-literal single (binary32 inner products and scalars, R11b)")
+        # convergence beyond the fixed 100 iterations (NEXT-2: true-residual floor and
+        # iterations to 1e-10): recursive h_k/h_0 of one long solve, true residual (FP64
+        # check of the returned x) after several lengths
+        if args.convergence:
+            conv = {"niter_max": args.convergence}
+            with torch.cuda.stream(stream):
+                for p_ in ("fp64", "fp32", "fp32s"):
+                    hh, _, rr = ctx.cg_solve(args.convergence, p_, trace=False)
+                    rel = hh / hh[0] if hh[0] else hh
+                    it_to = {}
+                    for thr in (1e-4, 1e-6, 1e-8, 1e-10, 1e-12):
+                        idx = np.nonzero(rel <= thr)[0]
+                        it_to[f"{thr:.0e}"] = int(idx[0]) if len(idx) else None
+                    tr_at = {}
+                    for nit in sorted({n_ for n_ in (250, 500, 1000, 2000) if n_ < args.convergence}):
+                        _, _, r2 = ctx.cg_solve(nit, p_, trace=False)
+                        tr_at[str(nit)] = r2["true_res_rel"]
+                    tr_at[str(args.convergence)] = rr["true_res_rel"]
+                    conv[p_] = {"iters_to_recursive_rel": it_to,
+                                "recursive_rel_final": float(rel[-1]),
+                                "true_res_rel_after": tr_at,
+                                "defect_iter": rr["defect_iter"]}
+            acc["convergence"] = conv
         extra["accuracy"] = acc
         del np
 

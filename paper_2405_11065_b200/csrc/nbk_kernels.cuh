@@ -568,6 +568,24 @@ struct DssumArgs {
     MeshView mesh;
 };
 
+// pap terms of a shared node with m copies (rule C6: one term RN(RN(w p) c) per
+// copy, c = 1/m, all copies equal after dssum).  FP32 vectors: w p is exact in
+// binary64 (RN32(w p) in single mode), so the m terms sum exactly to the one
+// term with c = 1.  FP64: RN(w p)/m rounds when it is subnormal, so the m equal
+// terms are accumulated (each exact in the double-double accumulator).
+template <typename T>
+__device__ __forceinline__ void add_node_pap(acc_t& acc, T w, T p, int m, int single)
+{
+    if constexpr (sizeof(T) == 8) {
+        const double t = dot_term(w, p, 1.0 / (double)m);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if (c < m) acc.add(t);
+    } else {
+        acc.add(dot_term(w, p, 1.0, single != 0));
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ bool masked_local(const MeshView& m, int32_t L)
 {
@@ -703,7 +721,10 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) a.w[ix[h][c]] = sum;
-                if constexpr (FUSED) acc.add(dot_term_pm<PM>(sum, p0[h], 1.0, a.single, a.pm));  // one term per node
+                if constexpr (FUSED) {
+                    if constexpr (PM == PM_NONE) add_node_pap<T>(acc, sum, p0[h], m[h], a.single);
+                    else acc.add(dot_term_pm<PM>(sum, p0[h], 1.0, a.single, a.pm));  // one term per node
+                }
             }
         }
         if (a.stage) __syncthreads();
@@ -1176,7 +1197,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
                 a.w[L] = sum;
             }
         if constexpr (FUSED)
-            if (upper) acc.add(dot_term(sum, p0, 1.0, a.single));  // one term per node (lower rank)
+            if (upper) add_node_pap<T>(acc, sum, p0, 2 * nx * ny, a.single);  // lower rank counts the node
     }
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());

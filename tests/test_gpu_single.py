@@ -110,3 +110,27 @@ def test_accuracy_report_shapes(nbk, ora):
     assert ae32.mean() < 1e-2 * h64[0] and ae1.mean() < 1e-2 * h64[0]
     assert 0 < r32["true_res_rel"] < 1e-3 and 0 < r1["true_res_rel"] < 1e-3
     ctx.close()
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp32s"])
+@pytest.mark.parametrize("args", [(2, 2, 2, 8, 0.0, 0, 1001), (3, 2, 2, 5, 0.2, 4, 5)])
+def test_long_runs_past_convergence_bitwise(nbk, ora, precision, args):
+    """1500 iterations: far past convergence, where the recursive residual of the
+    single-precision solvers runs into binary32 denormals / underflow (the bench's
+    convergence study sees the paper-literal solver break down there) -- the
+    GPU path must still follow the oracle bit for bit, defect flag included."""
+    ctx, om, D, s = make(nbk, ora, args)
+    niter = 1500
+    hist, trace, res = ctx.cg_solve(niter, precision)
+    ref = ora.cg(om, D, s["G"], s["f"], niter, precision)
+
+    def same(a, b):  # bitwise, except that any NaN matches any NaN (payloads differ)
+        a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+        na, nb = np.isnan(a), np.isnan(b)
+        return np.array_equal(na, nb) and bits_equal(np.where(na, 0.0, a), np.where(nb, 0.0, b))
+
+    assert res["defect_iter"] == ref.defect
+    assert same(hist, ref.hist)
+    assert same(trace, ref.trace)
+    assert same(ctx.solution(), ref.x.astype(np.float64))
+    ctx.close()
