@@ -573,16 +573,16 @@ struct DssumArgs {
 // binary64 (RN32(w p) in single mode), so the m terms sum exactly to the one
 // term with c = 1.  FP64: RN(w p)/m rounds when it is subnormal, so the m equal
 // terms are accumulated (each exact in the double-double accumulator).
-template <typename T>
-__device__ __forceinline__ void add_node_pap(acc_t& acc, T w, T p, int m, int single)
+template <typename T, int PM = PM_NONE>
+__device__ __forceinline__ void add_node_pap(acc_t& acc, T w, T p, int m, int single, const PmArgs& P)
 {
     if constexpr (sizeof(T) == 8) {
-        const double t = dot_term(w, p, 1.0 / (double)m);
+        const double t = dot_term_pm<PM>(w, p, 1.0 / (double)m, single != 0, P);
 #pragma unroll
         for (int c = 0; c < 8; ++c)
             if (c < m) acc.add(t);
     } else {
-        acc.add(dot_term(w, p, 1.0, single != 0));
+        acc.add(dot_term_pm<PM>(w, p, 1.0, single != 0, P));
     }
 }
 
@@ -721,10 +721,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) a.w[ix[h][c]] = sum;
-                if constexpr (FUSED) {
-                    if constexpr (PM == PM_NONE) add_node_pap<T>(acc, sum, p0[h], m[h], a.single);
-                    else acc.add(dot_term_pm<PM>(sum, p0[h], 1.0, a.single, a.pm));  // one term per node
-                }
+                if constexpr (FUSED) add_node_pap<T, PM>(acc, sum, p0[h], m[h], a.single, a.pm);
             }
         }
         if (a.stage) __syncthreads();
@@ -1197,7 +1194,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
                 a.w[L] = sum;
             }
         if constexpr (FUSED)
-            if (upper) add_node_pap<T>(acc, sum, p0, 2 * nx * ny, a.single);  // lower rank counts the node
+            if (upper) add_node_pap<T>(acc, sum, p0, 2 * nx * ny, a.single, PmArgs{52, 0});  // lower rank counts the node
     }
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());

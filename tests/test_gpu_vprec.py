@@ -116,3 +116,29 @@ def test_emulation_is_single_rank(nbk, ora):
     with pytest.raises(nbk.NbkError):
         grp.cg_solve(5, "vprec")
     grp.close()
+
+
+def _same(a, b):  # bitwise, any NaN matching any NaN
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    na, nb = np.isnan(a), np.isnan(b)
+    return np.array_equal(na, nb) and bits_equal(np.where(na, 0.0, a), np.where(nb, 0.0, b))
+
+
+@pytest.mark.parametrize("mode,t", [("vprec", 52), ("vprec", 30), ("vprec", 10), ("mca", 23),
+                                    ("rr", 23)])
+def test_emulation_long_runs_past_convergence(nbk, ora, mode, t):
+    """1200 iterations on C1, far past convergence (products and the per-copy
+    glsc3 terms RN(t(a b))/m subnormal): the emulated GPU solve still follows the
+    oracle bit for bit."""
+    args = (2, 2, 2, 8, 0.0, 0, 1001)
+    ctx, om, D, s = make(nbk, ora, args)
+    ctx.set_emulation(mode, t, 7)
+    niter = 1200
+    hist, trace, res = ctx.cg_solve(niter, "vprec")
+    if mode == "vprec":
+        ref = ora.cg_vprec(om, D, s["G"], s["f"], niter, t)
+    else:
+        ref = ora.cg_emulated(om, D, s["G"], s["f"], niter, mode, t, 7)
+    assert res["defect_iter"] == ref.defect
+    assert _same(hist, ref.hist) and _same(trace, ref.trace) and _same(ctx.solution(), ref.x)
+    ctx.close()
