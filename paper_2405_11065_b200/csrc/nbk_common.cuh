@@ -37,8 +37,12 @@ __device__ __forceinline__ void fast_two_sum(double a, double b, double& s, doub
     e = __dsub_rn(b, __dsub_rn(s, a));
 }
 
+// Non-finite operands: the plain IEEE sum (inf + finite = inf, inf - inf =
+// NaN), as the exact sum with special values is defined (TwoSum would turn
+// the error terms into NaN).
 __device__ __forceinline__ dd dd_add(dd a, dd b)
 {
+    if (!isfinite(a.hi) || !isfinite(b.hi)) return dd{__dadd_rn(a.hi, b.hi), 0.0};
     double s, e, t, f;
     two_sum(a.hi, b.hi, s, e);
     two_sum(a.lo, b.lo, t, f);
@@ -61,6 +65,7 @@ struct acc_t {
     }
     __device__ __forceinline__ dd get() const
     {
+        if (!isfinite(s)) return dd{s, 0.0};  // an infinite / NaN term (S is the plain IEEE sum)
         double h, l;
         two_sum(s, c, h, l);
         return dd{h, l};

@@ -134,3 +134,64 @@ def test_long_runs_past_convergence_bitwise(nbk, ora, precision, args):
     assert same(trace, ref.trace)
     assert same(ctx.solution(), ref.x.astype(np.float64))
     ctx.close()
+
+
+def _same(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    na, nb = np.isnan(a), np.isnan(b)
+    return np.array_equal(na, nb) and bits_equal(np.where(na, 0.0, a), np.where(nb, 0.0, b))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp32s"])
+def test_long_jacobi_runs_past_convergence_bitwise(nbk, ora, precision):
+    """Jacobi PCG for 1200 iterations (z = RN(r dinv) and the rtz terms reach the
+    subnormal range) -- bit for bit with the oracle."""
+    ctx, om, D, s = make(nbk, ora, (3, 2, 2, 5, 0.2, 4, 5))
+    _, dinv = ora.jacobi_dinv(om, D, s["G"])
+    ctx.load_precond(dinv)
+    ctx.set_precond("jacobi")
+    hist, trace, res = ctx.cg_solve(1200, precision)
+    ref = ora.cg(om, D, s["G"], s["f"], 1200, precision, dinv=dinv)
+    assert res["defect_iter"] == ref.defect
+    assert _same(hist, ref.hist) and _same(trace, ref.trace)
+    assert _same(ctx.solution(), ref.x.astype(np.float64))
+    ctx.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_long_virtual_slab_runs_past_convergence_bitwise(nbk, ora, P):
+    """The face merge's pap terms for slab-plane nodes in the subnormal regime."""
+    args = (2, 2, 4, 8, 0.0, 0, 1001)
+    spec = nbk.MeshSpec(*args)
+    grp = nbk.Group(spec, P, "fp32")
+    om = ora.Mesh(*args)
+    _, _, D = ora.gll(8)
+    s = ora.setup(om, want=("G", "f"))
+    El = om.E // P
+    grp.load_arrays(D, [s["G"][r * El:(r + 1) * El] for r in range(P)],
+                    [s["f"][r * El:(r + 1) * El] for r in range(P)])
+    for prec in ("fp64", "fp32"):
+        hist, trace, res = grp.cg_solve(1200, prec)
+        ref = ora.cg(om, D, s["G"], s["f"], 1200, prec)
+        assert res["defect_iter"] == ref.defect
+        assert _same(hist, ref.hist) and _same(trace, ref.trace)
+        assert _same(grp.solution(), ref.x.astype(np.float64))
+    grp.close()
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp32s"])
+@pytest.mark.parametrize("scale_exp", [600, -600, 120])
+def test_extreme_rhs_scaling_bitwise(nbk, ora, precision, scale_exp):
+    """f scaled by 2^600 / 2^-600 / 2^120 (exact): overflow of the inner
+    products to inf (defect flag), subnormal / underflowing data from the start,
+    and FP32 overflow of the RN32(f) rounding -- the library and the oracle take
+    the same path, defect iteration included."""
+    ctx, om, D, s = make(nbk, ora, (2, 2, 2, 6, 0.0, 0, 9))
+    f = s["f"] * (2.0 ** scale_exp)
+    ctx.load_arrays(D, s["G"], f)
+    hist, trace, res = ctx.cg_solve(60, precision)
+    ref = ora.cg(om, D, s["G"], f, 60, precision)
+    assert res["defect_iter"] == ref.defect
+    assert _same(hist, ref.hist) and _same(trace, ref.trace)
+    assert _same(ctx.solution(), ref.x.astype(np.float64))
+    ctx.close()
