@@ -69,3 +69,25 @@ def test_workspace_size_query_without_gpu_is_rejected_cleanly(lib):
         pytest.skip("GPU present")
     with pytest.raises(nbk.NbkError):
         nbk.Context(nbk.MeshSpec(2, 2, 2, 4), "fp64")
+
+
+@pytest.mark.parametrize("args,msg", [((128, 128, 128, 12), "int32"), ((1, 1, 1, 17), "N must"),
+                                      ((1, 1, 1, 1), "N must"), ((0, 2, 2, 4), ""),
+                                      ((2, -1, 2, 4), "")])
+def test_mesh_limits_are_validated_on_the_host(lib, args, msg):
+    """Maximum / degenerate sizes: more than 2^31 local points (int32 dssum
+    plan), N outside [2, 16], empty or negative boxes -- rejected with a status,
+    before any device work."""
+    from paper_2405_11065_b200 import nbk
+    with pytest.raises(nbk.NbkError, match=msg):
+        nbk.workspace_bytes(nbk.MeshSpec(*args), "fp32")
+
+
+def test_largest_single_gpu_workspaces_fit_hbm(lib):
+    """Workspace of the largest BASELINE configurations at one GPU (C5: 64^3,
+    N = 10; C4 global at P = 8 as one rank) against 180 GB of HBM."""
+    from paper_2405_11065_b200 import CONFIGS, nbk
+    c5 = nbk.workspace_bytes(nbk.MeshSpec(**CONFIGS["C5"].mesh_args(1)), "fp32")
+    assert c5 < 60e9
+    c4p8 = nbk.workspace_bytes(nbk.MeshSpec(**CONFIGS["C4"].mesh_args(8)), "fp32")
+    assert c4p8 < 180e9
