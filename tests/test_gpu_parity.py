@@ -281,3 +281,32 @@ def test_c3_cg_first_iterations_bitwise(nbk, ora):
     c = nbk.CONFIGS["C3"]
     args = (c.ex, c.ey, c.ez, c.N, c.jitter, c.seed_geom, c.seed_rhs)
     _cg_parity(nbk, ora, args, 5, "fp32")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_glsc3_special_values(nbk, ora, dtype):
+    """glsc3 with +-inf / NaN / huge / subnormal entries: the plain IEEE result
+    the exact-sum definition gives (inf, NaN for inf - inf), and correctly
+    rounded sums of subnormal terms (R25)."""
+    ctx, om, D, s = make(nbk, ora, 2, 2, 2, 4)
+    c = ora.multiplicity_weight(om)
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    big = np.finfo(dtype).max
+    tiny = np.finfo(dtype).smallest_subnormal
+    base = inputs.uniform_field((om.E, 4, 4, 4), 3, dtype)
+    cases = []
+    a = base.copy(); a.flat[5] = np.inf; cases.append((a, base))                 # +inf
+    a = base.copy(); a.flat[5] = np.inf; a.flat[9] = -np.inf; cases.append((a, np.abs(base) + 1))  # inf - inf
+    a = base.copy(); a.flat[7] = np.nan; cases.append((a, base))                 # NaN
+    a = np.full_like(base, big); cases.append((a, np.full_like(base, 2.0)))      # overflow of products
+    a = np.full_like(base, tiny); cases.append((a, np.full_like(base, 0.75)))    # subnormal terms
+    a = base * np.asarray(2.0 ** -500 if dtype == np.float64 else 2.0 ** -60, dtype)
+    cases.append((a, a))                                                          # squares underflow
+    for a, b in cases:
+        got = ctx.glsc3(dev(a, tdt), dev(b, tdt))
+        ref = ora.glsc3(a, b, c)
+        if np.isnan(ref):
+            assert np.isnan(got)
+        else:
+            assert got == ref, (got, ref)
+    ctx.close()
