@@ -42,15 +42,16 @@ __device__ __forceinline__ void fast_two_sum(double a, double b, double& s, doub
 // the error terms into NaN).
 __device__ __forceinline__ dd dd_add(dd a, dd b)
 {
-    if (!isfinite(a.hi) || !isfinite(b.hi)) return dd{__dadd_rn(a.hi, b.hi), 0.0};
     double s, e, t, f;
     two_sum(a.hi, b.hi, s, e);
+    const double plain = s;   // selects below, no branch: this sits in serial reductions
     two_sum(a.lo, b.lo, t, f);
     e = __dadd_rn(e, t);
     fast_two_sum(s, e, s, e);
     e = __dadd_rn(e, f);
     fast_two_sum(s, e, s, e);
-    return dd{s, e};
+    const bool fin = isfinite(plain);
+    return dd{fin ? s : plain, fin ? e : 0.0};
 }
 
 // Per-thread accumulator: running sum S plus the exact TwoSum errors in C.

@@ -578,9 +578,13 @@ __device__ __forceinline__ void add_node_pap(acc_t& acc, T w, T p, int m, int si
 {
     if constexpr (sizeof(T) == 8) {
         const double t = dot_term_pm<PM>(w, p, 1.0 / (double)m, single != 0, P);
+        // t normal: RN(w p)/m was exact, the m terms sum exactly to m t -- one add
+        const bool one = fabs(t) >= 2.2250738585072014e-308;
+        const double v = one ? t * (double)m : t;
+        const int cnt = one ? 1 : m;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-            if (c < m) acc.add(t);
+            if (c < cnt) acc.add(v);
     } else {
         acc.add(dot_term_pm<PM>(w, p, 1.0, single != 0, P));
     }
@@ -738,16 +742,25 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : 3) k_
     dssum_tiles<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
     pdl_launch_dependents();
     if constexpr (FUSED) {
-        dd v = block_reduce_dd(acc.get());
+        // K_A's nA pap partials are folded in here, a fixed slice per block, so
+        // that the serial last-block reduction sees gridDim partials, not nA + gridDim
+        dd ka{0.0, 0.0};
+        {
+            const int lo = (int)((long long)a.nA * blockIdx.x / gridDim.x);
+            const int hi = (int)((long long)a.nA * (blockIdx.x + 1) / gridDim.x);
+            for (int q = lo + (int)threadIdx.x; q < hi; q += blockDim.x)
+                ka = dd_add(ka, dd{__ldcg(&a.parts[q].hi), __ldcg(&a.parts[q].lo)});
+        }
+        dd v = block_reduce_dd(dd_add(acc.get(), ka));
         if (!a.fin) {
             // multi-rank: the face-merge kernel adds the slab-face terms and
-            // reduces every partial (K_A, K_B, merge) of this rank
+            // reduces the K_B and merge partials of this rank
             if (threadIdx.x == 0) a.parts[a.nA + blockIdx.x] = v;
             return;
         }
         const unsigned int total = gridDim.x;
         if (publish_and_check_last(a.parts, a.nA + blockIdx.x, v, &a.st->cnt[0], total)) {
-            dd pap_dd = reduce_partials(a.parts, a.nA + (int)gridDim.x);
+            dd pap_dd = reduce_partials(a.parts + a.nA, (int)gridDim.x);
             if (threadIdx.x == 0) {
                 fin_alpha(a.st, pap_dd, a.trace, a.single, PM, a.pm);
                 a.st->cnt[0] = 0;
@@ -1102,6 +1115,7 @@ struct FaceArgs {
     int mask;              // standalone: assign +0 to Dirichlet plane nodes (C5)
     dd* parts;             // fused: partials [0, nprev) of K_A and K_B, then this kernel's
     int nprev;
+    int nskip;             // K_A's partials (already folded into K_B's)
     CgState* st;
     dd* slot;              // fused: this rank's reduced pap partial
     int single;            // paper-literal single mode (NEXT-2)
@@ -1199,7 +1213,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
         if (publish_and_check_last(a.parts, a.nprev + blockIdx.x, v, &a.st->cnt[2], gridDim.x)) {
-            dd tot = reduce_partials(a.parts, a.nprev + (int)gridDim.x);
+            dd tot = reduce_partials(a.parts + a.nskip, a.nprev - a.nskip + (int)gridDim.x);
             if (threadIdx.x == 0) {
                 a.slot->hi = tot.hi;
                 a.slot->lo = tot.lo;

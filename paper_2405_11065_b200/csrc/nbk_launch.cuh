@@ -430,6 +430,7 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         if (FUSED) {
             f.p = p[q];
             f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED, PM>((int)c->ntiles, c->tile_smem);
+            f.nskip = ax_blocks_n<T>(c->E, c->N);
         }
         const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
         k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);
