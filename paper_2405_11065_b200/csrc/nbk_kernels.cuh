@@ -980,27 +980,34 @@ struct VecChunk {
 // K_A backward, ...): each kernel starts where its predecessor ended, on the
 // data still resident in the 126 MB L2.
 // V = 4 consecutive points per chunk for even N (N^3 % 4 == 0), 1 for odd N.
+#ifndef NBK_VEC_U
+#define NBK_VEC_U 2
+#endif
 template <typename T, int V, int MODE, int PM = PM_NONE>
 __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, acc_t& acc2)
 {
     const int64_t nch = a.n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // two chunks of V points per thread per step; every load of both is issued
-    // before any use (more bytes in flight per thread)
-    for (; q0 + stride < nch; q0 += 2 * stride) {
-        VecChunk<T, V, MODE, PM> C0, C1;
-        const int64_t c0 = a.rev ? nch - 1 - q0 : q0, c1 = a.rev ? nch - 1 - (q0 + stride) : q0 + stride;
-        const int64_t L0 = c0 * V, L1 = c1 * V;
-        C0.load(a, L0);
-        C1.load(a, L1);
-        double c[V];
-        chunk_weights<V>(a.mesh, L0, c);
-        C0.run(a, L0, c, am, acc, acc2);
-        chunk_weights<V>(a.mesh, L1, c);
-        C1.run(a, L1, c, am, acc, acc2);
+    // NBK_VEC_U chunks of V points per thread per step; every load of them is
+    // issued before any use (more bytes in flight per thread)
+    for (; q0 + (NBK_VEC_U - 1) * stride < nch; q0 += NBK_VEC_U * stride) {
+        VecChunk<T, V, MODE, PM> C[NBK_VEC_U];
+        int64_t L[NBK_VEC_U];
+#pragma unroll
+        for (int u = 0; u < NBK_VEC_U; ++u) {
+            const int64_t qu = q0 + u * stride;
+            L[u] = (a.rev ? nch - 1 - qu : qu) * V;
+            C[u].load(a, L[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < NBK_VEC_U; ++u) {
+            double c[V];
+            chunk_weights<V>(a.mesh, L[u], c);
+            C[u].run(a, L[u], c, am, acc, acc2);
+        }
     }
-    if (q0 < nch) {
+    for (; q0 < nch; q0 += stride) {  // tail: fewer than NBK_VEC_U chunks left
         VecChunk<T, V, MODE, PM> C0;
         const int64_t L0 = (a.rev ? nch - 1 - q0 : q0) * V;
         C0.load(a, L0);
