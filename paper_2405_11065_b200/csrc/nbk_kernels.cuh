@@ -577,14 +577,15 @@ template <typename T, int PM = PM_NONE>
 __device__ __forceinline__ void add_node_pap(acc_t& acc, T w, T p, int m, int single, const PmArgs& P)
 {
     if constexpr (sizeof(T) == 8) {
-        const double t = dot_term_pm<PM>(w, p, 1.0 / (double)m, single != 0, P);
+        const double cm = m == 2 ? 0.5 : (m == 4 ? 0.25 : 0.125);  // 1/m, m in {2, 4, 8}
+        const double t = dot_term_pm<PM>(w, p, cm, single != 0, P);
         // t normal: RN(w p)/m was exact, the m terms sum exactly to m t -- one add
         const bool one = fabs(t) >= 2.2250738585072014e-308;
-        const double v = one ? t * (double)m : t;
-        const int cnt = one ? 1 : m;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-            if (c < cnt) acc.add(v);
+        acc.add(one ? t * (double)m : t);
+        if (!one) {  // rare (subnormal t): the other m - 1 copies' terms
+#pragma unroll 1
+            for (int c = 1; c < m; ++c) acc.add(t);
+        }
     } else {
         acc.add(dot_term_pm<PM>(w, p, 1.0, single != 0, P));
     }
