@@ -541,6 +541,9 @@ __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, doubl
 #ifndef NBK_DSSUM_H
 #define NBK_DSSUM_H 2   // nodes per thread per step
 #endif
+#ifndef NBK_DSSUM_MINB64
+#define NBK_DSSUM_MINB64 2   // FP64: no spills at 2 CTAs per SM (+1.5 % FP64 C2 vs 3)
+#endif
 #ifndef NBK_DSSUM_MINB32
 #define NBK_DSSUM_MINB32 4
 #endif
@@ -734,7 +737,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
 }
 
 template <typename T, bool FUSED, int PM = PM_NONE>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : 3) k_dssum(DssumArgs<T> a)
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_DSSUM_MINB64) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
     extern __shared__ __align__(128) unsigned char dsm_tiles[];
