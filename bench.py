@@ -5,10 +5,15 @@
 
 A "step" is one complete fixed-iteration CG solve (all SURVEY 8(a) rows a1-a8:
 the fused p/x update + ax_e + mask, dssum, glsc3 reductions, r update, device
-scalars, and the final FP64 residual check) of BASELINE.json's configs[1]
-workload (C2: 16^3 hex elements, N = 8, 100 iterations) by the mixed FP32
-solver, replayed as one CUDA graph with all inputs resident in HBM.  The FP64
-solver is timed the same way and reported beside it.
+scalars, and the final FP64 residual check) by the mixed FP32 solver, replayed
+as one CUDA graph with all inputs resident in HBM.  Default workload: C5, the
+largest single-GPU configuration of BASELINE.json (64^3 hex elements, N = 10,
+jittered, 200 iterations; 262 M local points, working set far above the L2).
+The FP64 solver is timed the same way and reported beside it; C2-C4 are
+measured briefly under `other_configs`.
+
+--gpus N (N > 1) without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL z-slabs).
 
 metric = GDOF*iter/s = n_global * niter / step time (DOF = unique global GLL
 nodes, reading R19).  Prints ONE JSON line (rank 0).
@@ -36,7 +41,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--impl", default="nbk", choices=["nbk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -46,10 +51,15 @@ def parse():
     ap.add_argument("--no-precision-study", dest="precision_study", action="store_false",
                     help="skip the VPREC sweep / MCA ensembles (NEXT-4) on C1")
     ap.add_argument("--convergence", type=int, default=4000,
-                    help="iterations of the long convergence / true-residual-floor study (0: skip)")
+                    help="iterations of the long convergence / true-residual-floor study, run on "
+                         "C2 (0: skip)")
+    ap.add_argument("--prof-steps", type=int, default=3,
+                    help="solves replayed with CUDA events between the kernels (per-kernel times)")
+    ap.add_argument("--energy-reps", type=int, default=5,
+                    help="energy-to-solution repeats per solver (mean and spread, P:693-698)")
     ap.add_argument("--no-jacobi", dest="jacobi", action="store_false",
                     help="skip the Jacobi-PCG measurement beside the headline")
-    ap.add_argument("--others", default="C3,C4,C5",
+    ap.add_argument("--others", default="C2,C3,C4",
                     help="other configs measured briefly after the headline (1 GPU; '' = none)")
     return ap.parse_args()
 
@@ -158,40 +168,66 @@ def measured_peak():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg_name, precision):
-    """dram bytes per launch of the fused ax kernel from the committed ncu summary."""
+def ncu_entry(cfg_name, precision, kernel):
+    """Per-launch ncu numbers of one kernel (K_A 'k_ax_fused', K_B 'k_dssum_fused',
+    K_C 'k_vec_rupd') from the committed summary (profiles/ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d[cfg_name][precision]["k_ax_fused"]["dram_bytes_per_launch"]
+        return d[cfg_name][precision][kernel]
     except Exception:
         return None
 
 
+def ncu_traffic(cfg_name, precision, kernel="k_ax_fused"):
+    e = ncu_entry(cfg_name, precision, kernel)
+    return None if e is None else e["dram_bytes_per_launch"]
+
+
 # ---------------------------------------------------------------- oracle
-def oracle_sample(cfg, precision, niter_sample, threads=None):
+def sample_mesh_args(cfg, layers):
+    """A bounded sample of a config for the CPU oracle: its first `layers`
+    element layers in z as a Dirichlet box of their own (same N, element size,
+    jitter and RHS generator; SplitMix64 indices of vertices and nodes are those
+    of the full box for these layers)."""
+    a = cfg.mesh_args(1)
+    a["ez"] = min(a["ez"], layers)
+    return a
+
+
+def oracle_sample(cfg, precision, niter_sample, layers):
     """The oracle as it stands, timed on this host's cores on a bounded sample:
-    the FP64 set-up (untimed) and `niter_sample` CG iterations of the workload."""
+    FP64 set-up (untimed) and `niter_sample` CG iterations of the first `layers`
+    element layers of the workload."""
     import oracle
-    om = oracle.Mesh(**cfg.mesh_args())
+    om = oracle.Mesh(**sample_mesh_args(cfg, layers))
     _, _, D = oracle.gll(cfg.N)
     s = oracle.setup(om)
     t0 = time.perf_counter()
     oracle.cg(om, D, s["G"], s["f"], niter_sample, precision)
     dt = time.perf_counter() - t0
-    return om.sizes()["n_global"] * niter_sample / dt / 1e9, dt
+    return om.sizes()["n_global"] * niter_sample / dt / 1e9, dt, om
+
+
+def sample_layers(cfg):
+    """Element layers of the oracle sample: about 1/16 of C3-C5, all of C1/C2."""
+    return cfg.ez if cfg.ex * cfg.ey * cfg.ez <= 4096 else max(1, cfg.ez // 16)
 
 
 def run_reference(args):
+    """--impl reference: the CPU oracle (this tier's reference arm), timed as it
+    stands on the host's cores; each step = 1 CG iteration (2 for small
+    configs) of a bounded sample of the workload (sample_mesh_args)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from paper_2405_11065_b200.configs import CONFIGS
     import oracle
     cfg = CONFIGS[args.config]
-    iters = 20
-    om = oracle.Mesh(**cfg.mesh_args())
+    layers = sample_layers(cfg)
+    iters = 20 if layers == cfg.ez else 1
+    om = oracle.Mesh(**sample_mesh_args(cfg, layers))
     _, _, D = oracle.gll(cfg.N)
     s = oracle.setup(om)
     ng = om.sizes()["n_global"]
@@ -205,13 +241,16 @@ def run_reference(args):
     tot = sum(times)
     value = ng * iters * args.steps / tot / 1e9
     cores = oracle.num_threads()
-    sample = (f"{args.config} {args.precision} oracle CG, {iters} of {cfg.niter} iterations per step "
-              f"(set-up untimed), OpenMP threads={cores}")
+    sample = (f"{args.config} {args.precision} oracle CG on {om.ex}x{om.ey}x{om.ez} elements "
+              f"(first {layers} of {cfg.ez} z-layers of the workload, N={cfg.N}, {ng} DOF), "
+              f"{iters} of {cfg.niter} iterations per step (set-up untimed), OpenMP threads={cores}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak" if cfg.weak else "strong",
+            "vs_baseline": None,
             "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
-            "config": {"workload": workload_name(cfg, args.precision), "niter_per_step": iters},
+            "config": {"workload": workload_name(cfg, args.precision), "sample": sample,
+                       "niter_per_step": iters},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -293,7 +332,30 @@ def precision_study(nbk, torch, stream, niter=100, samples=20):
     return out
 
 
-def measure_other(nbk, torch, name, flush, stream, peak, steps=3, warmup=2):
+def convergence_study(ctx, niter_max):
+    """Convergence beyond the fixed iteration count (NEXT-2: true-residual floor
+    and iterations to 1e-10 of each solver): recursive h_k/h_0 of one long solve,
+    FP64 true residual (C12) of the returned x after several lengths."""
+    import numpy as np
+    conv = {"niter_max": niter_max}
+    for p_ in ("fp64", "fp32", "fp32s"):
+        hh, _, rr = ctx.cg_solve(niter_max, p_, trace=False)
+        rel = hh / hh[0] if hh[0] else hh
+        it_to = {}
+        for thr in (1e-4, 1e-6, 1e-8, 1e-10, 1e-12):
+            idx = np.nonzero(rel <= thr)[0]
+            it_to[f"{thr:.0e}"] = int(idx[0]) if len(idx) else None
+        tr_at = {}
+        for nit in sorted({n_ for n_ in (250, 500, 1000, 2000) if n_ < niter_max}):
+            _, _, r2 = ctx.cg_solve(nit, p_, trace=False)
+            tr_at[str(nit)] = r2["true_res_rel"]
+        tr_at[str(niter_max)] = rr["true_res_rel"]
+        conv[p_] = {"iters_to_recursive_rel": it_to, "recursive_rel_final": float(rel[-1]),
+                    "true_res_rel_after": tr_at, "defect_iter": rr["defect_iter"]}
+    return conv
+
+
+def measure_other(nbk, torch, name, flush, stream, peak, steps=3, warmup=2, convergence=0):
     """Short measurement of another BASELINE config on 1 GPU (not the headline):
     FP32 and FP64 solver GDOF*iter/s, K_A roofline fraction, FP32/FP64 ratio."""
     cfg = nbk.CONFIGS[name]
@@ -309,9 +371,60 @@ def measure_other(nbk, torch, name, flush, stream, peak, steps=3, warmup=2):
                          "ms_per_step": sum(ms) / steps,
                          "k_ax_hbm_frac": 12 * s_b * n / (ka / 1e3) / 1e9 / peak,
                          "true_res_rel": res["true_res_rel"]}
+        if convergence:
+            out["convergence"] = convergence_study(ctx, convergence)
     out["speedup_fp32_vs_fp64"] = out["fp32"]["value"] / out["fp64"]["value"]
     ctx.close()
     return out
+
+
+def kernel_times(torch, ctx, cfg, prec, steps, flush):
+    """Per-kernel device times from a replay with CUDA events between the
+    kernels of every iteration (events disable the PDL overlap)."""
+    ms, kA, _, _, _ = time_solves(ctx, torch, cfg, prec, steps, 1, flush, profile=True)
+    kB = sum(x[0] for x in time_solves.kBC)
+    kC = sum(x[1] for x in time_solves.kBC)
+    it = steps * cfg.niter
+    return {"K_A_ms": sum(kA) / it, "K_B_ms": kB / it, "K_C_ms": kC / it,
+            "share_K_A": sum(kA) / sum(ms)}
+
+
+def kernel_report(kt, n, ng, s_b, phi, psi, peak, cfg_name, prec):
+    """Algorithmic GB/s and HBM fractions of K_A / K_B / K_C (SURVEY 8(d) bytes
+    per local point: 12s, phi(2s+4) + psi(s+4), 3s) plus the ncu DRAM bytes of
+    the committed capture of the same kernels."""
+    alg = {"K_A": 12 * s_b * n, "K_B": n * (phi * (2 * s_b + 4) + psi * (s_b + 4)), "K_C": 3 * s_b * n}
+    names = {"K_A": "k_ax_fused", "K_B": "k_dssum_fused", "K_C": "k_vec_rupd"}
+    out = {}
+    for k in ("K_A", "K_B", "K_C"):
+        t = kt[k + "_ms"] / 1e3
+        e = ncu_entry(cfg_name, prec, names[k])
+        out[k] = {"ms": kt[k + "_ms"], "alg_bytes": alg[k], "alg_GBps": alg[k] / t / 1e9,
+                  "frac": alg[k] / t / 1e9 / peak,
+                  "ncu_dram_bytes": None if e is None else e["dram_bytes_per_launch"],
+                  "ncu_dram_over_alg": None if e is None else e["dram_bytes_per_launch"] / alg[k],
+                  "ncu_duration_us": None if e is None else e.get("duration_us")}
+    dram = [out[k]["ncu_dram_bytes"] for k in ("K_A", "K_B", "K_C")]
+    out["ncu_dram_bytes_per_global_dof_iter"] = None if None in dram else sum(dram) / ng
+    out["timing"] = ("CUDA events between the kernels of every iteration (profiling replay); "
+                     "ncu numbers: cold-cache --set full capture of one steady-state launch")
+    return out
+
+
+def maybe_relaunch(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run (one
+    rank per GPU, 127.0.0.1 rendezvous) and return its exit code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import subprocess
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def run_gpu(args):
@@ -319,7 +432,7 @@ def run_gpu(args):
     rank, world, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_2405_11065_b200 as nbk
     cfg = nbk.CONFIGS[args.config]
@@ -333,8 +446,10 @@ def run_gpu(args):
             idt.copy_(torch.frombuffer(bytearray(nbk.nccl_unique_id()), dtype=torch.uint8))
         torch.distributed.broadcast(idt, 0)
         nccl_id = bytes(idt.cpu().numpy())
+    t_setup = time.perf_counter()
     ctx = nbk.cg_setup(spec, "fp32", device=local, stream=stream, rank=rank, nranks=world,
                        nccl_id=nccl_id)
+    t_setup = time.perf_counter() - t_setup
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     prec = args.precision
 
@@ -351,42 +466,41 @@ def run_gpu(args):
                                                  flush, profile=False)
         ctx.sync()
     barrier()
-    # ---- same solves again with CUDA events around every k_ax launch (roofline) ----
-    with torch.cuda.stream(stream):
-        ms_prof, kA, _, _, _ = time_solves(ctx, torch, cfg, prec, args.steps, args.warmup, flush,
-                                           profile=True)
-    barrier()
     tot_ms = max_over_ranks(sum(ms), world)
     ng = ctx.n_global  # global unique nodes of the whole (all-rank) box
     value = ng * cfg.niter * args.steps / (tot_ms / 1e3) / 1e9
     launches = ctx.solve_launches(cfg.niter, prec) * args.steps
-
-    # ---- roofline of the dominant kernel (fused ax, K_A) ----
-    s = 4 if prec == "fp32" else 8
     n = ctx.n_local
-    bytes_ka = 12 * s * n  # reads r, p, x, G (9s) + writes p, x, w (3s) per local point
-    ka_avg_ms = sum(kA) / (args.steps * cfg.niter)
-    peak, peak_src = measured_peak()
-    achieved = bytes_ka / (ka_avg_ms / 1e3) / 1e9
-    kb_ms = sum(x[0] for x in time_solves.kBC) / (args.steps * cfg.niter)
-    kc_ms = sum(x[1] for x in time_solves.kBC) / (args.steps * cfg.niter)
-    s_b = 4 if prec == "fp32" else 8
     info0 = ctx.info
     phi0, psi0 = info0["n_copies"] / n, info0["n_shared"] / n
-    kernels = {"K_A_ms": ka_avg_ms, "K_B_ms": kb_ms, "K_C_ms": kc_ms,
-               "K_B_alg_GBps": n * (phi0 * (2 * s_b + 4) + psi0 * (s_b + 4)) / (kb_ms / 1e3) / 1e9,
-               "K_C_alg_GBps": 3 * s_b * n / (kc_ms / 1e3) / 1e9,
-               "timing": "CUDA events between the kernels of every iteration (profiling replay)"}
-    kernels["K_B_frac"] = kernels["K_B_alg_GBps"] / peak
-    kernels["K_C_frac"] = kernels["K_C_alg_GBps"] / peak
+    peak, peak_src = measured_peak()
+    s_b = 4 if prec == "fp32" else 8
+
+    # ---- per-kernel times (replay with events between the kernels) ----
+    with torch.cuda.stream(stream):
+        kt = kernel_times(torch, ctx, cfg, prec, args.prof_steps, flush)
+    barrier()
+    kernels = kernel_report(kt, n, ng, s_b, phi0, psi0, peak, args.config, prec)
+
+    # ---- roofline of the dominant kernel (fused ax, K_A) ----
+    bytes_ka = 12 * s_b * n  # reads r, p, x, G (9s) + writes p, x, w (3s) per local point
+    ka_avg_ms = kt["K_A_ms"]
+    achieved = bytes_ka / (ka_avg_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config, prec),
                 "kernel": "k_ax<fused> (p,x update + ax_e + mask + interior pap)",
                 "algorithmic_bytes_per_launch": bytes_ka, "avg_launch_ms": ka_avg_ms,
-                "share_of_step": sum(kA) / sum(ms_prof),
-                "timing": "CUDA events on the context stream around each k_ax launch, in a "
-                          "replay of the same K solves (events disable the PDL overlap)",
+                "share_of_step": kt["share_K_A"],
+                "ncu_share_of_iteration": None,
+                "timing": f"CUDA events on the context stream around each k_ax launch, in a "
+                          f"replay of {args.prof_steps} solves (events disable the PDL overlap)",
+                "traffic_source": "profiles/ncu_summary.json (ncu --set full, same config)",
                 "peak_source": peak_src}
+    eA, eB, eC = (ncu_entry(args.config, prec, k) for k in ("k_ax_fused", "k_dssum_fused", "k_vec_rupd"))
+    if eA and eB and eC and all(e.get("duration_us") for e in (eA, eB, eC)):
+        roofline["ncu_share_of_iteration"] = eA["duration_us"] / (
+            eA["duration_us"] + eB["duration_us"] + eC["duration_us"])
+        roofline["events_share_of_iteration"] = kt["K_A_ms"] / (kt["K_A_ms"] + kt["K_B_ms"] + kt["K_C_ms"])
 
     # ---- FP64 solver beside it ----
     extra = {}
@@ -396,49 +510,64 @@ def run_gpu(args):
             ms64, _, _, res64, _ = time_solves(ctx, torch, cfg, "fp64", args.steps,
                                                args.warmup, flush, profile=False)
             ctx.sync()
-            _, kA64, _, _, _ = time_solves(ctx, torch, cfg, "fp64", args.steps, args.warmup,
-                                           flush, profile=True)
+            kt64 = kernel_times(torch, ctx, cfg, "fp64", args.prof_steps, flush)
         barrier()
         v64 = ng * cfg.niter * args.steps / (max_over_ranks(sum(ms64), world) / 1e3) / 1e9
-        ka64 = sum(kA64) / (args.steps * cfg.niter)
+        ka64 = kt64["K_A_ms"]
+        k64 = kernel_report(kt64, n, ng, 8, phi0, psi0, peak, args.config, "fp64")
         extra["fp64"] = {"value": v64, "ms_per_step": sum(ms64) / args.steps,
+                         "median_step_ms": statistics.median(ms64),
                          "k_ax_avg_ms": ka64,
                          "k_ax_hbm_frac": 12 * 8 * n / (ka64 / 1e3) / 1e9 / peak,
-                         "true_res_rel": res64["true_res_rel"]}
+                         "kernels": k64, "true_res_rel": res64["true_res_rel"]}
         extra["speedup_fp32_vs_fp64"] = value / v64
-        # energy-to-solution: the NVML counter updates coarsely, so each
-        # solver runs back-to-back solves for >= 2 s and the energy per solve is taken
+        d32 = kernels["ncu_dram_bytes_per_global_dof_iter"]
+        d64 = k64["ncu_dram_bytes_per_global_dof_iter"]
+        extra["bytes_per_dof_ncu"] = {"fp32": d32, "fp64": d64,
+                                      "ratio_fp32_over_fp64": d32 / d64 if d32 and d64 else None,
+                                      "note": "sum of K_A+K_B+K_C ncu DRAM bytes per launch / n_global"}
+        # energy-to-solution: NVML total-energy counter over back-to-back
+        # solves; `energy_reps` windows per solver, mean and standard deviation
         en = {}
         with torch.cuda.stream(stream):
             for p_ in ("fp32", "fp64"):
                 ctx.cg_solve(cfg.niter, p_, trace=False)
                 ctx.sync()
-                nsol, t0 = 0, time.perf_counter()
-                with Energy(local) as eg:
-                    while time.perf_counter() - t0 < 2.0:
-                        for _ in range(10):
+                per = []
+                for _ in range(args.energy_reps):
+                    nsol, t0 = 0, time.perf_counter()
+                    with Energy(local) as eg:
+                        while time.perf_counter() - t0 < 1.5 or nsol < 2:
                             ctx.cg_solve(cfg.niter, p_, trace=False)
-                        nsol += 10
-                    ctx.sync()
-                    dt = time.perf_counter() - t0
-                if eg.joules:
-                    en[p_] = {"J_per_solve": eg.joules / nsol, "solves": nsol, "avg_W": eg.joules / dt}
+                            nsol += 1
+                        ctx.sync()
+                        dt = time.perf_counter() - t0
+                    if eg.joules:
+                        per.append((eg.joules / nsol, eg.joules / dt, nsol))
+                if per:
+                    j = [x[0] for x in per]
+                    en[p_] = {"J_per_solve_mean": statistics.mean(j),
+                              "J_per_solve_stdev": statistics.stdev(j) if len(j) > 1 else 0.0,
+                              "avg_W_mean": statistics.mean(x[1] for x in per),
+                              "windows": len(per), "solves_per_window": [x[2] for x in per]}
         if "fp32" in en and "fp64" in en:
-            extra["energy"] = {**en, "fp64_over_fp32": en["fp64"]["J_per_solve"] / en["fp32"]["J_per_solve"],
-                               "note": "NVML total-energy counter over >= 2 s of back-to-back "
-                                       "solves per solver (incl. the FP64 final check)"}
+            extra["energy"] = {**en, "fp64_over_fp32": en["fp64"]["J_per_solve_mean"] /
+                               en["fp32"]["J_per_solve_mean"],
+                               "energy_saving_fp32": 1 - en["fp32"]["J_per_solve_mean"] /
+                               en["fp64"]["J_per_solve_mean"],
+                               "note": "NVML total-energy counter, >= 1.5 s windows of back-to-back "
+                                       "solves (incl. the FP64 final check), mean / stdev over "
+                                       "windows (the paper: mean of 5 runs, P:693-698)"}
 
     # ---- accuracy of the single-precision solvers vs FP64 (P:517-522 AE / MAE; NEXT-2) ----
     if args.accuracy and world == 1:
         import numpy as np
         with torch.cuda.stream(stream):
-            h = {}
-            xs = {}
-            rs = {}
+            h, xs, rs = {}, {}, {}
             for p_ in ("fp64", "fp32", "fp32s"):
                 h[p_], _, rs[p_] = ctx.cg_solve(cfg.niter, p_, trace=False)
                 xs[p_] = ctx.solution()
-            ms1, _, _, _, _ = time_solves(ctx, torch, cfg, "fp32s", args.steps, args.warmup, flush,
+            ms1, _, _, _, _ = time_solves(ctx, torch, cfg, "fp32s", min(args.steps, 3), 1, flush,
                                           profile=False)
         acc = {}
         for p_ in ("fp32", "fp32s"):
@@ -449,34 +578,11 @@ def run_gpu(args):
                        "x_err_vs_fp64": float(np.abs(xs[p_] - xs["fp64"]).max() /
                                               np.abs(xs["fp64"]).max())}
         acc["fp64_true_res_rel"] = rs["fp64"]["true_res_rel"]
-        acc["fp32s_value"] = ng * cfg.niter * args.steps / (sum(ms1) / 1e3) / 1e9
+        acc["fp32s_value"] = ng * cfg.niter * len(ms1) / (sum(ms1) / 1e3) / 1e9
         acc["note"] = ("fp32: north_star mixed solver (FP64 inner-product accumulation); fp32s: "
-                       "paper-literal single (binary32 inner products and scalars, R11b)")
-        # convergence beyond the fixed 100 iterations (NEXT-2: true-residual floor and
-        # iterations to 1e-10): recursive h_k/h_0 of one long solve, true residual (FP64
-        # check of the returned x) after several lengths
-        if args.convergence:
-            conv = {"niter_max": args.convergence}
-            with torch.cuda.stream(stream):
-                for p_ in ("fp64", "fp32", "fp32s"):
-                    hh, _, rr = ctx.cg_solve(args.convergence, p_, trace=False)
-                    rel = hh / hh[0] if hh[0] else hh
-                    it_to = {}
-                    for thr in (1e-4, 1e-6, 1e-8, 1e-10, 1e-12):
-                        idx = np.nonzero(rel <= thr)[0]
-                        it_to[f"{thr:.0e}"] = int(idx[0]) if len(idx) else None
-                    tr_at = {}
-                    for nit in sorted({n_ for n_ in (250, 500, 1000, 2000) if n_ < args.convergence}):
-                        _, _, r2 = ctx.cg_solve(nit, p_, trace=False)
-                        tr_at[str(nit)] = r2["true_res_rel"]
-                    tr_at[str(args.convergence)] = rr["true_res_rel"]
-                    conv[p_] = {"iters_to_recursive_rel": it_to,
-                                "recursive_rel_final": float(rel[-1]),
-                                "true_res_rel_after": tr_at,
-                                "defect_iter": rr["defect_iter"]}
-            acc["convergence"] = conv
+                       "binary32 inner products (exactly rounded) and binary32 scalars (R11b)")
         extra["accuracy"] = acc
-        del np
+        del xs
 
     # ---- Jacobi PCG beside it: same workload, z = r / diag(A) ----
     if args.jacobi:
@@ -485,11 +591,11 @@ def run_gpu(args):
         with torch.cuda.stream(stream):
             ctx.set_precond("jacobi")
             for p_ in ("fp32", "fp64"):
-                msj, _, _, resj, histj = time_solves(ctx, torch, cfg, p_, args.steps, args.warmup,
+                msj, _, _, resj, histj = time_solves(ctx, torch, cfg, p_, min(args.steps, 3), 1,
                                                      flush, profile=False)
-                jac[p_] = {"value": ng * cfg.niter * args.steps /
+                jac[p_] = {"value": ng * cfg.niter * len(msj) /
                            (max_over_ranks(sum(msj), world) / 1e3) / 1e9,
-                           "ms_per_step": sum(msj) / args.steps,
+                           "ms_per_step": sum(msj) / len(msj),
                            "h_final_rel": float(histj[-1] / histj[0]) if histj[0] else 0.0,
                            "true_res_rel": resj["true_res_rel"]}
             ctx.set_precond("none")
@@ -497,15 +603,16 @@ def run_gpu(args):
         extra["jacobi_pcg"] = jac
 
     # ---- end to end through the C ABI with host buffers ----
-    import numpy as np
     f_host = torch.empty(ctx.shape, dtype=torch.float64).pin_memory()
-    _, _, f0 = ctx.get_arrays()
+    _, _, f0 = ctx.get_arrays(G=False)
     f_host.numpy()[...] = f0
+    del f0
     x_host = torch.empty(ctx.shape, dtype=torch.float64).pin_memory()
     ctx.set_profiling(False)
-    for _ in range(args.warmup):
+    for _ in range(min(args.warmup, 2)):
         ctx.cg_solve_host(f_host.numpy(), cfg.niter, prec, x_host.numpy())
     e2e_ms = []
+    barrier()
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -517,27 +624,26 @@ def run_gpu(args):
     e2e_val = ng * cfg.niter * args.steps / (max_over_ranks(sum(e2e_ms), world) / 1e3) / 1e9
     e2e = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
            "d2h_bytes_per_step": 8 * n + 8 * (cfg.niter + 1),
-           "path": "nbk_cg_solve_host (pinned host f -> solve -> host x)"}
-    del np
+           "path": "nbk_cg_solve_host (pinned host f -> solve -> host x), CUDA events on the "
+                   "context stream around each call"}
+    del f_host, x_host
 
     # ---- CPU baseline: the oracle on this host, bounded sample ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
-        iters = 40 if cfg.N <= 8 and cfg.ex * cfg.ey * cfg.ez <= 4096 else 2
-        v_cpu, dt = oracle_sample(cfg, prec, iters)
+        layers = sample_layers(cfg)
+        iters = 40 if layers == cfg.ez else 2
+        v_cpu, dt, om = oracle_sample(cfg, prec, iters, layers)
         cpu = {"value": v_cpu, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-               "sample": f"{args.config} {prec} oracle CG, {iters} of {cfg.niter} iterations "
-                         f"({dt:.1f} s; set-up untimed)"}
+               "sample": f"{args.config} {prec} oracle CG on {om.ex}x{om.ey}x{om.ez} elements "
+                         f"(first {layers} of {cfg.ez} z-layers of the workload), {iters} of "
+                         f"{cfg.niter} iterations ({dt:.1f} s; set-up untimed)"}
 
     # whole-iteration algorithmic bandwidth (SURVEY 8(d) B_fused model)
-    info = ctx.info
-    phi = info["n_copies"] / n
-    psi = info["n_shared"] / n
-    s_b = 4 if prec == "fp32" else 8
-    b_fused = 15 * s_b + phi * (2 * s_b + 4) + psi * (s_b + 4)
+    b_fused = 15 * s_b + phi0 * (2 * s_b + 4) + psi0 * (s_b + 4)
     t_iter = tot_ms / args.steps / cfg.niter / 1e3
-    b_fused64 = 15 * 8 + phi * (2 * 8 + 4) + psi * (8 + 4)
+    b_fused64 = 15 * 8 + phi0 * (2 * 8 + 4) + psi0 * (8 + 4)
     model = {"B_fused_bytes_per_local_point": b_fused,
              "bytes_per_global_dof": b_fused * n / ng,
              "bytes_per_global_dof_fp64_solver": b_fused64 * n / ng,
@@ -555,7 +661,8 @@ def run_gpu(args):
         del ctx
         torch.cuda.empty_cache()
         for name in args.others.split(","):
-            others[name] = measure_other(nbk, torch, name, flush, stream, peak)
+            others[name] = measure_other(nbk, torch, name, flush, stream, peak,
+                                         convergence=args.convergence if name == "C2" else 0)
             torch.cuda.empty_cache()
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -566,12 +673,13 @@ def run_gpu(args):
                        "niter": cfg.niter,
                        "parallelism": "1 GPU" if world == 1 else
                        f"{world} z-slabs (NCCL face exchange + all-gather)",
-                       "l2": "flushed between steps (512 MiB write, outside the events)"},
+                       "l2": "flushed between steps (512 MiB write, outside the events); the "
+                             "per-iteration working set is far above the 126 MB L2"},
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "true_res_rel": res["true_res_rel"],
             "h_final_rel": float(hist[-1] / hist[0]) if hist[0] else 0.0,
-            "median_step_ms": statistics.median(ms), "iteration_model": model,
-            "kernels": kernels, **extra,
+            "median_step_ms": statistics.median(ms), "setup_s": t_setup,
+            "iteration_model": model, "kernels": kernels, **extra,
             "other_configs": others or None, "precision_tools": precision}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -582,6 +690,9 @@ def run_gpu(args):
 
 def main():
     args = parse()
+    rc = maybe_relaunch(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

@@ -87,7 +87,9 @@ typedef struct {
 typedef struct {
     int32_t rank, nranks; /* this context's slab and the number of slabs            */
     int32_t device;       /* CUDA device ordinal                                    */
-    void* stream;         /* cudaStream_t the library enqueues on (NULL = legacy)   */
+    void* stream;         /* cudaStream_t the library enqueues on; NULL = a stream the
+                             context creates (blocking, so ordered with the legacy
+                             default stream) and destroys in nbk_destroy           */
     const void* nccl_id;  /* NCCL mode: 128-byte ncclUniqueId; NULL otherwise       */
 } nbk_dist;
 
@@ -156,7 +158,9 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
 /* Parity path (C10): replace the set-up data with host FP64 arrays (e.g. the
  * oracle's): D (N*N, row a = evaluation node), G (e_local*6*N^3), f
  * (e_local*N^3, local storage).  Any pointer may be NULL (keep current).
- * FP32 copies are re-derived.  Synchronous. */
+ * A new D or G re-derives the FP32 copies and invalidates the library's own
+ * Jacobi diagonal (a diagonal loaded with nbk_load_precond is kept only when
+ * just f changes).  Synchronous. */
 nbk_status nbk_load_arrays(nbk_ctx* ctx, const double* D_host, const double* G_host,
                            const double* f_host);
 
@@ -200,7 +204,9 @@ nbk_status nbk_cg_solve(nbk_ctx* ctx, int32_t niter, nbk_precision precision, do
 
 /* End-to-end form of cg_solve for host data: copies f_host (e_local*N^3 FP64,
  * NULL = keep the set-up RHS) to the device, solves, and copies the solution
- * (as FP64, exact for the FP32 solver) to x_host (may be NULL).  Synchronous. */
+ * (as FP64, exact for the FP32 solver) to x_host (may be NULL).  A new RHS
+ * leaves the operator, its FP32 copy and any Jacobi data untouched.
+ * Synchronous. */
 nbk_status nbk_cg_solve_host(nbk_ctx* ctx, const double* f_host, int32_t niter,
                              nbk_precision precision, double* x_host, double* hist_host,
                              nbk_result* result);
@@ -223,7 +229,8 @@ nbk_status nbk_solution_ptr(nbk_ctx* ctx, nbk_precision precision, void** x_dev)
  * xi = SplitMix64(seed, 4 key + slot) with key = (iteration, phase, global
  * local index, operation number): one seed = one sample, reproducible and
  * identical to the oracle's.  Each correctly rounded glsc3 counts as one
- * operation.  nbk_set_vprec(ctx, t) = nbk_set_emulation(ctx, VPREC, t, 0). */
+ * operation.  nbk_set_vprec(ctx, t) = nbk_set_emulation(ctx, VPREC, t, 0).
+ * An NBK_VPREC solve with NBK_PRECOND_JACOBI selected returns NBK_EINVAL. */
 #define NBK_EMU_VPREC 1
 #define NBK_EMU_RR 2
 #define NBK_EMU_MCA 3

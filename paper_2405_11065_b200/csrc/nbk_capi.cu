@@ -163,10 +163,14 @@ static nbk_status glsc3_team(const Team& t, const std::vector<const T*>& a, cons
     return NBK_OK;
 }
 
+// The operator (D and / or G) changed: re-derive the FP32 copies (C11) and
+// re-assemble the own Jacobi diagonal on demand.  A new RHS alone only needs
+// a new h0 (callers set h0_dirty): G is not re-downcast and a diagonal loaded
+// with nbk_load_precond stays in use.
 static nbk_status refresh_fp32(nbk_ctx* c)
 {
     cudaStream_t s = c->stream;
-    c->dinv_dirty = 1;  // the operator may have changed: own diagonal re-assembled on demand
+    c->dinv_dirty = 1;  // own diagonal re-assembled on demand
     if (c->G32) {
         k_downcast<<<vec_grid(6 * c->n), 256, 0, s>>>(c->G32, c->G64, 6 * c->n);
         k_downcast<<<1, 256, 0, s>>>(c->D32, c->D64, (int64_t)c->N * c->N);
@@ -242,6 +246,8 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
         if (prec == NBK_VPREC && m->pm_mode != PM_VPREC && m->N > NBK_MC_MAXN)
             return fail(c, NBK_EINVAL, "RR / MCA emulation supports N <= 8");
         if (prec == NBK_VPREC && t.multi) return fail(c, NBK_EINVAL, "precision emulation runs on one rank");
+        if (prec == NBK_VPREC && m->precond != NBK_PRECOND_NONE)
+            return fail(c, NBK_EINVAL, "precision emulation runs the unpreconditioned CG only");
     }
     nbk_status st = refresh_h0(t);
     if (st != NBK_OK) return st;
@@ -368,6 +374,15 @@ nbk_status nbk_cg_setup(const nbk_mesh* mesh, nbk_precision precision, const nbk
     c->dist = *d;
     c->setup_precision = precision;
     c->stream = (cudaStream_t)d->stream;
+    if (!c->stream) {
+        // NULL: the legacy default stream cannot be captured into the solve
+        // graph; a blocking stream of our own is implicitly ordered with it
+        if (cudaStreamCreate(&c->own_stream) != cudaSuccess) {
+            delete c;
+            return fail(nullptr, NBK_ECUDA, "cannot create the context stream");
+        }
+        c->stream = c->own_stream;
+    }
     c->N = mesh->N;
     c->E = L.E;
     c->n = L.n;
@@ -469,8 +484,11 @@ nbk_status nbk_load_arrays(nbk_ctx* c, const double* D_host, const double* G_hos
     if (D_host) NBK_CUDA(c, cudaMemcpyAsync(c->D64, D_host, 8 * c->N * c->N, cudaMemcpyHostToDevice, s));
     if (G_host) NBK_CUDA(c, cudaMemcpyAsync(c->G64, G_host, 8 * 6 * c->n, cudaMemcpyHostToDevice, s));
     if (f_host) NBK_CUDA(c, cudaMemcpyAsync(c->f64, f_host, 8 * c->n, cudaMemcpyHostToDevice, s));
-    nbk_status st = refresh_fp32(c);
-    if (st != NBK_OK) return st;
+    if (D_host || G_host) {  // operator changed
+        nbk_status st = refresh_fp32(c);
+        if (st != NBK_OK) return st;
+    }
+    if (f_host) c->h0_dirty = 1;
     NBK_CUDA(c, cudaStreamSynchronize(s));
     return NBK_OK;
 }
@@ -687,9 +705,7 @@ nbk_status nbk_cg_solve_host(nbk_ctx* c, const double* f_host, int32_t niter, nb
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
     if (f_host) {
         NBK_CUDA(c, cudaMemcpyAsync(c->f64, f_host, 8 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
-        nbk_status st0 = refresh_fp32(c);  // new RHS: new h0 for the relative residual
-        if (st0 != NBK_OK) return st0;
-        c->h0_dirty = 1;
+        c->h0_dirty = 1;  // new RHS: new h0 for the relative residual (operator unchanged)
     }
     nbk_status st = nbk_cg_solve(c, niter, prec, hist_host, nullptr, result);
     if (st != NBK_OK && st != NBK_EDEFECT) return st;
@@ -841,6 +857,10 @@ void nbk_destroy(nbk_ctx* c)
     if (c->ev_pack) cudaEventDestroy(c->ev_pack);
     if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->own_stream) {
+        cudaStreamSynchronize(c->own_stream);
+        cudaStreamDestroy(c->own_stream);
+    }
     // unlink from a virtual group: the others must not alias this workspace
     for (nbk_ctx* o : std::vector<nbk_ctx*>(c->group)) {
         if (o == c) continue;

@@ -1,7 +1,7 @@
 // nbk_emu.cu -- precision-emulated solves: the CG loop of
 // enqueue_solve instantiated with PM = NBK_EMU_MODE (compiled once per mode by
 // build.py, -DNBK_EMU_MODE=1/2/3, in parallel).  Entry points are suffixed by
-// the mode; nbk_emu_dispatch.cu (in nbk_capi.cu) selects them.
+// the mode; enqueue_emulated / emulated_attrs in nbk_capi.cu select them.
 #include "nbk_launch.cuh"
 
 namespace nbk {

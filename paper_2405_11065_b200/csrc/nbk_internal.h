@@ -28,6 +28,8 @@ struct nbk_ctx {
     nbk_dist dist{};
     nbk_precision setup_precision = NBK_FP64;
     cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;  // created when dist->stream is NULL (a blocking stream,
+                                        // implicitly ordered with the legacy default stream)
     int N = 0;
     int64_t E = 0, n = 0, n_global = 0, e_offset = 0;
     int64_t nseg = 0, ncopies = 0;

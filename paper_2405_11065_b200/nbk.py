@@ -246,26 +246,44 @@ class Context:
         arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64) for a in (D, G, f)]
         _check(self.lib.nbk_load_arrays(self._ctx, *[_ptr(a) for a in arrs]), self._ctx)
 
-    def get_arrays(self):
-        N, n = self.N, self.n_local
+    def get_arrays(self, G: bool = True):
+        """The context's FP64 set-up data (D, G, f); G=False skips the 48 B/pt G."""
+        N = self.N
         D = np.zeros((N, N))
-        G = np.zeros((self.shape[0], 6, N, N, N))
+        Ga = np.zeros((self.shape[0], 6, N, N, N)) if G else None
         f = np.zeros(self.shape)
-        _check(self.lib.nbk_get_arrays(self._ctx, _ptr(D), _ptr(G), _ptr(f)), self._ctx)
-        del n
-        return D, G, f
+        _check(self.lib.nbk_get_arrays(self._ctx, _ptr(D), _ptr(Ga), _ptr(f)), self._ctx)
+        return D, Ga, f
+
+    def _enter(self):
+        """Order the context stream after the caller's current stream (the
+        tensors passed in may still be being produced there)."""
+        cur = self.torch.cuda.current_stream(self.device)
+        if cur != self.stream:
+            self.stream.wait_stream(cur)
+        return cur
+
+    def _leave(self, cur, *tensors):
+        """Order the caller's stream after the library's work on `tensors`."""
+        if cur != self.stream:
+            cur.wait_stream(self.stream)
+            for t in tensors:
+                t.record_stream(self.stream)
 
     def ax_apply(self, u, w, flags: int = AX_DSSUM | AX_MASK):
         prec = self._prec_of(u)
-        with self.torch.cuda.stream(self.stream):
-            _check(self.lib.nbk_ax_apply(self._ctx, self._dev(u, u.dtype), self._dev(w, u.dtype),
-                                         flags, PREC[prec]), self._ctx)
+        cur = self._enter()
+        _check(self.lib.nbk_ax_apply(self._ctx, self._dev(u, u.dtype), self._dev(w, u.dtype),
+                                     flags, PREC[prec]), self._ctx)
+        self._leave(cur, u, w)
         return w
 
     def dssum(self, f, apply_mask: bool = False):
         prec = self._prec_of(f)
+        cur = self._enter()
         _check(self.lib.nbk_dssum(self._ctx, self._dev(f, f.dtype), int(apply_mask), PREC[prec]),
                self._ctx)
+        self._leave(cur, f)
         return f
 
     def glsc3(self, a, b, single: bool = False) -> float:
@@ -273,6 +291,7 @@ class Context:
         if single:
             prec = "fp32s"
         out = ctypes.c_double(0.0)
+        self._enter()  # synchronous call: nothing to order afterwards
         _check(self.lib.nbk_glsc3(self._ctx, self._dev(a, a.dtype), self._dev(b, a.dtype),
                                   PREC[prec], ctypes.byref(out)), self._ctx)
         return float(out.value)
@@ -380,19 +399,24 @@ class Group:
 
     def ax_apply(self, us, ws, flags: int = AX_DSSUM | AX_MASK):
         prec = Context._prec_of(us[0])
+        cur = self.ctxs[0]._enter()
         _check(self.lib.nbk_group_ax_apply(self._arr, self.P, self._ptrs(us), self._ptrs(ws),
                                            flags, PREC[prec]), self.ctxs[0]._ctx)
+        self.ctxs[0]._leave(cur, *us, *ws)
         return ws
 
     def dssum(self, fs, apply_mask: bool = False):
         prec = Context._prec_of(fs[0])
+        cur = self.ctxs[0]._enter()
         _check(self.lib.nbk_group_dssum(self._arr, self.P, self._ptrs(fs), int(apply_mask),
                                         PREC[prec]), self.ctxs[0]._ctx)
+        self.ctxs[0]._leave(cur, *fs)
         return fs
 
     def glsc3(self, a_s, b_s) -> float:
         prec = Context._prec_of(a_s[0])
         out = ctypes.c_double(0.0)
+        self.ctxs[0]._enter()
         _check(self.lib.nbk_group_glsc3(self._arr, self.P, self._ptrs(a_s), self._ptrs(b_s),
                                         PREC[prec], ctypes.byref(out)), self.ctxs[0]._ctx)
         return float(out.value)
@@ -409,15 +433,7 @@ class Group:
     def solution(self) -> np.ndarray:
         return np.concatenate([c.solution() for c in self.ctxs], axis=0)
 
-    def set_vprec(self, t: int):
-        """Mantissa bits of the VPREC-emulated solver (cg_solve(..., 'vprec'))."""
-        _check(self.lib.nbk_set_vprec(self._ctx, int(t)), self._ctx)
-
-    def set_emulation(self, mode: str, t: int, seed: int = 0):
-        """Emulation of cg_solve(..., 'vprec'): mode 'vprec', 'rr' or 'mca' at
-        virtual precision t; seed selects the RR / MCA sample."""
-        _check(self.lib.nbk_set_emulation(self._ctx, EMU[mode], int(t), seed & (2**64 - 1)),
-               self._ctx)
+    # (precision emulation runs on one rank: Group has no set_emulation)
 
     def set_precond(self, precond: str):
         for c in self.ctxs:

@@ -66,6 +66,18 @@ def stalls(h, r, top=5):
     return [(w, v / tot) for v, w in sorted(out, reverse=True)[:top]]
 
 
+def kernel_key(name):
+    """Summary key of a CG-loop kernel: K_A k_ax<T, N, 1, 0>, K_B k_dssum<T, 1, 0>,
+    K_C k_vec<T, V, 1, 0> (RUPD); None for the others."""
+    if "k_ax<" in name and name.replace(" ", "").endswith(",1,0>(AxArgs<T1>)"):
+        return "k_ax_fused"
+    if "k_dssum<" in name and ", 1, 0>" in name:
+        return "k_dssum_fused"
+    if "k_vec<" in name and name.replace(" ", "").split(">(")[0].endswith(",1,0"):
+        return "k_vec_rupd"
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
@@ -95,13 +107,23 @@ def main():
                     md.append(f"| {label} (`{m}`) | {v} {units[h.index(m)]} |")
             md.append("| top stalls | " + ", ".join(f"{w} {100 * f:.0f}%" for w, f in stalls(h, r)) + " |")
             md.append("")
-            if "k_ax" in name and (", 1>" in name or ", 1, 0>" in name):
+            key = kernel_key(name)
+            if key:
                 def b(m):
                     u = units[h.index(m)]
                     x = float(vals[m].replace(",", ""))
                     return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-                js.setdefault(cfg, {}).setdefault(prec, {})["k_ax_fused"] = {
+
+                def us(m):
+                    u = units[h.index(m)]
+                    x = float(vals[m].replace(",", ""))
+                    return x * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3,
+                             "second": 1e6, "s": 1e6}.get(u, 1)
+                js.setdefault(cfg, {}).setdefault(prec, {})[key] = {
                     "dram_bytes_per_launch": b("dram__bytes_read.sum") + b("dram__bytes_write.sum"),
+                    "dram_read_bytes": b("dram__bytes_read.sum"),
+                    "dram_write_bytes": b("dram__bytes_write.sum"),
+                    "duration_us": us("gpu__time_duration.sum"),
                     "source": os.path.basename(path), "round": a.round}
     for spec in a.launches:
         cfg, path = spec.split(":", 1)
