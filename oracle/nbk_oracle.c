@@ -881,13 +881,17 @@ int ora_cg32s(int ex, int ey, int ez, int N, const double* D, const double* G, c
 /* floor(log2|x|) + 1, slot 0 = result, 1.. = operands in order.        */
 /* key = ((it*8 + phase) * 2^40 + L) * 128 + op, phases A (ax step: ops  */
 /* per output point: 0 p update, 1 x update [key of iteration it+1, the  */
-/* iteration whose step applies it; both updates keyed by the global     */
-/* node id instead of L, so that every copy of a node draws the same xi  */
-/* and the vectors stay continuous], 2.. ur, 2+N.. us, 2+2N.. ut chains, */
+/* iteration whose step applies it], 2.. ur, 2+N.. us, 2+2N.. ut chains, */
 /* 2+3N.. metric (9), 11+3N.. r/s transpose chain (2N), 11+5N+l t chain, */
 /* 11+6N final add), B (dssum: chain add c of a node, L = first copy),   */
-/* C (r update, global node id), S (scalars, L = 0: 0 pap, 1 alpha, 2 rtr, 3 sqrt, 4 */
-/* beta of the next iteration; iteration 0 = initial rtr, h0).  Each     */
+/* C (r update), S (scalars, L = 0: 0 pap, 1 alpha, 2 rtr, 3 sqrt, 4     */
+/* beta of the next iteration; iteration 0 = initial rtr, h0).  L is the */
+/* local index of the point the operation produces: every dynamic FP     */
+/* operation draws its own xi ("the result and/or operands of   */
+/* each FP operation is replaced by a perturbed computation"), so the    */
+/* pointwise updates of the copies of a shared node are perturbed        */
+/* independently and, under RR / MCA, p, x and r are not continuous;     */
+/* dssum still writes one chain sum per node to every copy (C4).  Each   */
 /* correctly rounded glsc3 is one operation (VPREC also rounds the       */
 /* products of its terms).  This function shares no code with the       */
 /* macro-generated VPREC loop above (cross-checked in the pins).         */
@@ -1037,13 +1041,13 @@ int ora_cgpm(int ex, int ey, int ez, int N, const double* D, const double* G, co
         double rtz1 = rtz, beta = 0.0, alpha = 0.0, pap;
         if (rtz1 == 0.0) zero = 1;
         if (!zero && k > 1) beta = P_DIV(rtz1, rtz2, pm_key(k - 1, ORA_PH_S, 0, 4));
-        for (int64_t L = 0; L < n; ++L) p[L] = P_FMA(beta, p[L], r[L], pm_key(k, ORA_PH_A, point_gid(&m, L), 0));
+        for (int64_t L = 0; L < n; ++L) p[L] = P_FMA(beta, p[L], r[L], pm_key(k, ORA_PH_A, L, 0));
         pm_ax_local(k, E, N, D, G, p, w);
         pm_dssum_mask(k, &m, w);
         pap = pm_glsc3(n, w, p, c, pm_key(k, ORA_PH_S, 0, 0));
         if (!zero) alpha = P_DIV(rtz1, pap, pm_key(k, ORA_PH_S, 0, 1));
-        for (int64_t L = 0; L < n; ++L) x[L] = P_FMA(alpha, p[L], x[L], pm_key(k + 1, ORA_PH_A, point_gid(&m, L), 1));
-        for (int64_t L = 0; L < n; ++L) r[L] = P_FMA(-alpha, w[L], r[L], pm_key(k, ORA_PH_C, point_gid(&m, L), 0));
+        for (int64_t L = 0; L < n; ++L) x[L] = P_FMA(alpha, p[L], x[L], pm_key(k + 1, ORA_PH_A, L, 1));
+        for (int64_t L = 0; L < n; ++L) r[L] = P_FMA(-alpha, w[L], r[L], pm_key(k, ORA_PH_C, L, 0));
         rtr = pm_glsc3(n, r, r, c, pm_key(k, ORA_PH_S, 0, 2));
         hist[k] = P_SQRT(rtr, pm_key(k, ORA_PH_S, 0, 3));
         rtz = rtr;

@@ -265,6 +265,9 @@ __device__ __forceinline__ double vprec_round(double x, int t)
 // (iteration, phase, global local index, op number) -- the oracle numbers the
 // operations identically, so emulated runs are bitwise comparable.
 enum { PM_NONE = 0, PM_VPREC = 1, PM_RR = 2, PM_MCA = 3 };
+// Random perturbation modes draw per operation (per local point): the copies of
+// a shared node then differ, so no per-node shortcut of a sum over copies holds.
+__host__ __device__ constexpr bool pm_discontinuous(int pm) { return pm == PM_RR || pm == PM_MCA; }
 struct PmArgs {
     int t;                    // virtual precision (mantissa bits)
     unsigned long long seed;  // RR / MCA sample seed

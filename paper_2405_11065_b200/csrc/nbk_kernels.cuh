@@ -82,15 +82,13 @@ __device__ __forceinline__ void fma_row(T (&b)[N], const T (&d)[N], T t, const P
     }
 }
 
-// Global node id of local point (e, i, j, k): the emulation key of the pointwise
-// vector updates, so that every copy of a node draws the same perturbation and
-// the fields stay continuous (the fused per-node pap stays exact).
-__device__ __forceinline__ long long node_gid(const MeshView& m, uint32_t e, int i, int j, int k)
+// Emulation keys (NEXT-4) name the operation by the local index L of the point
+// it produces (every FP operation perturbed on its own), so under RR /
+// MCA the copies of a shared node get independent perturbations and p, x, r are
+// not continuous: the shared-node pap is then summed over all copies (K_B).
+__device__ __forceinline__ long long global_local_index(const MeshView& m, int64_t L)
 {
-    const ElemCoord ec = elem_coord(m, e);
-    const long long n1 = m.N - 1;
-    const long long Gx = (long long)m.ex * n1 + 1, Gy = (long long)m.ey * n1 + 1;
-    return (ec.ax * n1 + i) + Gx * ((ec.ay * n1 + j) + Gy * (ec.azg * n1 + k));
+    return (long long)m.z0 * m.ex * m.ey * m.N * m.N * m.N + L;
 }
 
 // glsc3 term: VPREC rounds the product, vp(a b) c (NEXT-4); RR / MCA treat the
@@ -296,8 +294,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 const T po = v;
                 T zk = rreg[k];
                 if constexpr (FUSED == 2) zk = mul_t<T>(rreg[k], dreg[k]);  // solveM (Jacobi)
-                long long gk = 0;  // emulation: pointwise updates keyed by the global node
-                if constexpr (PM != PM_NONE) gk = node_gid(a.mesh, (uint32_t)e, i, j, k);
+                const long long gk = goff + base + (long long)k * N2;  // emulation key: local index
                 v = pfma<PM>(betaT, po, zk, P, pm_key(a.it, PH_A, gk, 0));
                 a.x[base + k * N2] = pfma<PM>(alphaT, po, xreg[k], P, pm_key(a.it, PH_A, gk, 1));
                 a.p[base + k * N2] = v;
@@ -712,7 +709,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) v[h][c] = a.w[ix[h][c]];
-                if constexpr (FUSED)
+                if constexpr (FUSED && !pm_discontinuous(PM))
                     if (m[h]) p0[h] = __ldg(a.p + ix[h][0]);
             }
 #pragma unroll
@@ -729,7 +726,16 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
                     if (c < m[h]) a.w[ix[h][c]] = sum;
-                if constexpr (FUSED) add_node_pap<T, PM>(acc, sum, p0[h], m[h], a.single, a.pm);
+                if constexpr (FUSED && pm_discontinuous(PM)) {
+                    // RR / MCA: the copies of p differ -- one term RN(RN(w p_c) / m) per copy
+                    // (C6 over every local point, as the oracle's glsc3)
+                    const double cm = m[h] == 2 ? 0.5 : (m[h] == 4 ? 0.25 : 0.125);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        if (c < m[h]) acc.add(dot_term_pm<PM>(sum, __ldg(a.p + ix[h][c]), cm, false, a.pm));
+                } else if constexpr (FUSED) {
+                    add_node_pap<T, PM>(acc, sum, p0[h], m[h], a.single, a.pm);
+                }
             }
         }
         if (a.stage) __syncthreads();
@@ -926,17 +932,9 @@ struct VecChunk {
         } else if constexpr (MODE == VEC_RUPD) {
             VecT<T, V> r;
 #pragma unroll
-            for (int t = 0; t < V; ++t) {  // C8 (emulation key: the point's global node, phase C)
-                long long g = 0;
-                if constexpr (PM != PM_NONE) {
-                    const int N = a.mesh.N, N3 = N * N * N;
-                    const int64_t Lt = L + t;
-                    const uint32_t e = (uint32_t)(Lt / N3);
-                    const int rem = (int)(Lt - (int64_t)e * N3);
-                    g = node_gid(a.mesh, e, rem % N, (rem / N) % N, rem / (N * N));
-                }
-                r.v[t] = pfma<PM>(am, A.v[t], B.v[t], a.pm, pm_key(a.it, PH_C, g, 0));
-            }
+            for (int t = 0; t < V; ++t)  // C8 (emulation key: the point's local index, phase C)
+                r.v[t] = pfma<PM>(am, A.v[t], B.v[t], a.pm,
+                                  pm_key(a.it, PH_C, global_local_index(a.mesh, L + t), 0));
             r.store(a.r + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) acc.add(dot_term_pm<PM>(r.v[t], r.v[t], c[t], a.single, a.pm));
@@ -1056,7 +1054,7 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
 }
 
 // x = fma(alphaT, p, x) after the last iteration (deferred C8 x update).
-// PM: the x update of "iteration niter + 1" (emulation key: op 1 of phase A, global node)
+// PM: the x update of "iteration niter + 1" (emulation key: op 1 of phase A, local index)
 template <typename T, int PM = PM_NONE>
 __global__ void __launch_bounds__(256) k_tail_x(T* x, const T* p, const CgState* st, int64_t n,
                                                 PmArgs P, int it, MeshView m)
@@ -1065,14 +1063,7 @@ __global__ void __launch_bounds__(256) k_tail_x(T* x, const T* p, const CgState*
     if constexpr (sizeof(T) == 8) al = (T)st->alpha; else al = (T)st->alpha32;
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
          L += (int64_t)gridDim.x * blockDim.x) {
-        long long g = 0;
-        if constexpr (PM != PM_NONE) {
-            const int N = m.N, N3 = N * N * N;
-            const uint32_t e = (uint32_t)(L / N3);
-            const int rem = (int)(L - (int64_t)e * N3);
-            g = node_gid(m, e, rem % N, (rem / N) % N, rem / (N * N));
-        }
-        x[L] = pfma<PM>(al, p[L], x[L], P, pm_key(it, PH_A, g, 1));
+        x[L] = pfma<PM>(al, p[L], x[L], P, pm_key(it, PH_A, global_local_index(m, L), 1));
     }
 }
 

@@ -719,3 +719,68 @@ def test_mca_samples_statistics(ora, mode):
     assert np.abs(mu[:10] / r64.hist[:10] - 1).max() < 1e-5
     h40 = np.array([ora.cg_emulated(m, D, s["G"], s["f"], 30, mode, 40, sd).hist for sd in range(4)])
     assert h40.std(0)[1:10].max() < 1e-3 * sg[1:10].max()
+
+
+# ------------------------------------------------ C7: FP64 scalars in the FP32 solver
+def test_fp32_solver_scalars_are_fp64(ora):
+    """C7 (north_star "FP64 accumulation even in the FP32 solver", reading R11):
+    the mixed FP32 solver forms alpha, beta and h_k in binary64 from the binary64
+    inner products and rounds alpha / beta to binary32 only where they enter the
+    binary32 vector updates (C8).  Pinned by IEEE identities on the trace
+    (Python floats are binary64), by values that are not binary32 numbers, and
+    by the first iterate x_1 = RN32(RN32(alpha_1) f32): a solver with binary32
+    scalars (alpha = RN32(RN32(rtz1) / RN32(pap))) would fail each of them."""
+    m = ora.Mesh(2, 2, 2, 6, jitter=0.1, seed_geom=4, seed_rhs=3)
+    _, _, D = ora.gll(6)
+    s = ora.setup(m, want=("G", "f"))
+    r = ora.cg(m, D, s["G"], s["f"], 30, "fp32")
+    rtz1, beta, alpha, pap, rtr = r.trace.T
+    for k in range(30):
+        assert alpha[k] == rtz1[k] / pap[k]                    # binary64 division
+        assert r.hist[k + 1] == math.sqrt(rtr[k])               # binary64 sqrt
+        if k:
+            assert beta[k] == rtz1[k] / rtz1[k - 1] and rtz1[k] == rtr[k - 1]
+    as32 = lambda v: float(np.float32(v)) == v  # noqa: E731
+    assert not all(as32(v) for v in alpha) and not all(as32(v) for v in beta[1:])
+    assert not all(as32(v) for v in rtr)
+    # the binary32 loop uses RN32(alpha_1): x_1 = RN32(RN32(alpha_1) * f32) (p_1 = r_0 = f32)
+    r1 = ora.cg(m, D, s["G"], s["f"], 1, "fp32")
+    f32 = s["f"].astype(np.float32)
+    a1 = r1.trace[0, 2]
+    assert np.array_equal(r1.x, (np.float32(a1) * f32).astype(np.float32))
+    # the binary32-scalar variant (paper-literal single, R11b) follows another trajectory
+    rs = ora.cg(m, D, s["G"], s["f"], 30, "fp32s")
+    assert not np.array_equal(rs.hist, r.hist)
+
+
+# ------------------------------------------------ NEXT-4: one draw per FP operation
+@pytest.mark.parametrize("mode", ["rr", "mca"])
+def test_mca_draws_per_operation(ora, mode):
+    """each FP operation is perturbed by its own draw.  The pointwise
+    updates of the m copies of a shared node are separate operations, so under
+    RR / MCA the copies of x (and p, r) differ after one iteration, while VPREC
+    (deterministic rounding) keeps every copy bitwise equal; dssum still writes
+    one sum to every copy (C4).  The first iterate, p_1 = fma(0, 0, r_0) with
+    its result perturbed, is x_1 / alpha_1-free: check the copies of x_1."""
+    m = ora.Mesh(2, 2, 2, 5, jitter=0.1, seed_geom=4, seed_rhs=3)
+    _, _, D = ora.gll(5)
+    s = ora.setup(m, want=("G", "f", "gid"))
+    gid = s["gid"].reshape(-1)
+    order = np.argsort(gid, kind="stable")
+    g_sorted = gid[order]
+    first = np.r_[True, g_sorted[1:] != g_sorted[:-1]]
+    grp = np.cumsum(first) - 1
+
+    def spread(x):  # max over nodes of (max - min) over the node's copies
+        v = x.reshape(-1)[order]
+        mx = np.maximum.reduceat(v, np.nonzero(first)[0])
+        mn = np.minimum.reduceat(v, np.nonzero(first)[0])
+        return mx - mn
+
+    e = ora.cg_emulated(m, D, s["G"], s["f"], 3, mode, 23, 5)
+    v = ora.cg_emulated(m, D, s["G"], s["f"], 3, "vprec", 23)
+    assert (spread(v.x) == 0).all()
+    sp = spread(e.x)
+    shared = np.bincount(grp) > 1
+    assert (sp[shared] > 0).mean() > 0.5       # most shared nodes have differing copies
+    assert (sp[~shared] == 0).all()
