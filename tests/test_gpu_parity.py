@@ -276,13 +276,6 @@ def test_full_size_sampled_ax_and_continuity(nbk, ora, cfg):
     assert torch.equal(mx[gid], wf) and torch.equal(mn[gid], wf)
 
 
-def test_c3_cg_first_iterations_bitwise(nbk, ora):
-    """C3 at full size, contract mode, first 5 iterations."""
-    c = nbk.CONFIGS["C3"]
-    args = (c.ex, c.ey, c.ez, c.N, c.jitter, c.seed_geom, c.seed_rhs)
-    _cg_parity(nbk, ora, args, 5, "fp32")
-
-
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_glsc3_special_values(nbk, ora, dtype):
     """glsc3 with +-inf / NaN / huge / subnormal entries: the plain IEEE result
