@@ -481,7 +481,16 @@ nbk_status nbk_load_arrays(nbk_ctx* c, const double* D_host, const double* G_hos
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
     cudaStream_t s = c->stream;
-    if (D_host) NBK_CUDA(c, cudaMemcpyAsync(c->D64, D_host, 8 * c->N * c->N, cudaMemcpyHostToDevice, s));
+    if (D_host) {
+        NBK_CUDA(c, cudaMemcpyAsync(c->D64, D_host, 8 * c->N * c->N, cudaMemcpyHostToDevice, s));
+        for (int q = 0; q < c->N * c->N; ++q) {
+            c->Dh64[q] = D_host[q];
+            c->Dh32[q] = (float)D_host[q];  // RN32 (C11)
+        }
+        // D is a kernel parameter of k_ax2: captured solve graphs hold the old values
+        destroy_graphs(c);
+        for (nbk_ctx* o : c->group) destroy_graphs(o);
+    }
     if (G_host) NBK_CUDA(c, cudaMemcpyAsync(c->G64, G_host, 8 * 6 * c->n, cudaMemcpyHostToDevice, s));
     if (f_host) NBK_CUDA(c, cudaMemcpyAsync(c->f64, f_host, 8 * c->n, cudaMemcpyHostToDevice, s));
     if (D_host || G_host) {  // operator changed

@@ -41,6 +41,8 @@ struct nbk_ctx {
     double *D64 = nullptr, *G64 = nullptr, *f64 = nullptr;
     double *x64 = nullptr, *r64 = nullptr, *p64 = nullptr, *w64 = nullptr;
     float *D32 = nullptr, *G32 = nullptr;
+    double Dh64[256] = {};                // host copies of D (kernel parameter of k_ax2)
+    float Dh32[256] = {};
     float *x32 = nullptr, *r32 = nullptr, *p32 = nullptr, *w32 = nullptr;
     double* dinv64 = nullptr;             // Jacobi: 1 / assembled diag(A) (masked: 1)
     float* dinv32 = nullptr;              // RN32(dinv64) (C11)

@@ -152,6 +152,7 @@ __host__ __device__ constexpr int ax_min_blocks(int N)
 template <typename T>
 struct AxArgs {
     const T* D;        // N*N, D[a*N+b] = l_b'(xi_a)
+    const T* Dh;       // host copy of D (launchers pass it to k_ax2 as a kernel parameter)
     const T* G;        // E*6*N^3
     const T* u;        // input field (plain mode)
     T* w;              // output
@@ -398,6 +399,276 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 // nodes contribute once per node in K_B (bitwise-equal exact sum).
                 const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
                 if (!sxy && !sz) acc.add(dot_term_pm<PM>(wv, ureg[k], 1.0, a.single, P));
+            }
+        }
+    }
+    pdl_launch_dependents();
+    if constexpr (FUSED) {
+        dd v = block_reduce_dd(acc.get());
+        if (threadIdx.x == 0) a.parts[blockIdx.x] = v;
+    }
+}
+
+// ------------------------------------------------------------ K_A, 2 points per thread
+// Register-tiled variant for even N >= 10 (FP32; PM_NONE): thread (i, jj) of an
+// element computes the points (i, j0 = jj, k) and (i, j1 = jj + N/2, k) for all
+// k.  Both points read the same u / ws column (i fixed) in the s-derivative and
+// in the s-part of the transpose, so those N shared-memory loads serve two
+// points; the D[k][*] row of the t-derivative and of the t-transpose is a
+// kernel parameter indexed by compile-time constants (constant-bank operands,
+// no shared-memory traffic).  The pairing (jj, jj + N/2) keeps the G loads and
+// the wr / ws stores of a warp on consecutive words (conflict-free).  Staging,
+// barriers and the canonical evaluation order C1-C5 / C8 are those of k_ax, so
+// the results are bitwise identical.
+template <typename T>
+struct DConst {
+    T v[256];  // D[a*N+b], N <= 16
+};
+
+#ifndef NBK_AX2_EPB10
+#define NBK_AX2_EPB10 2
+#endif
+#ifndef NBK_AX2_EPB12
+#define NBK_AX2_EPB12 1
+#endif
+template <typename T>
+__host__ __device__ constexpr bool ax2_enabled(int N)
+{
+#ifdef NBK_NO_AX2
+    return false;
+#else
+    return sizeof(T) == 4 && (N == 10 || N == 12);
+#endif
+}
+template <typename T>
+__host__ __device__ constexpr int ax2_epb(int N)
+{
+    return N == 10 ? NBK_AX2_EPB10 : (N == 12 ? NBK_AX2_EPB12 : 1);
+}
+template <typename T>
+__host__ __device__ constexpr int ax2_threads(int N)
+{
+    return (N * (N / 2) * ax2_epb<T>(N) + 31) / 32 * 32;
+}
+template <typename T>
+__host__ __device__ constexpr int ax2_smem_bytes(int N)
+{
+    return 7 * ax2_epb<T>(N) * N * N * N * (int)sizeof(T);
+}
+template <typename T>
+__host__ __device__ constexpr int ax2_min_blocks(int N)
+{
+    int by_smem = (232448 - 1024) / (ax2_smem_bytes<T>(N) + 1024 + 2 * N * N * (int)sizeof(T) + 64);
+    int by_thr = 2048 / ax2_threads<T>(N);
+    int m = by_smem < by_thr ? by_smem : by_thr;
+    return m < 1 ? 1 : m;
+}
+
+template <typename T, int N, int FUSED>
+__global__ void __launch_bounds__(ax2_threads<T>(N), ax2_min_blocks<T>(N))
+    k_ax2(AxArgs<T> a, const __grid_constant__ DConst<T> dc)
+{
+    constexpr int N2 = N * N, N3 = N * N * N, H = N / 2, TPE = N * H, EPB = ax2_epb<T>(N);
+    static_assert(N % 2 == 0, "k_ax2 pairs rows j and j + N/2");
+    __shared__ __align__(16) T sD[N2];
+    __shared__ __align__(16) T sDt[N2];
+    __shared__ __align__(8) uint64_t bar[2];   // p / u block, G block
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* sG = reinterpret_cast<T*>(smem_raw);   // EPB*6*N3; wr / ws overwrite the g1 / g2 slots
+    T* sU = sG + EPB * 6 * N3;                // EPB*N3
+
+    const int tid = threadIdx.x;
+    const int el = tid / TPE, q = tid - el * TPE;
+    const int i = q % N, jj = q / N;
+    const int jr[2] = {jj, jj + H};
+    const int64_t e0 = (int64_t)(a.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * EPB;
+    const int64_t e = e0 + el;
+    const int nel = (int)((a.mesh.E - e0) < EPB ? (a.mesh.E - e0) : EPB);
+    const bool valid = el < nel;
+    const T* src_u = FUSED ? a.p : a.u;
+
+    T rreg[FUSED ? 2 : 1][FUSED ? N : 1], xreg[FUSED ? 2 : 1][FUSED ? N : 1];
+    T dreg[FUSED == 2 ? 2 : 1][FUSED == 2 ? N : 1];
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        const uint32_t ubytes = (uint32_t)(nel * N3 * sizeof(T));
+        const uint32_t gbytes = (uint32_t)(nel * 6 * N3 * sizeof(T));
+        if (FUSED && a.p_ready) {
+            mbar_arrive_expect_tx(&bar[0], ubytes);
+            tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
+        }
+        mbar_arrive_expect_tx(&bar[1], gbytes);
+        tma_load_1d(sG, a.G + e0 * 6 * N3, gbytes, &bar[1]);
+        pdl_wait();
+        if (!(FUSED && a.p_ready)) {
+            mbar_arrive_expect_tx(&bar[0], ubytes);
+            tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
+        }
+    }
+    const int64_t eb = e * N3 + i;  // + j N + k N2
+    if constexpr (FUSED) {
+        if (valid && a.p_ready) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    xreg[h][k] = a.x[eb + jr[h] * N + k * N2];
+                    if constexpr (FUSED == 2) dreg[h][k] = __ldg(a.dinv + eb + jr[h] * N + k * N2);
+                }
+        }
+    }
+    pdl_wait();
+    for (int t = tid; t < N2; t += blockDim.x) {
+        T d = a.D[t];
+        sD[t] = d;
+        sDt[(t % N) * N + t / N] = d;
+    }
+    T betaT = 0, alphaT = 0;
+    if constexpr (FUSED) {
+        if constexpr (sizeof(T) == 8) {
+            betaT = (T)a.st->beta;
+            alphaT = (T)a.st->alpha;
+        } else {
+            betaT = (T)a.st->beta32;
+            alphaT = (T)a.st->alpha32;
+        }
+        if (valid) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    rreg[h][k] = a.r[eb + jr[h] * N + k * N2];
+                    if (!a.p_ready) {
+                        xreg[h][k] = a.x[eb + jr[h] * N + k * N2];
+                        if constexpr (FUSED == 2) dreg[h][k] = __ldg(a.dinv + eb + jr[h] * N + k * N2);
+                    }
+                }
+        }
+    }
+    __syncthreads();
+    mbar_wait(&bar[0], 0);
+
+    T* ue = sU + el * N3;
+    T* wre = sG + el * 6 * N3;        // aliases g1
+    T* wse = sG + el * 6 * N3 + N3;   // aliases g2
+
+    // ---- p = fma(beta, p, r), x = fma(alpha_prev, p_prev, x)  (C8, fused)
+    T ureg[2][N];
+    if (valid) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const int o = k * N2 + jr[h] * N + i;
+                T v = ue[o];
+                if constexpr (FUSED) {
+                    const T po = v;
+                    T zk = rreg[h][k];
+                    if constexpr (FUSED == 2) zk = mul_t<T>(rreg[h][k], dreg[h][k]);  // solveM (Jacobi)
+                    v = fma_t<T>(betaT, po, zk);
+                    a.x[e * N3 + o] = fma_t<T>(alphaT, po, xreg[h][k]);
+                    a.p[e * N3 + o] = v;
+                    ue[o] = v;
+                }
+                ureg[h][k] = v;
+            }
+    }
+    if constexpr (FUSED) __syncthreads();
+
+    // ---- gradient (C1), metric (C2), t-part of the transpose (C3: b chain)
+    T b[2][N];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < N; ++k) b[h][k] = 0;
+    if (valid) {
+        const T* Ge = sG + el * 6 * N3 + i;
+        T Dri[N], Drj[2][N];
+        lds_row<T, N>(Dri, sD + i * N);         // D[i][:]
+        lds_row<T, N>(Drj[0], sD + jr[0] * N);  // D[j][:]
+        lds_row<T, N>(Drj[1], sD + jr[1] * N);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            if (k == 0) mbar_wait(&bar[1], 0);
+            T col[N];
+#pragma unroll
+            for (int l = 0; l < N; ++l) col[l] = ue[k * N2 + l * N + i];   // u[k][:][i]
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = jr[h];
+                T urow[N];
+                lds_row<T, N>(urow, ue + k * N2 + j * N);   // u[k][j][:]
+                T ur = 0, us = 0, ut = 0;
+#pragma unroll
+                for (int l = 0; l < N; ++l) ur = fma_t<T>(Dri[l], urow[l], ur);
+#pragma unroll
+                for (int l = 0; l < N; ++l) us = fma_t<T>(Drj[h][l], col[l], us);
+#pragma unroll
+                for (int l = 0; l < N; ++l) ut = fma_t<T>(dc.v[k * N + l], ureg[h][l], ut);
+                const int o = k * N2 + j * N;
+                const T g1 = Ge[0 * N3 + o], g2 = Ge[1 * N3 + o], g3 = Ge[2 * N3 + o];
+                const T g4 = Ge[3 * N3 + o], g5 = Ge[4 * N3 + o], g6 = Ge[5 * N3 + o];
+                T wr = mul_t<T>(g1, ur);
+                wr = fma_t<T>(g2, us, wr);
+                wr = fma_t<T>(g3, ut, wr);
+                T ws = mul_t<T>(g2, ur);
+                ws = fma_t<T>(g4, us, ws);
+                ws = fma_t<T>(g5, ut, ws);
+                T wt = mul_t<T>(g3, ur);
+                wt = fma_t<T>(g5, us, wt);
+                wt = fma_t<T>(g6, ut, wt);
+                wre[o + i] = wr;   // own slots of g1 / g2, dead after the reads above
+                wse[o + i] = ws;
+#pragma unroll
+                for (int kk = 0; kk < N; ++kk) b[h][kk] = fma_t<T>(dc.v[k * N + kk], wt, b[h][kk]);
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- r/s part of the transpose (C3: a chain), w = a + b, mask, pap
+    acc_t acc;
+    if (valid) {
+        const ElemCoord ec = elem_coord(a.mesh, (uint32_t)e);
+        const int n1 = N - 1;
+        const bool mz0 = ec.azg == 0, mz1 = ec.azg == a.mesh.ezg - 1;
+        T Dci[N], Dcj[2][N];
+        lds_row<T, N>(Dci, sDt + i * N);          // D[:][i]
+        lds_row<T, N>(Dcj[0], sDt + jr[0] * N);   // D[:][j]
+        lds_row<T, N>(Dcj[1], sDt + jr[1] * N);
+        bool mxy[2], sxy[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = jr[h];
+            mxy[h] = (i == 0 && ec.ax == 0) || (i == n1 && ec.ax == a.mesh.ex - 1) ||
+                     (j == 0 && ec.ay == 0) || (j == n1 && ec.ay == a.mesh.ey - 1);
+            sxy[h] = (i == 0 && ec.ax > 0) || (i == n1 && ec.ax < a.mesh.ex - 1) ||
+                     (j == 0 && ec.ay > 0) || (j == n1 && ec.ay < a.mesh.ey - 1);
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            T col[N];
+#pragma unroll
+            for (int l = 0; l < N; ++l) col[l] = wse[k * N2 + l * N + i];   // ws[k][:][i]
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = jr[h];
+                T wrow[N];
+                lds_row<T, N>(wrow, wre + k * N2 + j * N);  // wr[k][j][:]
+                T s = 0;
+#pragma unroll
+                for (int l = 0; l < N; ++l) s = fma_t<T>(Dci[l], wrow[l], s);
+#pragma unroll
+                for (int l = 0; l < N; ++l) s = fma_t<T>(Dcj[h][l], col[l], s);
+                T wv = add_t<T>(s, b[h][k]);
+                const bool masked = mxy[h] || (k == 0 && mz0) || (k == n1 && mz1);
+                if (a.mask && masked) wv = 0;   // C5: assign +0
+                a.w[eb + j * N + k * N2] = wv;
+                if constexpr (FUSED) {
+                    const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
+                    if (!sxy[h] && !sz) acc.add(dot_term(wv, ureg[h][k], 1.0, a.single != 0));
+                }
             }
         }
     }

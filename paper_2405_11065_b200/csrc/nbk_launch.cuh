@@ -68,6 +68,17 @@ template <typename T, int N, int FUSED, int PM = PM_NONE>
 inline cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
                                bool pdl = false)
 {
+    if constexpr (PM == PM_NONE && ax2_enabled<T>(N)) {  // 2 points per thread (N = 10, 12)
+        constexpr int EPB2 = ax2_epb<T>(N);
+        const size_t smem2 = (size_t)ax2_smem_bytes<T>(N);
+        if (attr_only)
+            return cudaFuncSetAttribute(k_ax2<T, N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem2);
+        DConst<T> dc{};
+        for (int q = 0; q < N * N; ++q) dc.v[q] = a.Dh[q];
+        const unsigned grid2 = (unsigned)((a.mesh.E + EPB2 - 1) / EPB2);
+        return launch_k(k_ax2<T, N, FUSED>, grid2, ax2_threads<T>(N), smem2, s, pdl, a, dc);
+    }
     constexpr int EPB = ax_epb<T>(N);
     const size_t smem = (size_t)ax_smem_bytes<T>(N);
     if (attr_only)
@@ -333,6 +344,7 @@ inline AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
 {
     AxArgs<T> a{};
     a.D = D;
+    if constexpr (sizeof(T) == 8) a.Dh = (const T*)c->Dh64; else a.Dh = (const T*)c->Dh32;
     a.G = G;
     a.mesh = c->view;
     a.st = c->st;
@@ -340,10 +352,11 @@ inline AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
     return a;
 }
 
-template <typename T>
+template <typename T, int PM = PM_NONE>
 inline int ax_blocks_n(int64_t E, int N)
 {
-#define EPBN(n) (int)((E + ax_epb<T>(n) - 1) / ax_epb<T>(n))
+#define EPBN(n) (int)((PM == PM_NONE && ax2_enabled<T>(n)) ? (E + ax2_epb<T>(n) - 1) / ax2_epb<T>(n) \
+                                        : (E + ax_epb<T>(n) - 1) / ax_epb<T>(n))
     NBK_SWITCH_N(N, EPBN)
 #undef EPBN
 }
@@ -414,7 +427,7 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         if (FUSED) {
             d.p = p[q];
             d.parts = c->parts;
-            d.nA = ax_blocks_n<T>(c->E, c->N);
+            d.nA = ax_blocks_n<T, PM>(c->E, c->N);
             d.fin = t.multi ? 0 : 1;
         }
         if ((e = launch_dssum<T, FUSED, PM>(d, s, pdl && !t.multi)) != cudaSuccess) return e;
@@ -429,8 +442,8 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         f.single = single;
         if (FUSED) {
             f.p = p[q];
-            f.nprev = ax_blocks_n<T>(c->E, c->N) + dssum_grid_t<T, FUSED, PM>((int)c->ntiles, c->tile_smem);
-            f.nskip = ax_blocks_n<T>(c->E, c->N);
+            f.nprev = ax_blocks_n<T, PM>(c->E, c->N) + dssum_grid_t<T, FUSED, PM>((int)c->ntiles, c->tile_smem);
+            f.nskip = ax_blocks_n<T, PM>(c->E, c->N);
         }
         const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
         k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);

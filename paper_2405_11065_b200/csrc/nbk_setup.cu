@@ -637,6 +637,10 @@ cudaError_t setup_device(nbk_ctx* ctx, const Layout& L)
     GeoParams gp{};
     double D[256];
     gll_host(ctx->N, gp.xi, gp.rho, D);
+    for (int q = 0; q < ctx->N * ctx->N; ++q) {
+        ctx->Dh64[q] = D[q];
+        ctx->Dh32[q] = (float)D[q];  // RN32, as k_downcast (C11)
+    }
     gp.N = ctx->N;
     gp.jitter = ctx->mesh.jitter;
     gp.seed_geom = ctx->mesh.seed_geom;
