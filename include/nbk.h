@@ -215,7 +215,15 @@ nbk_status nbk_cg_solve_host(nbk_ctx* ctx, const double* f_host, int32_t niter,
  * host memory, e_local*N^3 doubles.  Synchronous. */
 nbk_status nbk_get_solution(nbk_ctx* ctx, double* x_host);
 
-/* Device pointer of the last solution in its native precision (do not free). */
+/* Device pointer of the last solution in its native precision (do not free).
+ * The library stores its CG vectors (x, r, p, w, f, dinv) per element in the
+ * split layout, not in natural order: slots [0, (N-2)^3) hold the element's
+ * interior points (i, j, k in 1..N-2, natural order), slots [(N-2)^3, N^3) its
+ * boundary points in natural order (so dssum touches only the compact tail of
+ * each element).  Every host transfer (nbk_get_solution, nbk_load_arrays,
+ * nbk_cg_solve_host, the precond calls) and every public device call
+ * (nbk_ax_apply, nbk_dssum, nbk_glsc3) uses natural order; only this pointer
+ * exposes the internal layout. */
 nbk_status nbk_solution_ptr(nbk_ctx* ctx, nbk_precision precision, void** x_dev);
 
 /* Precision emulation of the following NBK_VPREC solves (SURVEY 8(f) NEXT-4,

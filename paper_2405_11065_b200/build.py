@@ -48,13 +48,16 @@ def _stale() -> bool:
     return False
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Build libnbk.so (or, for A/B experiments, a variant at `out` with
+    NBK_EXTRA_FLAGS; load it with NBK_LIB=<path>)."""
+    if out is None and not force and not _stale():
         return LIB
+    target = out or LIB
     objs, procs = [], []
     extra = os.environ.get("NBK_EXTRA_FLAGS", "").split()  # tuning experiments only
     for src, stem, defs in SOURCES:  # the translation units compile in parallel
-        obj = os.path.join(CSRC, stem + ".o")
+        obj = os.path.join(CSRC, stem + ".o") if out is None else out + "." + stem + ".o"
         cmd = [NVCC, *ARCH, *FLAGS, *NCCL_INC, *NCCL_DEF, *defs, *extra, "-c", os.path.join(CSRC, src),
                "-o", obj]
         procs.append((stem, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
@@ -66,15 +69,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {stem}")
         if verbose:
             sys.stderr.write(err)
-        with open(os.path.join(CSRC, stem + ".ptxas.log"), "w") as fh:
+        with open(obj[:-2] + ".ptxas.log", "w") as fh:
             fh.write(err)
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=o))

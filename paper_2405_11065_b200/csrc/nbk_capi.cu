@@ -69,7 +69,7 @@ cudaError_t enqueue_final_check(const Team& t, std::string& err)
         vt[q].r = c->r64; vt[q].w = c->w64; vt[q].f = c->f64;
     }
     cudaError_t e;
-    if ((e = ax_team<double>(t, x64, w64, NBK_AX_DSSUM | NBK_AX_MASK, false, err)) != cudaSuccess) return e;
+    if ((e = ax_team<double>(t, x64, w64, NBK_AX_DSSUM | NBK_AX_MASK, false, err, true)) != cudaSuccess) return e;
     return vec_team<double, VEC_TRUE>(t, vt, false, err);
 }
 
@@ -144,9 +144,10 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
 }
 
 // glsc3 over a team (synchronous); result identical on every member.
+// natural: a, b are public natural-order arrays (else SL vectors of the library)
 template <typename T>
 static nbk_status glsc3_team(const Team& t, const std::vector<const T*>& a, const std::vector<const T*>& b,
-                             double* out, int single = 0)
+                             double* out, int single = 0, bool natural = true)
 {
     nbk_ctx* c0 = t.m[0];
     std::vector<VecArgs<T>> v(t.m.size());
@@ -154,6 +155,7 @@ static nbk_status glsc3_team(const Team& t, const std::vector<const T*>& a, cons
         v[q] = vec_args<T>(t.m[q]);
         v[q].a = a[q]; v[q].b = b[q];
         v[q].single = single;
+        v[q].natural = natural ? 1 : 0;
     }
     std::string err;
     cudaError_t e = vec_team<T, VEC_DOT>(t, v, false, err);
@@ -189,7 +191,7 @@ static nbk_status refresh_h0(const Team& t)
     std::vector<const double*> f(t.m.size());
     for (size_t q = 0; q < t.m.size(); ++q) f[q] = t.m[q]->f64;
     double dot = 0.0;
-    nbk_status st = glsc3_team<double>(t, f, f, &dot);
+    nbk_status st = glsc3_team<double>(t, f, f, &dot, 0, false);   // f64 is an SL vector
     if (st != NBK_OK) return st;
     for (nbk_ctx* c : t.m) {
         c->h0_64 = std::sqrt(dot);
@@ -296,6 +298,29 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
         result->kC_ms = kc;
     }
     return hs.defect ? fail(c, NBK_EDEFECT, "CG defect: pap <= 0 or non-finite scalar") : NBK_OK;
+}
+
+// Public dssum of natural-order fields: permute into the member's SL scratch,
+// sum with the SL plan, permute back, mask (C5) in natural order.
+template <typename T>
+static cudaError_t dssum_natural(const Team& t, void* const* f_dev, int32_t apply_mask, std::string& err)
+{
+    const size_t P = t.m.size();
+    cudaError_t e;
+    std::vector<T*> w(P);
+    for (size_t q = 0; q < P; ++q) {
+        w[q] = sl_scratch<T>(t.m[q]);
+        if ((e = perm_sl<T>(t.m[q], w[q], (const T*)f_dev[q], true, t.s)) != cudaSuccess) return e;
+    }
+    if ((e = dssum_team<T, false>(t, w, {}, 0, false, err)) != cudaSuccess) return e;
+    for (size_t q = 0; q < P; ++q) {
+        if ((e = perm_sl<T>(t.m[q], (T*)f_dev[q], w[q], false, t.s)) != cudaSuccess) return e;
+        if (apply_mask) {
+            k_mask<T><<<vec_grid(t.m[q]->n), 256, 0, t.s>>>((T*)f_dev[q], t.m[q]->view);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
 }
 
 // ================================================================== ABI
@@ -487,12 +512,15 @@ nbk_status nbk_load_arrays(nbk_ctx* c, const double* D_host, const double* G_hos
             c->Dh64[q] = D_host[q];
             c->Dh32[q] = (float)D_host[q];  // RN32 (C11)
         }
-        // D is a kernel parameter of k_ax2: captured solve graphs hold the old values
+        // D is a kernel parameter of k_ax: captured solve graphs hold the old values
         destroy_graphs(c);
         for (nbk_ctx* o : c->group) destroy_graphs(o);
     }
     if (G_host) NBK_CUDA(c, cudaMemcpyAsync(c->G64, G_host, 8 * 6 * c->n, cudaMemcpyHostToDevice, s));
-    if (f_host) NBK_CUDA(c, cudaMemcpyAsync(c->f64, f_host, 8 * c->n, cudaMemcpyHostToDevice, s));
+    if (f_host) {  // natural order on the host, split layout on the device
+        NBK_CUDA(c, cudaMemcpyAsync(c->w64, f_host, 8 * c->n, cudaMemcpyHostToDevice, s));
+        NBK_CUDA(c, perm_sl<double>(c, c->f64, c->w64, true, s));
+    }
     if (D_host || G_host) {  // operator changed
         nbk_status st = refresh_fp32(c);
         if (st != NBK_OK) return st;
@@ -508,7 +536,10 @@ nbk_status nbk_get_arrays(nbk_ctx* c, double* D_host, double* G_host, double* f_
     cudaStream_t s = c->stream;
     if (D_host) NBK_CUDA(c, cudaMemcpyAsync(D_host, c->D64, 8 * c->N * c->N, cudaMemcpyDeviceToHost, s));
     if (G_host) NBK_CUDA(c, cudaMemcpyAsync(G_host, c->G64, 8 * 6 * c->n, cudaMemcpyDeviceToHost, s));
-    if (f_host) NBK_CUDA(c, cudaMemcpyAsync(f_host, c->f64, 8 * c->n, cudaMemcpyDeviceToHost, s));
+    if (f_host) {
+        NBK_CUDA(c, perm_sl<double>(c, c->w64, c->f64, false, s));
+        NBK_CUDA(c, cudaMemcpyAsync(f_host, c->w64, 8 * c->n, cudaMemcpyDeviceToHost, s));
+    }
     NBK_CUDA(c, cudaStreamSynchronize(s));
     return NBK_OK;
 }
@@ -560,21 +591,11 @@ static nbk_status dssum_team_abi(const Team& t, void* const* f_dev, int32_t appl
     std::string err;
     cudaError_t e;
     if (prec == NBK_FP64) {
-        std::vector<double*> w(P);
-        for (size_t q = 0; q < P; ++q) w[q] = (double*)f_dev[q];
-        e = dssum_team<double, false>(t, w, {}, apply_mask ? 1 : 0, false, err);
-        for (size_t q = 0; e == cudaSuccess && apply_mask && q < P; ++q) {
-            k_mask<double><<<vec_grid(t.m[q]->n), 256, 0, t.s>>>(w[q], t.m[q]->view);
-            e = cudaGetLastError();
-        }
+        e = dssum_natural<double>(t, f_dev, apply_mask, err);
     } else if (prec == NBK_FP32) {
-        std::vector<float*> w(P);
-        for (size_t q = 0; q < P; ++q) w[q] = (float*)f_dev[q];
-        e = dssum_team<float, false>(t, w, {}, apply_mask ? 1 : 0, false, err);
-        for (size_t q = 0; e == cudaSuccess && apply_mask && q < P; ++q) {
-            k_mask<float><<<vec_grid(t.m[q]->n), 256, 0, t.s>>>(w[q], t.m[q]->view);
-            e = cudaGetLastError();
-        }
+        for (size_t q = 0; q < P; ++q)
+            if (!t.m[q]->w32) return fail(c, NBK_ESTATE, "context has no FP32 arrays");
+        e = dssum_natural<float>(t, f_dev, apply_mask, err);
     } else {
         return fail(c, NBK_EINVAL, "bad precision");
     }
@@ -662,7 +683,8 @@ nbk_status nbk_set_precond(nbk_ctx* c, int32_t precond)
 nbk_status nbk_load_precond(nbk_ctx* c, const double* dinv_host)
 {
     if (!c || !dinv_host) return fail(c, NBK_EINVAL, "NULL argument");
-    NBK_CUDA(c, cudaMemcpyAsync(c->dinv64, dinv_host, 8 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
+    NBK_CUDA(c, cudaMemcpyAsync(c->w64, dinv_host, 8 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
+    NBK_CUDA(c, perm_sl<double>(c, c->dinv64, c->w64, true, c->stream));
     if (c->dinv32) {
         k_downcast<<<vec_grid(c->n), 256, 0, c->stream>>>(c->dinv32, c->dinv64, c->n);
         NBK_CUDA(c, cudaGetLastError());
@@ -686,7 +708,8 @@ nbk_status nbk_get_precond(nbk_ctx* c, double* dinv_host)
     }
     nbk_status st = refresh_dinv(t);
     if (st != NBK_OK) return st;
-    NBK_CUDA(c, cudaMemcpyAsync(dinv_host, c->dinv64, 8 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+    NBK_CUDA(c, perm_sl<double>(c, c->w64, c->dinv64, false, c->stream));
+    NBK_CUDA(c, cudaMemcpyAsync(dinv_host, c->w64, 8 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
     NBK_CUDA(c, cudaStreamSynchronize(c->stream));
     return NBK_OK;
 }
@@ -713,13 +736,15 @@ nbk_status nbk_cg_solve_host(nbk_ctx* c, const double* f_host, int32_t niter, nb
 {
     if (!c) return fail(nullptr, NBK_EINVAL, "ctx is NULL");
     if (f_host) {
-        NBK_CUDA(c, cudaMemcpyAsync(c->f64, f_host, 8 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
+        NBK_CUDA(c, cudaMemcpyAsync(c->w64, f_host, 8 * (size_t)c->n, cudaMemcpyHostToDevice, c->stream));
+        NBK_CUDA(c, perm_sl<double>(c, c->f64, c->w64, true, c->stream));
         c->h0_dirty = 1;  // new RHS: new h0 for the relative residual (operator unchanged)
     }
     nbk_status st = nbk_cg_solve(c, niter, prec, hist_host, nullptr, result);
     if (st != NBK_OK && st != NBK_EDEFECT) return st;
     if (x_host) {
-        NBK_CUDA(c, cudaMemcpyAsync(x_host, c->x64, 8 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+        NBK_CUDA(c, perm_sl<double>(c, c->w64, c->x64, false, c->stream));
+        NBK_CUDA(c, cudaMemcpyAsync(x_host, c->w64, 8 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
         NBK_CUDA(c, cudaStreamSynchronize(c->stream));
     }
     return st;
@@ -729,7 +754,8 @@ nbk_status nbk_get_solution(nbk_ctx* c, double* x_host)
 {
     if (!c || !x_host) return fail(c, NBK_EINVAL, "NULL argument");
     if (c->last_solved_precision < 0) return fail(c, NBK_ESTATE, "no solve yet");
-    NBK_CUDA(c, cudaMemcpyAsync(x_host, c->x64, 8 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
+    NBK_CUDA(c, perm_sl<double>(c, c->w64, c->x64, false, c->stream));
+    NBK_CUDA(c, cudaMemcpyAsync(x_host, c->w64, 8 * (size_t)c->n, cudaMemcpyDeviceToHost, c->stream));
     NBK_CUDA(c, cudaStreamSynchronize(c->stream));
     return NBK_OK;
 }

@@ -214,6 +214,84 @@ __device__ __forceinline__ int multiplicity(const MeshView& m, const ElemCoord& 
     return mx * my * mz;
 }
 
+// ------------------------------------------------------------ split layout
+// Element-local storage order of the CG vectors x, r, p, w, f and dinv inside
+// the library ("split layout", SL; G and the public-API arrays stay natural,
+// i fastest).  Slots [0, I^3) of an element (I = N - 2) hold its interior
+// points in natural order; slots [I^3, N^3) its boundary points, also in
+// natural order: the k = 0 face (N^2 points), then per inner plane k = 1..N-2
+// its ring of R = 4 (N - 1) points (row j = 0, the pairs i = 0 / i = N-1 of
+// rows 1..N-2, row j = N-1), then the k = N-1 face.  Every copy of a shared
+// node is a boundary point, so dssum reads and writes only the compact tail of
+// each element (whole 32-byte sectors) instead of every sector the stride-N
+// x-face points of the natural order touch.
+__host__ __device__ __forceinline__ int sl_slot(int N, int i, int j, int k)
+{
+    const int I = N - 2, n1 = N - 1;
+    if (i > 0 && i < n1 && j > 0 && j < n1 && k > 0 && k < n1) return ((k - 1) * I + (j - 1)) * I + (i - 1);
+    const int B = I * I * I, R = 4 * n1;
+    if (k == 0) return B + j * N + i;
+    if (k == n1) return B + N * N + (N - 2) * R + j * N + i;
+    int r;
+    if (j == 0) r = i;
+    else if (j == n1) r = N + 2 * (N - 2) + i;
+    else r = N + 2 * (j - 1) + (i == n1 ? 1 : 0);
+    return B + N * N + (k - 1) * R + r;
+}
+// Inverse: the natural (i, j, k) of slot s.
+__host__ __device__ __forceinline__ void sl_point(int N, int s, int& i, int& j, int& k)
+{
+    const int I = N - 2, n1 = N - 1, B = I * I * I, R = 4 * n1;
+    if (s < B) {
+        i = 1 + s % I;
+        j = 1 + (s / I) % I;
+        k = 1 + s / (I * I);
+        return;
+    }
+    int f = s - B;
+    if (f < N * N) { i = f % N; j = f / N; k = 0; return; }
+    f -= N * N;
+    if (f < (N - 2) * R) {
+        k = 1 + f / R;
+        int r = f - (k - 1) * R;
+        if (r < N) { i = r; j = 0; }
+        else if (r < N + 2 * (N - 2)) { r -= N; j = 1 + r / 2; i = (r & 1) ? n1 : 0; }
+        else { i = r - N - 2 * (N - 2); j = n1; }
+        return;
+    }
+    f -= (N - 2) * R;
+    i = f % N; j = f / N; k = n1;
+}
+// First SL slot of the k = 0 or the k = N-1 face (N^2 slots in natural (j, i) order).
+__host__ __device__ __forceinline__ int sl_plane(int N, int k)
+{
+    const int I = N - 2;
+    return I * I * I + (k == 0 ? 0 : N * N + (N - 2) * 4 * (N - 1));
+}
+// Per-thread slot bases of column (i, j): slot(k) = k == 0 ? b0 : k == N-1 ? b1 : bm + (k-1) st.
+struct SlCol {
+    int b0, b1, bm, st;
+    __host__ __device__ __forceinline__ int at(int N, int k) const
+    {
+        return k == 0 ? b0 : (k == N - 1 ? b1 : bm + (k - 1) * st);
+    }
+};
+__host__ __device__ __forceinline__ SlCol sl_col(int N, int i, int j)
+{
+    SlCol c;
+    const int I = N - 2, n1 = N - 1, B = I * I * I, R = 4 * n1;
+    c.b0 = B + j * N + i;
+    c.b1 = B + N * N + (N - 2) * R + j * N + i;
+    if (i > 0 && i < n1 && j > 0 && j < n1) {
+        c.bm = (j - 1) * I + (i - 1);
+        c.st = I * I;
+    } else {
+        c.bm = N > 2 ? sl_slot(N, i, j, 1) : 0;
+        c.st = R;
+    }
+    return c;
+}
+
 // c = 1/m is exact (m in {1,2,4,8}).
 __device__ __forceinline__ double inv_mult(int m)
 {

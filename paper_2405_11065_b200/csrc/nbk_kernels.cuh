@@ -152,7 +152,7 @@ __host__ __device__ constexpr int ax_min_blocks(int N)
 template <typename T>
 struct AxArgs {
     const T* D;        // N*N, D[a*N+b] = l_b'(xi_a)
-    const T* Dh;       // host copy of D (launchers pass it to k_ax2 as a kernel parameter)
+    const T* Dh;       // host copy of D (the launchers pass it to k_ax as a DConst parameter)
     const T* G;        // E*6*N^3
     const T* u;        // input field (plain mode)
     T* w;              // output
@@ -169,6 +169,16 @@ struct AxArgs {
     int mask;          // assign +0 to Dirichlet points of w
     int rev;           // sweep the element tiles in reverse order (L2 reuse, see k_vec)
     int p_ready;       // fused: p is final before the PDL wait (CG iterations >= 2)
+    int in_sl, out_sl; // plain ax: u / w in the split layout (SL) instead of natural order
+                       // (the fused CG step always works on SL vectors)
+};
+
+// D as a kernel parameter: k_ax reads D[k][*] (t-derivative, t-transpose) with
+// compile-time indices, i.e. as constant-bank operands of the FMAs, not from
+// shared memory.
+template <typename T>
+struct DConst {
+    T v[256];  // D[a*N+b], N <= 16
 };
 
 // ---------------------------------------------------------------- K_A
@@ -176,7 +186,7 @@ struct AxArgs {
 // step (p = beta p + z, z = RN(r * dinv) formed here: S:376-384, T1 line 2).
 template <typename T, int N, int FUSED, int PM = PM_NONE>
 __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
-    k_ax(AxArgs<T> a)
+    k_ax(AxArgs<T> a, const __grid_constant__ DConst<T> dc)
 {
     // PM: every operation goes through the emulation (NEXT-4); op numbers per point:
     // 0 p, 1 x (these two keyed by the global node), 2.. ur, 2+N.. us, 2+2N.. ut,
@@ -231,10 +241,11 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
         }
         if constexpr (FUSED) {  // x and dinv are final too (x: previous K_A)
             if (valid && a.p_ready) {
+                const SlCol cs = sl_col(N, i, j);
 #pragma unroll
                 for (int k = 0; k < N; ++k) {
-                    xreg[k] = a.x[e * N3 + ij + k * N2];
-                    if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + e * N3 + ij + k * N2);
+                    xreg[k] = a.x[e * N3 + cs.at(N, k)];
+                    if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + e * N3 + cs.at(N, k));
                 }
             }
         }
@@ -253,10 +264,15 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
         sDt[(q % N) * N + q / N] = d;
     }
 
-    const int64_t base = e * N3 + ij;
+    const int64_t base = e * N3 + ij;   // natural index of (i, j, 0)
     const long long goff = (long long)a.mesh.z0 * a.mesh.ex * a.mesh.ey * N3;  // global local index
     auto key = [&](int kk, int o) { return pm_key(a.it, PH_A, goff + base + (long long)kk * N2, o); };
     (void)key;
+    // storage of the thread's column (i, j, *): SL slots (CG vectors) or natural
+    const SlCol cs = sl_col(N, i, j);
+    const bool isl = FUSED || a.in_sl, osl = FUSED || a.out_sl;
+    auto gin = [&](int kk) -> int64_t { return isl ? e * N3 + cs.at(N, kk) : base + (int64_t)kk * N2; };
+    auto gout = [&](int kk) -> int64_t { return osl ? e * N3 + cs.at(N, kk) : base + (int64_t)kk * N2; };
     T betaT = 0, alphaT = 0;
     if constexpr (FUSED) {
         if constexpr (sizeof(T) == 8) {
@@ -270,10 +286,10 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             const bool early = TMA && a.p_ready;
 #pragma unroll
             for (int k = 0; k < N; ++k) {
-                rreg[k] = a.r[base + k * N2];
+                rreg[k] = a.r[gin(k)];
                 if (!early) {
-                    xreg[k] = a.x[base + k * N2];
-                    if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + base + k * N2);
+                    xreg[k] = a.x[gin(k)];
+                    if constexpr (FUSED == 2) dreg[k] = __ldg(a.dinv + gin(k));
                 }
             }
         }
@@ -286,25 +302,33 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     T* wse = STAGE ? sG + el * 6 * N3 + N3 : sW + (EPB + el) * N3;  // aliases g2
 
     // ---- p = fma(beta, p, r), x = fma(alpha_prev, p_prev, x)  (C8, fused)
+    // The staged block is in the storage order of the source: SL (CG vectors)
+    // is read per column and re-stored in natural order for the derivatives.
     T ureg[N];
     if (valid) {
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            T v = ue[k * N2 + ij];
+            T v = ue[isl ? cs.at(N, k) : k * N2 + ij];
             if constexpr (FUSED) {
                 const T po = v;
                 T zk = rreg[k];
                 if constexpr (FUSED == 2) zk = mul_t<T>(rreg[k], dreg[k]);  // solveM (Jacobi)
-                const long long gk = goff + base + (long long)k * N2;  // emulation key: local index
+                const long long gk = goff + base + (long long)k * N2;  // emulation key: natural local index
                 v = pfma<PM>(betaT, po, zk, P, pm_key(a.it, PH_A, gk, 0));
-                a.x[base + k * N2] = pfma<PM>(alphaT, po, xreg[k], P, pm_key(a.it, PH_A, gk, 1));
-                a.p[base + k * N2] = v;
-                ue[k * N2 + ij] = v;
+                a.x[gin(k)] = pfma<PM>(alphaT, po, xreg[k], P, pm_key(a.it, PH_A, gk, 1));
+                a.p[gin(k)] = v;
             }
             ureg[k] = v;
         }
     }
-    if constexpr (FUSED) __syncthreads();
+    if (isl) {
+        __syncthreads();  // every SL value of the block has been read
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) ue[k * N2 + ij] = ureg[k];
+        }
+        __syncthreads();
+    }
 
     // D rows / columns of this thread: D[i][l], D[j][l] (gradient) and
     // D[l][i], D[l][j] (transpose), in registers when they fit.
@@ -332,7 +356,12 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             }
             T urow[N], Dk[N];
             lds_row<T, N>(urow, ue + k * N2 + j * N);   // u[k][j][:]
-            lds_row<T, N>(Dk, sD + k * N);              // D[k][:] (broadcast)
+#ifdef NBK_D_SMEM
+            lds_row<T, N>(Dk, sD + k * N);   // D[k][:] (broadcast)
+#else
+#pragma unroll
+            for (int l = 0; l < N; ++l) Dk[l] = dc.v[k * N + l];   // D[k][:] (kernel parameter)
+#endif
             T ur = 0, us = 0, ut = 0;
 #pragma unroll
             for (int l = 0; l < N; ++l) ur = pfma<PM>(Dri[l], urow[l], ur, P, key(k, 2 + l));
@@ -393,282 +422,12 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             T wv = padd<PM>(s, b[k], P, key(k, 11 + 6 * N));
             const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
             if (a.mask && masked) wv = 0;   // C5: assign +0
-            a.w[base + k * N2] = wv;
+            a.w[gout(k)] = wv;
             if constexpr (FUSED) {
                 // element-interior points (m == 1) contribute w p c here; shared
                 // nodes contribute once per node in K_B (bitwise-equal exact sum).
                 const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
                 if (!sxy && !sz) acc.add(dot_term_pm<PM>(wv, ureg[k], 1.0, a.single, P));
-            }
-        }
-    }
-    pdl_launch_dependents();
-    if constexpr (FUSED) {
-        dd v = block_reduce_dd(acc.get());
-        if (threadIdx.x == 0) a.parts[blockIdx.x] = v;
-    }
-}
-
-// ------------------------------------------------------------ K_A, 2 points per thread
-// Register-tiled variant for even N >= 10 (FP32; PM_NONE): thread (i, jj) of an
-// element computes the points (i, j0 = jj, k) and (i, j1 = jj + N/2, k) for all
-// k.  Both points read the same u / ws column (i fixed) in the s-derivative and
-// in the s-part of the transpose, so those N shared-memory loads serve two
-// points; the D[k][*] row of the t-derivative and of the t-transpose is a
-// kernel parameter indexed by compile-time constants (constant-bank operands,
-// no shared-memory traffic).  The pairing (jj, jj + N/2) keeps the G loads and
-// the wr / ws stores of a warp on consecutive words (conflict-free).  Staging,
-// barriers and the canonical evaluation order C1-C5 / C8 are those of k_ax, so
-// the results are bitwise identical.
-template <typename T>
-struct DConst {
-    T v[256];  // D[a*N+b], N <= 16
-};
-
-#ifndef NBK_AX2_EPB10
-#define NBK_AX2_EPB10 2
-#endif
-#ifndef NBK_AX2_EPB12
-#define NBK_AX2_EPB12 1
-#endif
-template <typename T>
-__host__ __device__ constexpr bool ax2_enabled(int N)
-{
-#ifdef NBK_NO_AX2
-    return false;
-#else
-    return sizeof(T) == 4 && (N == 10 || N == 12);
-#endif
-}
-template <typename T>
-__host__ __device__ constexpr int ax2_epb(int N)
-{
-    return N == 10 ? NBK_AX2_EPB10 : (N == 12 ? NBK_AX2_EPB12 : 1);
-}
-template <typename T>
-__host__ __device__ constexpr int ax2_threads(int N)
-{
-    return (N * (N / 2) * ax2_epb<T>(N) + 31) / 32 * 32;
-}
-template <typename T>
-__host__ __device__ constexpr int ax2_smem_bytes(int N)
-{
-    return 7 * ax2_epb<T>(N) * N * N * N * (int)sizeof(T);
-}
-template <typename T>
-__host__ __device__ constexpr int ax2_min_blocks(int N)
-{
-    int by_smem = (232448 - 1024) / (ax2_smem_bytes<T>(N) + 1024 + 2 * N * N * (int)sizeof(T) + 64);
-    int by_thr = 2048 / ax2_threads<T>(N);
-    int m = by_smem < by_thr ? by_smem : by_thr;
-    return m < 1 ? 1 : m;
-}
-
-template <typename T, int N, int FUSED>
-__global__ void __launch_bounds__(ax2_threads<T>(N), ax2_min_blocks<T>(N))
-    k_ax2(AxArgs<T> a, const __grid_constant__ DConst<T> dc)
-{
-    constexpr int N2 = N * N, N3 = N * N * N, H = N / 2, TPE = N * H, EPB = ax2_epb<T>(N);
-    static_assert(N % 2 == 0, "k_ax2 pairs rows j and j + N/2");
-    __shared__ __align__(16) T sD[N2];
-    __shared__ __align__(16) T sDt[N2];
-    __shared__ __align__(8) uint64_t bar[2];   // p / u block, G block
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T* sG = reinterpret_cast<T*>(smem_raw);   // EPB*6*N3; wr / ws overwrite the g1 / g2 slots
-    T* sU = sG + EPB * 6 * N3;                // EPB*N3
-
-    const int tid = threadIdx.x;
-    const int el = tid / TPE, q = tid - el * TPE;
-    const int i = q % N, jj = q / N;
-    const int jr[2] = {jj, jj + H};
-    const int64_t e0 = (int64_t)(a.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * EPB;
-    const int64_t e = e0 + el;
-    const int nel = (int)((a.mesh.E - e0) < EPB ? (a.mesh.E - e0) : EPB);
-    const bool valid = el < nel;
-    const T* src_u = FUSED ? a.p : a.u;
-
-    T rreg[FUSED ? 2 : 1][FUSED ? N : 1], xreg[FUSED ? 2 : 1][FUSED ? N : 1];
-    T dreg[FUSED == 2 ? 2 : 1][FUSED == 2 ? N : 1];
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        const uint32_t ubytes = (uint32_t)(nel * N3 * sizeof(T));
-        const uint32_t gbytes = (uint32_t)(nel * 6 * N3 * sizeof(T));
-        if (FUSED && a.p_ready) {
-            mbar_arrive_expect_tx(&bar[0], ubytes);
-            tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
-        }
-        mbar_arrive_expect_tx(&bar[1], gbytes);
-        tma_load_1d(sG, a.G + e0 * 6 * N3, gbytes, &bar[1]);
-        pdl_wait();
-        if (!(FUSED && a.p_ready)) {
-            mbar_arrive_expect_tx(&bar[0], ubytes);
-            tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
-        }
-    }
-    const int64_t eb = e * N3 + i;  // + j N + k N2
-    if constexpr (FUSED) {
-        if (valid && a.p_ready) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int k = 0; k < N; ++k) {
-                    xreg[h][k] = a.x[eb + jr[h] * N + k * N2];
-                    if constexpr (FUSED == 2) dreg[h][k] = __ldg(a.dinv + eb + jr[h] * N + k * N2);
-                }
-        }
-    }
-    pdl_wait();
-    for (int t = tid; t < N2; t += blockDim.x) {
-        T d = a.D[t];
-        sD[t] = d;
-        sDt[(t % N) * N + t / N] = d;
-    }
-    T betaT = 0, alphaT = 0;
-    if constexpr (FUSED) {
-        if constexpr (sizeof(T) == 8) {
-            betaT = (T)a.st->beta;
-            alphaT = (T)a.st->alpha;
-        } else {
-            betaT = (T)a.st->beta32;
-            alphaT = (T)a.st->alpha32;
-        }
-        if (valid) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int k = 0; k < N; ++k) {
-                    rreg[h][k] = a.r[eb + jr[h] * N + k * N2];
-                    if (!a.p_ready) {
-                        xreg[h][k] = a.x[eb + jr[h] * N + k * N2];
-                        if constexpr (FUSED == 2) dreg[h][k] = __ldg(a.dinv + eb + jr[h] * N + k * N2);
-                    }
-                }
-        }
-    }
-    __syncthreads();
-    mbar_wait(&bar[0], 0);
-
-    T* ue = sU + el * N3;
-    T* wre = sG + el * 6 * N3;        // aliases g1
-    T* wse = sG + el * 6 * N3 + N3;   // aliases g2
-
-    // ---- p = fma(beta, p, r), x = fma(alpha_prev, p_prev, x)  (C8, fused)
-    T ureg[2][N];
-    if (valid) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-                const int o = k * N2 + jr[h] * N + i;
-                T v = ue[o];
-                if constexpr (FUSED) {
-                    const T po = v;
-                    T zk = rreg[h][k];
-                    if constexpr (FUSED == 2) zk = mul_t<T>(rreg[h][k], dreg[h][k]);  // solveM (Jacobi)
-                    v = fma_t<T>(betaT, po, zk);
-                    a.x[e * N3 + o] = fma_t<T>(alphaT, po, xreg[h][k]);
-                    a.p[e * N3 + o] = v;
-                    ue[o] = v;
-                }
-                ureg[h][k] = v;
-            }
-    }
-    if constexpr (FUSED) __syncthreads();
-
-    // ---- gradient (C1), metric (C2), t-part of the transpose (C3: b chain)
-    T b[2][N];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int k = 0; k < N; ++k) b[h][k] = 0;
-    if (valid) {
-        const T* Ge = sG + el * 6 * N3 + i;
-        T Dri[N], Drj[2][N];
-        lds_row<T, N>(Dri, sD + i * N);         // D[i][:]
-        lds_row<T, N>(Drj[0], sD + jr[0] * N);  // D[j][:]
-        lds_row<T, N>(Drj[1], sD + jr[1] * N);
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            if (k == 0) mbar_wait(&bar[1], 0);
-            T col[N];
-#pragma unroll
-            for (int l = 0; l < N; ++l) col[l] = ue[k * N2 + l * N + i];   // u[k][:][i]
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int j = jr[h];
-                T urow[N];
-                lds_row<T, N>(urow, ue + k * N2 + j * N);   // u[k][j][:]
-                T ur = 0, us = 0, ut = 0;
-#pragma unroll
-                for (int l = 0; l < N; ++l) ur = fma_t<T>(Dri[l], urow[l], ur);
-#pragma unroll
-                for (int l = 0; l < N; ++l) us = fma_t<T>(Drj[h][l], col[l], us);
-#pragma unroll
-                for (int l = 0; l < N; ++l) ut = fma_t<T>(dc.v[k * N + l], ureg[h][l], ut);
-                const int o = k * N2 + j * N;
-                const T g1 = Ge[0 * N3 + o], g2 = Ge[1 * N3 + o], g3 = Ge[2 * N3 + o];
-                const T g4 = Ge[3 * N3 + o], g5 = Ge[4 * N3 + o], g6 = Ge[5 * N3 + o];
-                T wr = mul_t<T>(g1, ur);
-                wr = fma_t<T>(g2, us, wr);
-                wr = fma_t<T>(g3, ut, wr);
-                T ws = mul_t<T>(g2, ur);
-                ws = fma_t<T>(g4, us, ws);
-                ws = fma_t<T>(g5, ut, ws);
-                T wt = mul_t<T>(g3, ur);
-                wt = fma_t<T>(g5, us, wt);
-                wt = fma_t<T>(g6, ut, wt);
-                wre[o + i] = wr;   // own slots of g1 / g2, dead after the reads above
-                wse[o + i] = ws;
-#pragma unroll
-                for (int kk = 0; kk < N; ++kk) b[h][kk] = fma_t<T>(dc.v[k * N + kk], wt, b[h][kk]);
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---- r/s part of the transpose (C3: a chain), w = a + b, mask, pap
-    acc_t acc;
-    if (valid) {
-        const ElemCoord ec = elem_coord(a.mesh, (uint32_t)e);
-        const int n1 = N - 1;
-        const bool mz0 = ec.azg == 0, mz1 = ec.azg == a.mesh.ezg - 1;
-        T Dci[N], Dcj[2][N];
-        lds_row<T, N>(Dci, sDt + i * N);          // D[:][i]
-        lds_row<T, N>(Dcj[0], sDt + jr[0] * N);   // D[:][j]
-        lds_row<T, N>(Dcj[1], sDt + jr[1] * N);
-        bool mxy[2], sxy[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int j = jr[h];
-            mxy[h] = (i == 0 && ec.ax == 0) || (i == n1 && ec.ax == a.mesh.ex - 1) ||
-                     (j == 0 && ec.ay == 0) || (j == n1 && ec.ay == a.mesh.ey - 1);
-            sxy[h] = (i == 0 && ec.ax > 0) || (i == n1 && ec.ax < a.mesh.ex - 1) ||
-                     (j == 0 && ec.ay > 0) || (j == n1 && ec.ay < a.mesh.ey - 1);
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            T col[N];
-#pragma unroll
-            for (int l = 0; l < N; ++l) col[l] = wse[k * N2 + l * N + i];   // ws[k][:][i]
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int j = jr[h];
-                T wrow[N];
-                lds_row<T, N>(wrow, wre + k * N2 + j * N);  // wr[k][j][:]
-                T s = 0;
-#pragma unroll
-                for (int l = 0; l < N; ++l) s = fma_t<T>(Dci[l], wrow[l], s);
-#pragma unroll
-                for (int l = 0; l < N; ++l) s = fma_t<T>(Dcj[h][l], col[l], s);
-                T wv = add_t<T>(s, b[h][k]);
-                const bool masked = mxy[h] || (k == 0 && mz0) || (k == n1 && mz1);
-                if (a.mask && masked) wv = 0;   // C5: assign +0
-                a.w[eb + j * N + k * N2] = wv;
-                if constexpr (FUSED) {
-                    const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
-                    if (!sxy[h] && !sz) acc.add(dot_term(wv, ureg[h][k], 1.0, a.single != 0));
-                }
             }
         }
     }
@@ -862,14 +621,25 @@ __device__ __forceinline__ void add_node_pap(acc_t& acc, T w, T p, int m, int si
     }
 }
 
-template <typename T>
-__device__ __forceinline__ bool masked_local(const MeshView& m, int32_t L)
+// Natural local index of the SL position Ls (the plan stores SL positions).
+__device__ __forceinline__ int64_t sl_natural(const MeshView& m, int64_t Ls)
 {
     const int N = m.N, N3 = N * N * N;
-    const uint32_t e = (uint32_t)(L / N3);
-    const int rem = L - (int)e * N3;
+    const int64_t e = Ls / N3;
+    int i, j, k;
+    sl_point(N, (int)(Ls - e * N3), i, j, k);
+    return e * N3 + (k * N + j) * N + i;
+}
+
+template <typename T>
+__device__ __forceinline__ bool masked_local(const MeshView& m, int32_t Ls)
+{
+    const int N = m.N, N3 = N * N * N;
+    const uint32_t e = (uint32_t)(Ls / N3);
+    int i, j, k;
+    sl_point(N, Ls - (int)e * N3, i, j, k);
     ElemCoord ec = elem_coord(m, e);
-    return is_masked(m, ec, rem % N, (rem / N) % N, rem / (N * N));
+    return is_masked(m, ec, i, j, k);
 }
 
 // Load the (ascending) local indices of node q of a tile (q counts the tile's
@@ -991,8 +761,7 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
                 for (int c = 1; c < 8; ++c)
                     if (c < m[h])  // chain add c of the node (key: its first copy)
                         sum = padd<PM>(sum, v[h][c], a.pm,
-                                       pm_key(a.it, PH_B, (long long)a.mesh.z0 * a.mesh.ex * a.mesh.ey *
-                                                          a.mesh.N * a.mesh.N * a.mesh.N + ix[h][0], c));
+                                       pm_key(a.it, PH_B, global_local_index(a.mesh, sl_natural(a.mesh, ix[h][0])), c));
                 if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[h][0])) sum = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
@@ -1072,6 +841,7 @@ struct VecArgs {
     PmArgs pm;          // precision emulation (NEXT-4)
     int it;             // CG iteration (emulation keys)
     int rev;            // visit the chunks in reverse order
+    int natural;        // DOT only: a, b in natural order (public glsc3); else SL vectors
     MeshView mesh;
 };
 
@@ -1157,6 +927,48 @@ __device__ __forceinline__ void chunk_weights(const MeshView& m, int64_t L, doub
 
 // Vector kernel over all local points: chunks of V = 4 consecutive points
 // (N^3 % 4 == 0) in one element, 16-byte loads/stores; structural c = 1/m.
+// SL weights: sh_tab[f] = boundary code of face slot I^3 + f (bit 0 i = 0,
+// 1 i = N-1, 2 j = 0, 3 j = N-1, 4 k = 0, 5 k = N-1), built per block; an
+// element's neighbour code nb has the same bits for "a neighbour lies on that
+// side".  Bits 0/1 (2/3, 4/5) exclude each other, so popc(code & nb) is the
+// number of directions in which the point is shared and m = 2^popc (R8).
+#define NBK_SL_TAB 1352   // N^3 - (N-2)^3 at N = 16
+__device__ __forceinline__ void sl_tab_build(int N, unsigned char* tab)
+{
+    const int I = N - 2, F = N * N * N - I * I * I;
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+        int i, j, k;
+        sl_point(N, I * I * I + f, i, j, k);
+        tab[f] = (unsigned char)((i == 0) | ((i == N - 1) << 1) | ((j == 0) << 2) | ((j == N - 1) << 3) |
+                                 ((k == 0) << 4) | ((k == N - 1) << 5));
+    }
+}
+__device__ __forceinline__ unsigned elem_nb(const MeshView& m, uint32_t e)
+{
+    const ElemCoord ec = elem_coord(m, e);
+    return (ec.ax > 0) | ((ec.ax < m.ex - 1) << 1) | ((ec.ay > 0) << 2) | ((ec.ay < m.ey - 1) << 3) |
+           ((ec.azg > 0) << 4) | ((ec.azg < m.ezg - 1) << 5);
+}
+// c = 1/m of the V consecutive SL slots L..L+V-1 (one element; interior slots and
+// face slots never share a chunk: I^3 % V == 0).
+template <int V>
+__device__ __forceinline__ void chunk_weights_sl(const MeshView& m, int64_t L, const unsigned char* tab,
+                                                 double (&c)[V])
+{
+    const int N = m.N, I = N - 2;
+    const uint32_t Lu = (uint32_t)L;
+    const uint32_t e = fast_div(Lu, m.n3_mul, m.n3_shr);
+    const int s = (int)(Lu - e * (uint32_t)(N * N * N)) - I * I * I;
+    if (s < 0) {
+#pragma unroll
+        for (int t = 0; t < V; ++t) c[t] = 1.0;
+        return;
+    }
+    const unsigned nb = elem_nb(m, e);
+#pragma unroll
+    for (int t = 0; t < V; ++t) c[t] = inv_mult(1 << __popc(tab[s + t] & nb));
+}
+
 // Per-chunk loads and arithmetic of each mode (split so that the loads of two
 // chunks can be issued before either is used).
 template <typename T, int V, int MODE, int PM = PM_NONE>
@@ -1203,9 +1015,11 @@ struct VecChunk {
         } else if constexpr (MODE == VEC_RUPD) {
             VecT<T, V> r;
 #pragma unroll
-            for (int t = 0; t < V; ++t)  // C8 (emulation key: the point's local index, phase C)
-                r.v[t] = pfma<PM>(am, A.v[t], B.v[t], a.pm,
-                                  pm_key(a.it, PH_C, global_local_index(a.mesh, L + t), 0));
+            for (int t = 0; t < V; ++t) {  // C8 (emulation key: the point's natural local index, phase C)
+                unsigned long long key = 0;
+                if constexpr (PM != PM_NONE) key = pm_key(a.it, PH_C, global_local_index(a.mesh, sl_natural(a.mesh, L + t)), 0);
+                r.v[t] = pfma<PM>(am, A.v[t], B.v[t], a.pm, key);
+            }
             r.store(a.r + L);
 #pragma unroll
             for (int t = 0; t < V; ++t) acc.add(dot_term_pm<PM>(r.v[t], r.v[t], c[t], a.single, a.pm));
@@ -1256,9 +1070,19 @@ struct VecChunk {
 #ifndef NBK_VEC_U
 #define NBK_VEC_U 2
 #endif
-template <typename T, int V, int MODE, int PM = PM_NONE>
-__device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, acc_t& acc2)
+template <int V>
+__device__ __forceinline__ void chunk_weights_any(const MeshView& m, int64_t L, const unsigned char* tab,
+                                                  bool natural, double (&c)[V])
 {
+    if (natural) chunk_weights<V>(m, L, c);
+    else chunk_weights_sl<V>(m, L, tab, c);
+}
+
+template <typename T, int V, int MODE, int PM = PM_NONE>
+__device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, acc_t& acc2,
+                                         const unsigned char* tab)
+{
+    const bool nat = MODE == VEC_DOT && a.natural;
     const int64_t nch = a.n / V;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1276,7 +1100,7 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, 
 #pragma unroll
         for (int u = 0; u < NBK_VEC_U; ++u) {
             double c[V];
-            chunk_weights<V>(a.mesh, L[u], c);
+            chunk_weights_any<V>(a.mesh, L[u], tab, nat, c);
             C[u].run(a, L[u], c, am, acc, acc2);
         }
     }
@@ -1285,7 +1109,7 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, 
         const int64_t L0 = (a.rev ? nch - 1 - q0 : q0) * V;
         C0.load(a, L0);
         double c[V];
-        chunk_weights<V>(a.mesh, L0, c);
+        chunk_weights_any<V>(a.mesh, L0, tab, nat, c);
         C0.run(a, L0, c, am, acc, acc2);
     }
 }
@@ -1296,11 +1120,14 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
     constexpr bool J = vec_jacobi(MODE);
     acc_t acc, acc2;
     T am = 0;
+    __shared__ unsigned char sl_tab[NBK_SL_TAB];
+    sl_tab_build(a.mesh.N, sl_tab);  // before the PDL wait: overlaps the previous kernel's tail
     pdl_wait();
     if constexpr (MODE == VEC_RUPD || MODE == VEC_RUPD_J) {
         if constexpr (sizeof(T) == 8) am = (T)a.st->alpham; else am = (T)a.st->alpham32;
     }
-    vec_loop<T, V, MODE, PM>(a, am, acc, acc2);
+    __syncthreads();
+    vec_loop<T, V, MODE, PM>(a, am, acc, acc2, sl_tab);
     pdl_launch_dependents();
     dd v = block_reduce_dd(acc.get());
     dd v2 = J ? block_reduce_dd(acc2.get()) : dd{0.0, 0.0};
@@ -1334,7 +1161,9 @@ __global__ void __launch_bounds__(256) k_tail_x(T* x, const T* p, const CgState*
     if constexpr (sizeof(T) == 8) al = (T)st->alpha; else al = (T)st->alpha32;
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
          L += (int64_t)gridDim.x * blockDim.x) {
-        x[L] = pfma<PM>(al, p[L], x[L], P, pm_key(it, PH_A, global_local_index(m, L), 1));
+        unsigned long long key = 0;
+        if constexpr (PM != PM_NONE) key = pm_key(it, PH_A, global_local_index(m, sl_natural(m, L)), 1);
+        x[L] = pfma<PM>(al, p[L], x[L], P, key);
     }
 }
 
@@ -1350,6 +1179,24 @@ static __global__ void __launch_bounds__(256) k_downcast(float* dst, const doubl
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
          L += (int64_t)gridDim.x * blockDim.x)
         dst[L] = __double2float_rn(src[L]);
+}
+
+// Natural order <-> split layout (SL) of a local-storage field (public-API
+// arrays, host transfers of f / x / dinv).  One thread per natural point.
+template <typename T, bool TO_SL>
+__global__ void __launch_bounds__(256) k_perm_sl(T* dst, const T* src, MeshView m)
+{
+    const int N = m.N, N3 = N * N * N;
+    const int64_t n = m.E * N3;
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
+         L += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = fast_div((uint32_t)L, m.n3_mul, m.n3_shr);
+        const uint32_t rem = (uint32_t)L - e * (uint32_t)N3;
+        const uint32_t q1 = fast_div(rem, m.n_mul, m.n_shr);
+        const uint32_t q2 = fast_div(q1, m.n_mul, m.n_shr);
+        const int64_t Ls = (int64_t)e * N3 + sl_slot(N, (int)(rem - q1 * N), (int)(q1 - q2 * N), (int)q2);
+        if (TO_SL) dst[Ls] = src[L]; else dst[L] = src[Ls];
+    }
 }
 
 // Standalone mask (C5) over all local points.
@@ -1411,9 +1258,9 @@ __global__ void __launch_bounds__(256) k_face_pack(FaceArgs<T> a)
         const int pos = (int)(t - el * N2);
         if (hi) {
             const int64_t e = (int64_t)(a.mesh.ez_local - 1) * exy + el;
-            a.send_hi[t] = a.w[e * N3 + (int64_t)(N - 1) * N2 + pos];
+            a.send_hi[t] = a.w[e * N3 + sl_plane(N, N - 1) + pos];
         } else {
-            a.send_lo[t] = a.w[el * N3 + pos];
+            a.send_lo[t] = a.w[el * N3 + sl_plane(N, 0) + pos];
         }
     }
 }
@@ -1453,7 +1300,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
         const int ny = plane_elems(gy, m.ey, N, aye, jl);
         // own copies: layer base element and plane k
         const int64_t ebase = upper ? (int64_t)(m.ez_local - 1) * exy : 0;
-        const int kpl = upper ? N - 1 : 0;
+        const int kpl = sl_plane(N, upper ? N - 1 : 0);   // SL slot of the face plane's (0, 0)
         const T* other = upper ? a.recv_hi : a.recv_lo;
         T sum = 0;
         bool first = true;
@@ -1465,7 +1312,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
                 for (int bx = 0; bx < nx; ++bx) {
                     const int64_t el = axe[bx] + (int64_t)m.ex * aye[by];
                     const int pos = jl[by] * N + il[bx];
-                    const T v = own ? a.w[(ebase + el) * N3 + (int64_t)kpl * N2 + pos]
+                    const T v = own ? a.w[(ebase + el) * N3 + kpl + pos]
                                     : other[el * N2 + pos];
                     sum = first ? v : add_t<T>(sum, v);
                     first = false;
@@ -1476,7 +1323,7 @@ __global__ void __launch_bounds__(256) k_face_merge(FaceArgs<T> a)
         for (int by = 0; by < ny; ++by)
             for (int bx = 0; bx < nx; ++bx) {
                 const int64_t el = axe[bx] + (int64_t)m.ex * aye[by];
-                const int64_t L = (ebase + el) * N3 + (int64_t)kpl * N2 + jl[by] * N + il[bx];
+                const int64_t L = (ebase + el) * N3 + kpl + jl[by] * N + il[bx];
                 if (FUSED && by == 0 && bx == 0) p0 = a.p[L];
                 a.w[L] = sum;
             }

@@ -68,24 +68,15 @@ template <typename T, int N, int FUSED, int PM = PM_NONE>
 inline cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
                                bool pdl = false)
 {
-    if constexpr (PM == PM_NONE && ax2_enabled<T>(N)) {  // 2 points per thread (N = 10, 12)
-        constexpr int EPB2 = ax2_epb<T>(N);
-        const size_t smem2 = (size_t)ax2_smem_bytes<T>(N);
-        if (attr_only)
-            return cudaFuncSetAttribute(k_ax2<T, N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem2);
-        DConst<T> dc{};
-        for (int q = 0; q < N * N; ++q) dc.v[q] = a.Dh[q];
-        const unsigned grid2 = (unsigned)((a.mesh.E + EPB2 - 1) / EPB2);
-        return launch_k(k_ax2<T, N, FUSED>, grid2, ax2_threads<T>(N), smem2, s, pdl, a, dc);
-    }
     constexpr int EPB = ax_epb<T>(N);
     const size_t smem = (size_t)ax_smem_bytes<T>(N);
     if (attr_only)
         return cudaFuncSetAttribute(k_ax<T, N, FUSED, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem);
     const unsigned grid = (unsigned)((a.mesh.E + EPB - 1) / EPB);
-    return launch_k(k_ax<T, N, FUSED, PM>, grid, ax_threads<T>(N), smem, s, pdl, a);
+    DConst<T> dc{};
+    for (int q = 0; q < N * N; ++q) dc.v[q] = a.Dh[q];
+    return launch_k(k_ax<T, N, FUSED, PM>, grid, ax_threads<T>(N), smem, s, pdl, a, dc);
 }
 
 #define NBK_SWITCH_N(N, CALL)                 \
@@ -355,8 +346,7 @@ inline AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
 template <typename T, int PM = PM_NONE>
 inline int ax_blocks_n(int64_t E, int N)
 {
-#define EPBN(n) (int)((PM == PM_NONE && ax2_enabled<T>(n)) ? (E + ax2_epb<T>(n) - 1) / ax2_epb<T>(n) \
-                                        : (E + ax_epb<T>(n) - 1) / ax_epb<T>(n))
+#define EPBN(n) (int)((E + ax_epb<T>(n) - 1) / ax_epb<T>(n))
     NBK_SWITCH_N(N, EPBN)
 #undef EPBN
 }
@@ -491,20 +481,46 @@ inline VecArgs<T> vec_args(nbk_ctx* c)
     return v;
 }
 
-// ax (+ dssum + mask) of per-member fields over a team (standalone / final check).
+// Field permutation natural <-> split layout (one pass).
+template <typename T>
+inline cudaError_t perm_sl(nbk_ctx* c, T* dst, const T* src, bool to_sl, cudaStream_t s)
+{
+    if (to_sl) k_perm_sl<T, true><<<vec_grid(c->n), 256, 0, s>>>(dst, src, c->view);
+    else k_perm_sl<T, false><<<vec_grid(c->n), 256, 0, s>>>(dst, src, c->view);
+    return cudaGetLastError();
+}
+
+// The solver's w buffer of precision T: scratch of the public natural-order calls
+// (dead between solves).
+template <typename T>
+inline T* sl_scratch(nbk_ctx* c) { return (T*)(sizeof(T) == 8 ? (void*)c->w64 : (void*)c->w32); }
+
+// ax (+ dssum + mask) of per-member fields over a team.  sl: u, w are CG vectors
+// in the split layout (final check); otherwise natural-order public arrays --
+// with DSSUM, K_A writes SL into the member's scratch, the SL plan sums it and
+// the result is permuted into w.
 template <typename T>
 inline cudaError_t ax_team(const Team& t, const std::vector<const T*>& u, const std::vector<T*>& w,
-                           int flags, bool fp32, std::string& err)
+                           int flags, bool fp32, std::string& err, bool sl = false)
 {
     cudaError_t e;
+    const bool ds = (flags & NBK_AX_DSSUM) != 0;
+    std::vector<T*> wsl(t.m.size());
     for (size_t q = 0; q < t.m.size(); ++q) {
         nbk_ctx* c = t.m[q];
         AxArgs<T> a = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
                            : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
-        a.u = u[q]; a.w = w[q]; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
+        wsl[q] = (sl || !ds) ? w[q] : sl_scratch<T>(c);
+        a.u = u[q]; a.w = wsl[q]; a.mask = (flags & NBK_AX_MASK) ? 1 : 0;
+        a.in_sl = sl ? 1 : 0;
+        a.out_sl = (sl || ds) ? 1 : 0;
         if ((e = launch_ax<T, 0>(a, t.s)) != cudaSuccess) return e;
     }
-    if (flags & NBK_AX_DSSUM) return dssum_team<T, false>(t, w, {}, 0, false, err);
+    if (!ds) return cudaSuccess;
+    if ((e = dssum_team<T, false>(t, wsl, {}, 0, false, err)) != cudaSuccess) return e;
+    if (sl) return cudaSuccess;
+    for (size_t q = 0; q < t.m.size(); ++q)
+        if ((e = perm_sl<T>(t.m[q], w[q], wsl[q], false, t.s)) != cudaSuccess) return e;
     return cudaSuccess;
 }
 

@@ -295,6 +295,15 @@ __device__ __forceinline__ uint32_t point_gid_dev(const MeshView& m, int64_t L, 
     return gx + Gx * (gy + Gy * gz);
 }
 
+// SL position (nbk_common.cuh) of natural local index L.
+__device__ __forceinline__ int64_t sl_of_natural(const MeshView& m, int64_t L)
+{
+    const int N = m.N, N3 = N * N * N;
+    const int64_t e = L / N3;
+    const int rem = (int)(L - e * N3);
+    return e * N3 + sl_slot(N, rem % N, (rem / N) % N, rem / (N * N));
+}
+
 __global__ void __launch_bounds__(256) k_rhs(MeshView m, unsigned long long seed, double* f)
 {
     const int64_t n = m.E * m.N * m.N * m.N;
@@ -302,7 +311,7 @@ __global__ void __launch_bounds__(256) k_rhs(MeshView m, unsigned long long seed
          L += (int64_t)gridDim.x * blockDim.x) {
         bool msk;
         uint32_t g = point_gid_dev(m, L, &msk);
-        f[L] = msk ? 0.0 : pm1_dev(seed, g);
+        f[sl_of_natural(m, L)] = msk ? 0.0 : pm1_dev(seed, g);   // f in the split layout
     }
 }
 
@@ -346,11 +355,12 @@ __global__ void __launch_bounds__(256) k_scatter_plan(const uint32_t* vals, cons
                                                       const uint32_t* head_pos,
                                                       const uint32_t* run_pos, int64_t n,
                                                       int32_t* seg_off, int32_t* seg_idx,
-                                                      int64_t ncopies, int64_t nseg)
+                                                      int64_t ncopies, int64_t nseg, MeshView m)
 {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
-        if (inrun[q]) seg_idx[run_pos[q]] = (int32_t)vals[q];
+        // copies in ascending NATURAL local index (chain order C4), stored as SL positions
+        if (inrun[q]) seg_idx[run_pos[q]] = (int32_t)sl_of_natural(m, vals[q]);
         if (head[q]) seg_off[head_pos[q]] = (int32_t)run_pos[q];
         if (q == 0) seg_off[nseg] = (int32_t)ncopies;
     }
@@ -470,7 +480,7 @@ cudaError_t build_plan(nbk_ctx* ctx)
     err = cub::DeviceScan::ExclusiveSum(tmp, need, inrun, valt, (int)n, s);
     if (err != cudaSuccess) return err;
     k_scatter_plan<<<grid_for(n), 256, 0, s>>>(vals, head, inrun, kalt, valt, n, ctx->seg_off,
-                                              ctx->seg_idx, ctx->ncopies, ctx->nseg);
+                                              ctx->seg_idx, ctx->ncopies, ctx->nseg, ctx->view);
     // check the counts match the analytic plan size
     uint32_t last_head, last_run, h_last, r_last;
     cudaMemcpyAsync(&last_head, kalt + n - 1, 4, cudaMemcpyDeviceToHost, s);
@@ -597,7 +607,7 @@ __global__ void __launch_bounds__(256) k_local_diag(const double* G, const doubl
         }
         const double di = D[i * N + i], dj = D[j * N + j], dk = D[k * N + k];
         s += 2.0 * (di * dj * g[1 * N3 + pt] + di * dk * g[2 * N3 + pt] + dj * dk * g[4 * N3 + pt]);
-        d[e * N3 + pt] = s;
+        d[e * N3 + sl_slot(N, i, j, k)] = s;   // split layout, as every CG vector
     }
 }
 
@@ -609,10 +619,11 @@ __global__ void __launch_bounds__(256) k_finish_dinv(MeshView m, double* d, floa
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n;
          L += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t e = (uint32_t)(L / N3);
-        const int rem = (int)(L - (int64_t)e * N3);
+        int i, j, k;
+        sl_point(N, (int)(L - (int64_t)e * N3), i, j, k);   // d is in the split layout
         ElemCoord ec = elem_coord(m, e);
         double v = d[L];
-        if (is_masked(m, ec, rem % N, (rem / N) % N, rem / (N * N))) v = 1.0;
+        if (is_masked(m, ec, i, j, k)) v = 1.0;
         const double inv = 1.0 / v;
         d[L] = inv;
         if (d32) d32[L] = __double2float_rn(inv);

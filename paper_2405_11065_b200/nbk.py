@@ -18,6 +18,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "csrc", "libnbk.so")
+if os.environ.get("NBK_LIB"):  # A/B experiments: a variant build (build.py --out)
+    LIB_PATH = os.path.abspath(os.environ["NBK_LIB"])
 
 NBK_OK, NBK_EINVAL, NBK_EDEFECT, NBK_ECUDA, NBK_ENCCL, NBK_ENOMEM, NBK_ESTATE = 0, 2, 3, 4, 5, 6, 7
 NBK_FP64, NBK_FP32 = 0, 1
