@@ -82,6 +82,10 @@ def lib():
         L.ora_cg32s.argtypes = [ctypes.c_int] * 4 + [_p] * 4 + [ctypes.c_int] + [_p] * 3
         L.ora_glsc3_32s.restype = ctypes.c_float
         L.ora_glsc3_32s.argtypes = [c_i64, _p, _p, _p]
+        L.ora_cg32a.restype = ctypes.c_int
+        L.ora_cg32a.argtypes = [ctypes.c_int] * 4 + [_p] * 4 + [ctypes.c_int] * 2 + [_p] * 3
+        L.ora_glsc3_32a_p.restype = ctypes.c_float
+        L.ora_glsc3_32a_p.argtypes = [c_i64, _p, _p, _p, ctypes.c_int]
         L.ora_fsum32.restype = ctypes.c_float
         L.ora_fsum32.argtypes = [c_i64, _p]
         L.ora_vprec_round.restype = c_dbl
@@ -231,6 +235,16 @@ def glsc3_single(a, b, c) -> float:
     return float(lib().ora_glsc3_32s(a.size, _ptr(a), _ptr(b), _ptr(c)))
 
 
+def glsc3_accum32(a, b, c, nranks: int = 1) -> float:
+    """The paper's binary32 glsc3 (NEXT-2, R11c): sequential binary32
+    accumulation of RN32(RN32(a b) c) per rank (contiguous ranges), then the
+    per-rank sums added in binary32 in rank order."""
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    return float(lib().ora_glsc3_32a_p(a.size, _ptr(a), _ptr(b), _ptr(c), int(nranks)))
+
+
 def fsum32(t) -> float:
     """RN32 of the exact sum of binary64 terms."""
     t = np.ascontiguousarray(t, dtype=np.float64)
@@ -302,19 +316,28 @@ def jacobi_dinv(mesh: Mesh, D, G):
     return d, dinv
 
 
-def cg(mesh: Mesh, D, G, f, niter: int, precision: str = "fp64", dinv=None) -> CgResult:
+def cg(mesh: Mesh, D, G, f, niter: int, precision: str = "fp64", dinv=None,
+       nranks: int = 1) -> CgResult:
     """Fixed-iteration CG (T1).  precision 'fp64', 'fp32' (mixed: FP64 set-up
-    data rounded once to binary32, FP64 accumulation of glsc3) or 'fp32s'
-    (paper-literal single: binary32 inner products and scalars).  dinv (FP64
-    local array) selects Jacobi PCG: z = r * dinv (dinv rounded to the loop's
-    precision), rtz1 = glsc3(r, c, z)."""
+    data rounded once to binary32, FP64 accumulation of glsc3), 'fp32s'
+    (binary32 scalars, exactly rounded binary32 inner products, R11b) or
+    'fp32a' (the paper's single-precision solver: binary32 accumulation of the
+    inner products per rank, binary32 all-reduce in rank order over `nranks`
+    z-slabs, binary32 scalars; R11c).  dinv (FP64 local array) selects Jacobi
+    PCG: z = r * dinv (dinv rounded to the loop's precision), rtz1 = glsc3(r, c, z)."""
     D = np.ascontiguousarray(D, np.float64)
     G = np.ascontiguousarray(G, np.float64)
     f = np.ascontiguousarray(f, np.float64)
     hist = np.zeros(niter + 1)
     trace = np.zeros((niter, 5))
     L = lib()
-    if precision == "fp32s":  # paper-literal single precision (NEXT-2)
+    if precision == "fp32a":  # the paper's single-precision solver (NEXT-2, R11c)
+        di = None if dinv is None else np.ascontiguousarray(dinv, np.float64)
+        x = np.zeros(f.shape, np.float32)
+        rc = L.ora_cg32a(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), _ptr(di), int(nranks), niter,
+                         _ptr(x), _ptr(hist), _ptr(trace))
+        return CgResult(x=x, hist=hist, trace=trace, defect=int(rc))
+    if precision == "fp32s":  # binary32 scalars, exactly rounded binary32 glsc3 (R11b)
         di = None if dinv is None else np.ascontiguousarray(dinv, np.float64)
         x = np.zeros(f.shape, np.float32)
         rc = L.ora_cg32s(*mesh.dims, _ptr(D), _ptr(G), _ptr(f), _ptr(di), niter, _ptr(x),

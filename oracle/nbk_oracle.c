@@ -635,6 +635,35 @@ float ora_glsc3_32s(int64_t n, const float* a, const float* b, const double* c)
     return xsum_round32(&tot);
 }
 
+/* Paper-literal binary32 accumulation (NEXT-2 as the paper ran it: "the
+ * solver runs exclusively in single precision", P:507 math.f -- where glsc3
+ * lives -- converted to single, P:510 single-precision MPI communication).
+ * Nekbone's glsc3 loop, tmp = tmp + a(i)*b(i)*mult(i), in binary32 and in
+ * ascending local index, no contraction (-O2; reading R11c): per rank
+ * t = RN32(RN32(a_L b_L) c_L), s = RN32(s + t); then the all-reduce, in
+ * binary32 and in rank order.  Ranks own contiguous element ranges (z-slabs,
+ * R21), i.e. contiguous ranges of L: rank r the range [r n/P, (r+1) n/P). */
+static int g_glsc3a_ranks = 1;
+float ora_glsc3_32a_p(int64_t n, const float* a, const float* b, const double* c, int nranks)
+{
+    float tot = 0.0f;
+    for (int r = 0; r < nranks; ++r) {
+        const int64_t lo = n * r / nranks, hi = n * (r + 1) / nranks;
+        float s = 0.0f;
+        for (int64_t L = lo; L < hi; ++L) {
+            const float ab = a[L] * b[L];
+            const float t = ab * (float)c[L];
+            s = s + t;
+        }
+        tot = r == 0 ? s : tot + s;
+    }
+    return tot;
+}
+static float ora_glsc3_32a(int64_t n, const float* a, const float* b, const double* c)
+{
+    return ora_glsc3_32a_p(n, a, b, c, g_glsc3a_ranks);
+}
+
 /* RN32 of an exact sum of binary64 terms (pins the GPU's dd -> binary32 step) */
 float ora_fsum32(int64_t n, const double* t)
 {
@@ -788,6 +817,9 @@ DEFINE_CG(ora_cg32_core, float, double, fmaf, sqrt, PLAIN_DIV, ora_ax_local32, o
 /* paper-literal single precision: binary32 inner products (above) and binary32
  * scalars: beta = rtz1/rtz2, alpha = rtz1/pap, sqrt in binary32 (NEXT-2) */
 DEFINE_CG(ora_cg32s_core, float, float, fmaf, sqrtf, PLAIN_DIV, ora_ax_local32, ora_dssum32, ora_glsc3_32s)
+/* the paper's single-precision solver (NEXT-2, reading R11c): binary32
+ * accumulation of every inner product and binary32 scalars */
+DEFINE_CG(ora_cg32a_core, float, float, fmaf, sqrtf, PLAIN_DIV, ora_ax_local32, ora_dssum32, ora_glsc3_32a)
 
 /* VPREC CG loop (NEXT-4): binary64 loop with every operation of the CG
  * kernels rounded to t bits (ax: every fma / mul / add; dssum adds; the
@@ -867,6 +899,28 @@ int ora_cg32s(int ex, int ey, int ez, int N, const double* D, const double* G, c
         if (di32) di32[q] = (float)dinv[q];
     }
     int rc = ora_cg32s_core(ex, ey, ez, N, D32, G32, f32, di32, niter, x32, hist, trace);
+    free(D32); free(G32); free(f32); free(di32);
+    return rc;
+}
+
+int ora_cg32a(int ex, int ey, int ez, int N, const double* D, const double* G, const double* f,
+              const double* dinv, int nranks, int niter, float* x32, double* hist, double* trace)
+{
+    int64_t E = (int64_t)ex * ey * ez, nn = (int64_t)N * N * N, n = E * nn;
+    float* D32 = (float*)malloc(sizeof(float) * N * N);
+    float* G32 = (float*)malloc(sizeof(float) * 6 * n);
+    float* f32 = (float*)malloc(sizeof(float) * n);
+    float* di32 = dinv ? (float*)malloc(sizeof(float) * n) : NULL;
+    for (int q = 0; q < N * N; ++q) D32[q] = (float)D[q];
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < 6 * n; ++q) G32[q] = (float)G[q];
+    for (int64_t q = 0; q < n; ++q) {
+        f32[q] = (float)f[q];
+        if (di32) di32[q] = (float)dinv[q];
+    }
+    g_glsc3a_ranks = nranks < 1 ? 1 : nranks;
+    int rc = ora_cg32a_core(ex, ey, ez, N, D32, G32, f32, di32, niter, x32, hist, trace);
+    g_glsc3a_ranks = 1;
     free(D32); free(G32); free(f32); free(di32);
     return rc;
 }

@@ -784,3 +784,53 @@ def test_mca_draws_per_operation(ora, mode):
     shared = np.bincount(grp) > 1
     assert (sp[shared] > 0).mean() > 0.5       # most shared nodes have differing copies
     assert (sp[~shared] == 0).all()
+
+
+# ------------------------------------------------ NEXT-2: the paper's binary32 accumulation (R11c)
+def test_glsc3_accum32_is_sequential_binary32(ora):
+    """P:42 / P:507 / P:510: glsc3 accumulated in binary32 in loop order, per
+    rank, then a binary32 all-reduce.  Hand-computed cases: small integers sum
+    exactly (S:336-337 examples); 2^24 followed by four ones stays 2^24 in a
+    binary32 accumulator (2^24 + 1 rounds to even) while the exactly rounded
+    sum (R11b) is 2^24 + 4; the ones first give 2^24 + 4; with two ranks
+    [2^24, 1 | 1, 1] gives 2^24 + 2 (rank sums 2^24 and 2); the product is
+    rounded to binary32 before the weight (c = 1/2 exact)."""
+    one = np.ones(3, np.float32)
+    assert ora.glsc3_accum32(one, one, np.ones(3)) == 3.0
+    assert ora.glsc3_accum32(np.array([1, 2], np.float32), np.array([3, 4], np.float32),
+                             np.array([1.0, 0.5])) == 7.0
+    big = np.float32(2.0 ** 24)
+    a = np.array([big, 1, 1, 1, 1], np.float32)
+    o = np.ones(5, np.float32)
+    c = np.ones(5)
+    assert ora.glsc3_accum32(a, o, c) == 2.0 ** 24
+    assert ora.glsc3_single(a, o, c) == 2.0 ** 24 + 4   # exactly rounded (R11b) differs
+    assert ora.glsc3_accum32(a[::-1].copy(), o, c) == 2.0 ** 24 + 4
+    a4 = np.array([big, 1, 1, 1], np.float32)
+    assert ora.glsc3_accum32(a4, np.ones(4, np.float32), np.ones(4), nranks=2) == 2.0 ** 24 + 2
+    # RN32(a b) before the weight: (1 + 2^-12)^2 = 1 + 2^-11 + 2^-24 -> 1 + 2^-11 in binary32
+    x = np.float32(1 + 2.0 ** -12)
+    assert ora.glsc3_accum32(np.array([x]), np.array([x]), np.array([0.5])) == (1 + 2.0 ** -11) / 2
+
+
+def test_paper_single_solver_plausibility(ora):
+    """The paper's single-precision solver (R11c) on C1: tracks FP64 early,
+    scalars are binary32 values, its history differs from the exactly rounded
+    binary32 variant (R11b) once accumulation errors matter, and the rank
+    split changes the rounding (P:510 all-reduce) but not the early history."""
+    m = ora.Mesh(2, 2, 2, 8, seed_rhs=1001)
+    _, _, D = ora.gll(8)
+    s = ora.setup(m, want=("G", "f"))
+    r64 = ora.cg(m, D, s["G"], s["f"], 60, "fp64")
+    ra = ora.cg(m, D, s["G"], s["f"], 60, "fp32a")
+    rb = ora.cg(m, D, s["G"], s["f"], 60, "fp32s")
+    r2 = ora.cg(m, D, s["G"], s["f"], 60, "fp32a", nranks=2)
+    assert ra.defect == 0
+    rel = np.abs(ra.hist[:15] - r64.hist[:15]) / r64.hist[:15]
+    assert rel.max() < 1e-3
+    assert (ra.trace.astype(np.float32).astype(np.float64) == ra.trace).all()
+    assert not np.array_equal(ra.hist, rb.hist)
+    assert not np.array_equal(ra.hist, r2.hist)
+    assert np.abs(r2.hist[:10] - ra.hist[:10]).max() / ra.hist[0] < 1e-5
+    tr, h0 = ora.true_residual(m, D, s["G"], s["f"], ra.x)
+    assert 1e-9 < tr / h0 < 1e-3
