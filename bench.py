@@ -338,7 +338,7 @@ def convergence_study(ctx, niter_max):
     FP64 true residual (C12) of the returned x after several lengths."""
     import numpy as np
     conv = {"niter_max": niter_max}
-    for p_ in ("fp64", "fp32", "fp32s"):
+    for p_ in ("fp64", "fp32", "fp32s", "fp32a"):
         hh, _, rr = ctx.cg_solve(niter_max, p_, trace=False)
         rel = hh / hh[0] if hh[0] else hh
         it_to = {}
@@ -564,13 +564,15 @@ def run_gpu(args):
         import numpy as np
         with torch.cuda.stream(stream):
             h, xs, rs = {}, {}, {}
-            for p_ in ("fp64", "fp32", "fp32s"):
+            for p_ in ("fp64", "fp32", "fp32s", "fp32a"):
                 h[p_], _, rs[p_] = ctx.cg_solve(cfg.niter, p_, trace=False)
                 xs[p_] = ctx.solution()
             ms1, _, _, _, _ = time_solves(ctx, torch, cfg, "fp32s", min(args.steps, 3), 1, flush,
                                           profile=False)
+            msa, _, _, _, _ = time_solves(ctx, torch, cfg, "fp32a", min(args.steps, 3), 1, flush,
+                                          profile=False)
         acc = {}
-        for p_ in ("fp32", "fp32s"):
+        for p_ in ("fp32", "fp32s", "fp32a"):
             ae = np.abs(h[p_][1:] - h["fp64"][1:])
             acc[p_] = {"MAE": float(ae.mean()), "AE_max": float(ae.max()),
                        "MAE_rel_h0": float(ae.mean() / h["fp64"][0]),
@@ -579,8 +581,11 @@ def run_gpu(args):
                                               np.abs(xs["fp64"]).max())}
         acc["fp64_true_res_rel"] = rs["fp64"]["true_res_rel"]
         acc["fp32s_value"] = ng * cfg.niter * len(ms1) / (sum(ms1) / 1e3) / 1e9
+        acc["fp32a_value"] = ng * cfg.niter * len(msa) / (sum(msa) / 1e3) / 1e9
         acc["note"] = ("fp32: north_star mixed solver (FP64 inner-product accumulation); fp32s: "
-                       "binary32 inner products (exactly rounded) and binary32 scalars (R11b)")
+                       "exactly rounded binary32 inner products and binary32 scalars (R11b); "
+                       "fp32a: the paper's single-precision solver, inner products accumulated "
+                       "in binary32 (R11c, P:42, P:507, P:510); AE/MAE vs the FP64 solver (P:519-522)")
         extra["accuracy"] = acc
         del xs
 

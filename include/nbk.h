@@ -48,13 +48,21 @@ typedef enum {
     NBK_FP64 = 0, /* FP64 CG solver (Nekbone's reference precision)                        */
     NBK_FP32 = 1, /* mixed: FP64 set-up, FP32 CG loop with FP64 inner-product accumulation
                      (north_star; reading R11), FP64 final residual check (C12)          */
-    NBK_FP32S = 2, /* paper-literal single: as
-                     NBK_FP32 but inner products RN32(sum RN32(a b) c) and the scalars
-                     alpha, beta, sqrt in binary32 (cg_solve and glsc3 only)           */
-    NBK_VPREC = 3  /* VPREC emulation (NEXT-4): binary64 CG loop with
+    NBK_FP32S = 2, /* exactly rounded binary32 (SURVEY 8(f) NEXT-2 variant, reading R11b):
+                     as NBK_FP32 but inner products RN32(sum RN32(a b) c), the best value a
+                     binary32 accumulator could return, and the scalars alpha, beta, sqrt
+                     in binary32 (cg_solve and glsc3 only; bitwise against the oracle)   */
+    NBK_VPREC = 3, /* VPREC emulation (NEXT-4): binary64 CG loop with
                      every operation's result rounded to t mantissa bits (nbk_set_vprec;
                      glsc3 terms vp(a b) c, the sum vp(RN64(sum)); alpha, beta, sqrt);
                      set-up data and the final FP64 check are not rounded (cg_solve only) */
+    NBK_FP32A = 4  /* the paper's single-precision solver (NEXT-2, "exclusively in
+                     single", P:507 math.f in single, P:510 single-precision MPI; reading
+                     R11c): inner products ACCUMULATED in binary32 (terms RN32(RN32(a b) c),
+                     a fixed binary32 summation tree per rank, the rank sums added in
+                     binary32 in rank order), binary32 scalars; unpreconditioned
+                     cg_solve only; agrees with the oracle's sequential binary32 loop to
+                     rounding, not bitwise                                               */
 } nbk_precision;
 
 /* Box mesh (reading R5): cubic elements of edge h = 1/ex on

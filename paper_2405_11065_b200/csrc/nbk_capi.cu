@@ -100,7 +100,7 @@ static nbk_status get_graph(const Team& t, int niter, nbk_precision prec, nbk_gr
     cudaError_t e = prec == NBK_FP64    ? enqueue_solve<double>(t, niter, &g, false, c->profiling, err)
                     : prec == NBK_VPREC ? enqueue_emulated(t, niter, &g, c->profiling, err, c->pm_mode)
                                         : enqueue_solve<float>(t, niter, &g, true, c->profiling, err,
-                                                               prec == NBK_FP32S ? 1 : 0);
+                                                               prec == NBK_FP32S ? 1 : (prec == NBK_FP32A ? 2 : 0));
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(t.s, &graph);
     if (e != cudaSuccess) {
@@ -238,10 +238,12 @@ static nbk_status solve_team(const Team& t, int32_t niter, nbk_precision prec, d
 {
     nbk_ctx* c = t.m[0];
     if (niter < 1 || niter > NBK_MAX_NITER) return fail(c, NBK_EINVAL, "niter out of range");
-    if (prec != NBK_FP64 && prec != NBK_FP32 && prec != NBK_FP32S && prec != NBK_VPREC)
+    if (prec != NBK_FP64 && prec != NBK_FP32 && prec != NBK_FP32S && prec != NBK_VPREC && prec != NBK_FP32A)
         return fail(c, NBK_EINVAL, "bad precision");
     for (nbk_ctx* m : t.m) {
-        if ((prec == NBK_FP32 || prec == NBK_FP32S) && !m->G32)
+        if (prec == NBK_FP32A && m->precond != NBK_PRECOND_NONE)
+            return fail(c, NBK_EINVAL, "the binary32-accumulating solver is unpreconditioned");
+        if ((prec == NBK_FP32 || prec == NBK_FP32S || prec == NBK_FP32A) && !m->G32)
             return fail(c, NBK_ESTATE, "context was set up without FP32 arrays");
         if (prec == NBK_VPREC && m->vp_t != c->vp_t) return fail(c, NBK_EINVAL, "members differ in VPREC t");
         if (prec == NBK_VPREC && m->N > NBK_VPREC_MAXN) return fail(c, NBK_EINVAL, "VPREC emulation supports N <= 12");
@@ -791,7 +793,8 @@ nbk_status nbk_solve_launches(const nbk_ctx* c, int32_t niter, nbk_precision pre
     // init (+fin), per iteration K_A, K_B, K_C (+ pack, merge, 2 fin), tail_x, [upcast],
     // final check K_A, K_B, K_C (+ pack, merge, fin)
     *launches = (1 + multi) + (3 + 4 * multi) * (int64_t)niter + 1 +
-                ((prec == NBK_FP32 || prec == NBK_FP32S) ? 1 : 0) +
+                ((prec == NBK_FP32 || prec == NBK_FP32S || prec == NBK_FP32A) ? 1 : 0) +
+                (prec == NBK_FP32A ? (1 + multi) * (int64_t)niter : 0) +   // the binary32 pap kernel (+ fin)
                 (3 + 3 * multi);
     return NBK_OK;
 }

@@ -1151,6 +1151,103 @@ __global__ void __launch_bounds__(256) k_vec(VecArgs<T> a)
     }
 }
 
+// ------------------------------------------------ binary32 accumulation (NEXT-2)
+// The paper's single-precision solver (reading R11c): the
+// inner products accumulated in binary32.  Terms RN32(RN32(a b) c) are added
+// into a binary32 running sum per thread (its chunks in grid-stride order),
+// the block sums by a fixed binary32 shuffle tree, the per-block sums by the
+// last block (fixed slices, then the same tree), the per-rank sums in binary32
+// in rank order (k_fin): a fixed binary32 summation tree, not the oracle's
+// sequential loop, so the two agree to rounding (parity by tolerance).  The
+// scalars are binary32 (fin_* with single = 1).  Separate from k_vec so the
+// FP64-accumulating hot path is untouched.
+enum VecAMode { VA_INIT = 0, VA_RUPD = 1, VA_PAP = 2 };
+
+__device__ __forceinline__ float block_reduce_f32(float v)
+{
+    __shared__ float red32[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = __fadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+    __syncthreads();
+    if (lane == 0) red32[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        v = lane < nw ? red32[lane] : 0.0f;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = __fadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+    }
+    return v;
+}
+
+template <int V, int MODE>
+__global__ void __launch_bounds__(256) k_vec_a(VecArgs<float> a)
+{
+    __shared__ unsigned char sl_tab[NBK_SL_TAB];
+    sl_tab_build(a.mesh.N, sl_tab);
+    const float am = MODE == VA_RUPD ? a.st->alpham32 : 0.0f;
+    __syncthreads();
+    float s = 0.0f;
+    const int64_t nch = a.n / V, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nch; q += stride) {
+        const int64_t L = (a.rev ? nch - 1 - q : q) * V;
+        double c[V];
+        chunk_weights_sl<V>(a.mesh, L, sl_tab, c);
+        VecT<float, V> X, Y;
+        if constexpr (MODE == VA_INIT) {
+            VecT<double, V> F;
+            F.load(a.f + L);
+            VecT<float, V> z;
+#pragma unroll
+            for (int t = 0; t < V; ++t) {
+                X.v[t] = (float)F.v[t];  // C11
+                z.v[t] = 0.0f;
+            }
+            X.store(a.r + L);
+            z.store(a.x + L);
+            z.store(a.p + L);
+            Y = X;
+        } else if constexpr (MODE == VA_RUPD) {
+            VecT<float, V> W;
+            W.load(a.w + L);
+            X.load(a.r + L);
+#pragma unroll
+            for (int t = 0; t < V; ++t) X.v[t] = __fmaf_rn(am, W.v[t], X.v[t]);  // C8
+            X.store(a.r + L);
+            Y = X;
+        } else {
+            X.load(a.w + L);
+            Y.load(a.p + L);
+        }
+#pragma unroll
+        for (int t = 0; t < V; ++t) s = __fadd_rn(s, __fmul_rn(__fmul_rn(X.v[t], Y.v[t]), (float)c[t]));
+    }
+    const float bsum = block_reduce_f32(s);
+    if (publish_and_check_last(a.parts, blockIdx.x, dd{(double)bsum, 0.0}, &a.st->cnt[1], gridDim.x)) {
+        const int P = gridDim.x;
+        const int lo = (int)((int64_t)P * threadIdx.x / blockDim.x);
+        const int hi = (int)((int64_t)P * (threadIdx.x + 1) / blockDim.x);
+        float t = 0.0f;
+        for (int q = lo; q < hi; ++q) t = __fadd_rn(t, (float)__ldcg(&a.parts[q].hi));
+        const float tot = block_reduce_f32(t);
+        if (threadIdx.x == 0) {
+            const dd v{(double)tot, 0.0};
+            if (a.slot) {
+                a.slot[0] = v;   // multi-rank: k_fin adds the rank sums in binary32, rank order
+                a.slot[1] = v;
+            } else if constexpr (MODE == VA_PAP) {
+                fin_alpha(a.st, v, a.trace, true);
+            } else if constexpr (MODE == VA_INIT) {
+                fin_rtr<VEC_INIT>(a.st, v, v, a.hist, a.trace, true);
+            } else {
+                fin_rtr<VEC_RUPD>(a.st, v, v, a.hist, a.trace, true);
+            }
+            a.st->cnt[1] = 0;
+        }
+    }
+}
+
 // x = fma(alphaT, p, x) after the last iteration (deferred C8 x update).
 // PM: the x update of "iteration niter + 1" (emulation key: op 1 of phase A, local index)
 template <typename T, int PM = PM_NONE>
@@ -1353,9 +1450,16 @@ __global__ void k_fin(const dd* gather, int P, CgState* st, double* hist, double
     if (threadIdx.x != 0) return;
     dd t{__ldcg(&gather[0].hi), __ldcg(&gather[0].lo)};
     dd t2{__ldcg(&gather[1].hi), __ldcg(&gather[1].lo)};
-    for (int r = 1; r < P; ++r) {
-        t = dd_add(t, dd{__ldcg(&gather[2 * r].hi), __ldcg(&gather[2 * r].lo)});
-        t2 = dd_add(t2, dd{__ldcg(&gather[2 * r + 1].hi), __ldcg(&gather[2 * r + 1].lo)});
+    if (single == 2) {  // binary32 all-reduce (NEXT-2): rank sums added in binary32, rank order
+        float f = (float)t.hi;
+        for (int r = 1; r < P; ++r) f = __fadd_rn(f, (float)__ldcg(&gather[2 * r].hi));
+        t = t2 = dd{(double)f, 0.0};
+        single = 1;
+    } else {
+        for (int r = 1; r < P; ++r) {
+            t = dd_add(t, dd{__ldcg(&gather[2 * r].hi), __ldcg(&gather[2 * r].lo)});
+            t2 = dd_add(t2, dd{__ldcg(&gather[2 * r + 1].hi), __ldcg(&gather[2 * r + 1].lo)});
+        }
     }
     if constexpr (KIND == 0) fin_alpha(st, t, trace, single, pm, pa);
     else fin_rtr<KIND - 1>(st, t, vec_jacobi(KIND - 1) ? t2 : t, hist, trace, single, pm, pa);

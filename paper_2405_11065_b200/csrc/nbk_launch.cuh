@@ -472,6 +472,35 @@ inline cudaError_t vec_team(const Team& t, const std::vector<VecArgs<T>>& args, 
     return cudaSuccess;
 }
 
+// Binary32-accumulating vector kernel over a team (NEXT-2 paper single solver).
+template <int MODE>
+inline cudaError_t vec_a_team(const Team& t, const std::vector<VecArgs<float>>& args, std::string& err)
+{
+    cudaError_t e;
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        VecArgs<float> a = args[q];
+        a.slot = t.multi ? t.m[q]->gather + 2 * t.m[q]->rank : nullptr;
+        const bool v4 = a.mesh.N % 2 == 0;
+        const void* kern = v4 ? (const void*)k_vec_a<4, MODE> : (const void*)k_vec_a<1, MODE>;
+        const int cap = resident_grid(kern, 256, 0);
+        int64_t g = (a.n / 4 + 511) / 512;
+        if (g < 1) g = 1;
+        if (g > cap) g = cap;
+        if (v4) k_vec_a<4, MODE><<<(unsigned)g, 256, 0, t.s>>>(a);
+        else k_vec_a<1, MODE><<<(unsigned)g, 256, 0, t.s>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (!t.multi) return cudaSuccess;
+    if ((e = xchg_gather(t, t.s, err)) != cudaSuccess) return e;
+    for (nbk_ctx* c : t.m) {
+        constexpr int KIND = MODE == VA_PAP ? 0 : (MODE == VA_INIT ? 1 + VEC_INIT : 1 + VEC_RUPD);
+        k_fin<KIND><<<1, 32, 0, t.s>>>(c->gather, c->nranks, c->st, c->hist, c->trace, 2, PM_NONE,
+                                      PmArgs{52, 0});
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 template <typename T>
 inline VecArgs<T> vec_args(nbk_ctx* c)
 {
@@ -561,7 +590,18 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
         vr[q] = vi[q];
         vr[q].w = w[q];
     }
-    e = jac ? vec_team<T, VEC_INIT_J>(t, vi, false, err) : vec_team<T, VEC_INIT, PM>(t, vi, false, err);
+    // the paper's single-precision solver (NEXT-2, R11c): binary32 accumulation of
+    // pap and rtr in separate kernels (K_B runs as a plain dssum)
+    const bool acc32 = single == 2;
+    if constexpr (sizeof(T) == 4) {
+        if (acc32) {
+            std::vector<VecArgs<float>> v32(P);
+            for (size_t q = 0; q < P; ++q) v32[q] = *(const VecArgs<float>*)&vi[q];
+            e = vec_a_team<VA_INIT>(t, v32, err);
+        }
+    }
+    if (!acc32)
+        e = jac ? vec_team<T, VEC_INIT_J>(t, vi, false, err) : vec_team<T, VEC_INIT, PM>(t, vi, false, err);
     if (e != cudaSuccess) return e;
     launches += (int64_t)P * (1 + per_fin);
 
@@ -587,16 +627,37 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
             if (e != cudaSuccess) return e;
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 1], s, cudaEventRecordExternal);
-        if ((e = dssum_team<T, true, PM>(t, w, pc, 0, pdl && (g_pdl_mask & 2), err, !rev, single, pm, k)) !=
-            cudaSuccess)
+        if (acc32) {
+            if ((e = dssum_team<T, false>(t, w, {}, 0, false, err, !rev)) != cudaSuccess) return e;
+            if constexpr (sizeof(T) == 4) {
+                std::vector<VecArgs<float>> vp(P);
+                for (size_t q = 0; q < P; ++q) {
+                    vp[q] = *(const VecArgs<float>*)&vr[q];
+                    vp[q].p = (float*)p[q];
+                    vp[q].rev = rev;
+                }
+                if ((e = vec_a_team<VA_PAP>(t, vp, err)) != cudaSuccess) return e;
+            }
+            launches += (int64_t)P * (1 + per_fin);
+        } else if ((e = dssum_team<T, true, PM>(t, w, pc, 0, pdl && (g_pdl_mask & 2), err, !rev, single, pm, k)) !=
+                   cudaSuccess) {
             return e;
+        }
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 2], s, cudaEventRecordExternal);
         for (size_t q = 0; q < P; ++q) {
             vr[q].rev = rev;
             vr[q].it = k;
         }
         const bool pc_ = pdl && (g_pdl_mask & 4);
-        e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pc_, err) : vec_team<T, VEC_RUPD, PM>(t, vr, pc_, err);
+        if constexpr (sizeof(T) == 4) {
+            if (acc32) {
+                std::vector<VecArgs<float>> v32(P);
+                for (size_t q = 0; q < P; ++q) v32[q] = *(const VecArgs<float>*)&vr[q];
+                e = vec_a_team<VA_RUPD>(t, v32, err);
+            }
+        }
+        if (!acc32)
+            e = jac ? vec_team<T, VEC_RUPD_J>(t, vr, pc_, err) : vec_team<T, VEC_RUPD, PM>(t, vr, pc_, err);
         if (e != cudaSuccess) return e;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 3], s, cudaEventRecordExternal);
         rev = !rev;

@@ -24,8 +24,9 @@ if os.environ.get("NBK_LIB"):  # A/B experiments: a variant build (build.py --ou
 NBK_OK, NBK_EINVAL, NBK_EDEFECT, NBK_ECUDA, NBK_ENCCL, NBK_ENOMEM, NBK_ESTATE = 0, 2, 3, 4, 5, 6, 7
 NBK_FP64, NBK_FP32 = 0, 1
 AX_LOCAL, AX_DSSUM, AX_MASK = 0, 1, 2
-NBK_FP32S, NBK_VPREC = 2, 3
-PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32, "fp32s": NBK_FP32S, "vprec": NBK_VPREC}
+NBK_FP32S, NBK_VPREC, NBK_FP32A = 2, 3, 4
+PREC = {"fp64": NBK_FP64, "fp32": NBK_FP32, "fp32s": NBK_FP32S, "vprec": NBK_VPREC,
+        "fp32a": NBK_FP32A}
 PRECOND = {"none": 0, "jacobi": 1}
 EMU = {"vprec": 1, "rr": 2, "mca": 3}
 

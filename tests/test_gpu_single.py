@@ -195,3 +195,56 @@ def test_extreme_rhs_scaling_bitwise(nbk, ora, precision, scale_exp):
     assert _same(hist, ref.hist) and _same(trace, ref.trace)
     assert _same(ctx.solution(), ref.x.astype(np.float64))
     ctx.close()
+
+
+# ------------------------------------------- the paper's binary32-accumulating solver (R11c)
+@pytest.mark.parametrize("args", [(2, 2, 2, 8, 0.0, 0, 1001), (3, 3, 3, 10, 0.1, 2005, 1005)])
+def test_accum32_solver_tracks_oracle(nbk, ora, args):
+    """NEXT-2 as the paper ran it (R11c): binary32
+    accumulation of every glsc3.  The oracle sums sequentially, the library by a
+    fixed binary32 tree: the two are different roundings of the same sums, so
+    parity is the north_star FP32 tolerance (1e-4 relative) over the
+    iterations before the recursive residual reaches the binary32 noise floor
+    (h_k/h_0 > 1e-4), where the order of rounding decides nothing yet."""
+    ctx, om, D, s = make(nbk, ora, args)
+    niter = 60
+    hist, trace, res = ctx.cg_solve(niter, "fp32a")
+    ref = ora.cg(om, D, s["G"], s["f"], niter, "fp32a")
+    assert res["defect_iter"] == 0 and ref.defect == 0
+    win = np.nonzero(ref.hist / ref.hist[0] > 1e-4)[0]
+    win = win[win <= niter]
+    assert len(win) > 10
+    rel = np.abs(hist[win] - ref.hist[win]) / ref.hist[win]
+    assert rel.max() <= 1e-4, rel.max()
+    # binary32 scalars; not the exactly rounded variant (R11b)
+    assert (trace.astype(np.float32).astype(np.float64) == trace).all()
+    hs, _, _ = ctx.cg_solve(niter, "fp32s")
+    assert not np.array_equal(hist, hs)
+    ctx.close()
+
+
+def test_accum32_virtual_slabs_track_oracle(nbk, ora):
+    """Two z-slabs: per-rank binary32 sums added in binary32 in rank order (the
+    paper's single-precision all-reduce) vs the oracle with nranks = 2."""
+    args = (3, 3, 4, 8, 0.1, 7, 9)
+    ex, ey, ez, N, jit, sg, sr = args
+    grp = nbk.Group(nbk.MeshSpec(*args), 2, "fp32")
+    om = ora.Mesh(*args)
+    _, _, D = ora.gll(N)
+    s = ora.setup(om, want=("G", "f"))
+    E2 = om.E // 2
+    grp.load_arrays(D, [s["G"][:E2], s["G"][E2:]], [s["f"][:E2], s["f"][E2:]])
+    hist, trace, res = grp.cg_solve(40, "fp32a")
+    ref = ora.cg(om, D, s["G"], s["f"], 40, "fp32a", nranks=2)
+    win = np.nonzero(ref.hist / ref.hist[0] > 1e-4)[0]
+    rel = np.abs(hist[win] - ref.hist[win]) / ref.hist[win]
+    assert rel.max() <= 1e-4, rel.max()
+    grp.close()
+
+
+def test_accum32_rejects_jacobi(nbk):
+    ctx = nbk.cg_setup(nbk.MeshSpec(2, 2, 2, 4, 0.0, 0, 1), "fp32")
+    ctx.set_precond("jacobi")
+    with pytest.raises(nbk.NbkError):
+        ctx.cg_solve(5, "fp32a")
+    ctx.close()
