@@ -136,14 +136,37 @@ __host__ __device__ constexpr int ax_threads(int N)
     return (N * N * ax_epb<T>(N) + 31) / 32 * 32;
 }
 template <typename T>
-__host__ __device__ constexpr int ax_smem_bytes(int N)
+__host__ __device__ constexpr int ax_blocks_by_smem(int N, int slabs)
 {
-    return (ax_stage_g<T>(N) ? 7 : 3) * ax_epb<T>(N) * N * N * N * (int)sizeof(T);
+    return (232448 - 1024) / (slabs * ax_epb<T>(N) * N * N * N * (int)sizeof(T) + 1024 +
+                              2 * N * N * (int)sizeof(T) + 64);
+}
+// TMA I/O of the fused CG step (TIO): r and x are bulk-loaded like p and G, and
+// p, x, w leave through bulk stores from shared memory -- no per-thread global
+// access to the split-layout vectors (their scattered column addresses cost
+// address arithmetic and L1 sectors).  Two more N^3 blocks per element: used
+// where they do not lower the CTAs per SM (N = 10); NBK_TIO_ALL forces it.
+template <typename T>
+__host__ __device__ constexpr bool ax_tio(int N, int fused)
+{
+    if (fused != 1 || N % 2 != 0 || 7 * N * N * N * (int)sizeof(T) * ax_epb<T>(N) > 200 * 1024) return false;
+#if defined(NBK_TIO_ALL)
+    return 9 * N * N * N * (int)sizeof(T) * ax_epb<T>(N) <= 200 * 1024;
+#elif defined(NBK_TIO_NONE)
+    return false;
+#else
+    return ax_blocks_by_smem<T>(N, 9) == ax_blocks_by_smem<T>(N, 7);
+#endif
 }
 template <typename T>
-__host__ __device__ constexpr int ax_min_blocks(int N)
+__host__ __device__ constexpr int ax_smem_bytes(int N, int fused = 0)
 {
-    int by_smem = (232448 - 1024) / (ax_smem_bytes<T>(N) + 1024 + 2 * N * N * (int)sizeof(T) + 64);
+    return (ax_stage_g<T>(N) ? (ax_tio<T>(N, fused) ? 9 : 7) : 3) * ax_epb<T>(N) * N * N * N * (int)sizeof(T);
+}
+template <typename T>
+__host__ __device__ constexpr int ax_min_blocks(int N, int fused = 0)
+{
+    int by_smem = (232448 - 1024) / (ax_smem_bytes<T>(N, fused) + 1024 + 2 * N * N * (int)sizeof(T) + 64);
     int by_thr = 2048 / ax_threads<T>(N);
     int m = by_smem < by_thr ? by_smem : by_thr;
     return m < 1 ? 1 : m;
@@ -185,7 +208,7 @@ struct DConst {
 // FUSED: 0 = plain ax (u -> w); 1 = CG step (p = beta p + r); 2 = Jacobi PCG
 // step (p = beta p + z, z = RN(r * dinv) formed here: S:376-384, T1 line 2).
 template <typename T, int N, int FUSED, int PM = PM_NONE>
-__global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
+__global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
     k_ax(AxArgs<T> a, const __grid_constant__ DConst<T> dc)
 {
     // PM: every operation goes through the emulation (NEXT-4); op numbers per point:
@@ -195,13 +218,16 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     constexpr int N2 = N * N, N3 = N * N * N, EPB = ax_epb<T>(N);
     constexpr bool STAGE = ax_stage_g<T>(N);
     constexpr bool TMA = STAGE && (N % 2 == 0);
+    constexpr bool TIO = ax_tio<T>(N, FUSED);
     __shared__ __align__(16) T sD[N2];
     __shared__ __align__(16) T sDt[N2];
-    __shared__ __align__(8) uint64_t bar[2];   // TMA: p / u block, G block
+    __shared__ __align__(8) uint64_t bar[3];   // TMA: p / u (+ x) block, G block, (TIO) r block
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* sG = reinterpret_cast<T*>(smem_raw);                  // STAGE: EPB*6*N3
     T* sU = STAGE ? sG + EPB * 6 * N3 : sG;                  // EPB*N3
     T* sW = sU + EPB * N3;                                   // !STAGE: wr, ws (2*EPB*N3)
+    T* sR = sU + EPB * N3;                                   // TIO: r (SL), then u in natural order
+    T* sX = sR + EPB * N3;                                   // TIO: x (SL)
 
     const int tid = threadIdx.x;
     const int el = tid / N2, ij = tid - el * N2;
@@ -225,21 +251,29 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
         if (tid == 0) {
             mbar_init(&bar[0], 1);
             mbar_init(&bar[1], 1);
+            if (TIO) mbar_init(&bar[2], 1);
             const uint32_t ubytes = (uint32_t)(nel * N3 * sizeof(T));
             const uint32_t gbytes = (uint32_t)(nel * 6 * N3 * sizeof(T));
+            // p (and, TIO, x: both written by the previous K_A) on bar[0]
             if (FUSED && a.p_ready) {
-                mbar_arrive_expect_tx(&bar[0], ubytes);
+                mbar_arrive_expect_tx(&bar[0], TIO ? 2 * ubytes : ubytes);
                 tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
+                if (TIO) tma_load_1d(sX, a.x + e0 * N3, ubytes, &bar[0]);
             }
             mbar_arrive_expect_tx(&bar[1], gbytes);
             tma_load_1d(sG, a.G + e0 * 6 * N3, gbytes, &bar[1]);
             pdl_wait();
             if (!(FUSED && a.p_ready)) {
-                mbar_arrive_expect_tx(&bar[0], ubytes);
+                mbar_arrive_expect_tx(&bar[0], TIO ? 2 * ubytes : ubytes);
                 tma_load_1d(sU, src_u + e0 * N3, ubytes, &bar[0]);
+                if (TIO) tma_load_1d(sX, a.x + e0 * N3, ubytes, &bar[0]);
+            }
+            if (TIO) {  // r: written by the previous K_C (after the PDL wait)
+                mbar_arrive_expect_tx(&bar[2], ubytes);
+                tma_load_1d(sR, a.r + e0 * N3, ubytes, &bar[2]);
             }
         }
-        if constexpr (FUSED) {  // x and dinv are final too (x: previous K_A)
+        if constexpr (FUSED && !TIO) {  // x and dinv are final too (x: previous K_A)
             if (valid && a.p_ready) {
                 const SlCol cs = sl_col(N, i, j);
 #pragma unroll
@@ -282,7 +316,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             betaT = (T)a.st->beta32;
             alphaT = (T)a.st->alpha32;
         }
-        if (valid) {  // issued before the TMA wait: overlaps with the bulk copies
+        if (valid && !TIO) {  // issued before the TMA wait: overlaps with the bulk copies
             const bool early = TMA && a.p_ready;
 #pragma unroll
             for (int k = 0; k < N; ++k) {
@@ -305,7 +339,40 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
     // The staged block is in the storage order of the source: SL (CG vectors)
     // is read per column and re-stored in natural order for the derivatives.
     T ureg[N];
-    if (valid) {
+    T* un = ue;   // natural-order u of the element for the derivatives
+    if constexpr (TIO) {
+        // p, x, r blocks (SL) in shared memory: p and x updated in place and
+        // bulk-stored; the natural u goes into the (consumed) r block.
+        mbar_wait(&bar[2], 0);
+        T* re = sR + el * N3;
+        T* xe = sX + el * N3;
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const int sk = cs.at(N, k);
+                const T po = ue[sk];
+                const long long gk = goff + base + (long long)k * N2;  // emulation key: natural local index
+                const T v = pfma<PM>(betaT, po, re[sk], P, pm_key(a.it, PH_A, gk, 0));
+                xe[sk] = pfma<PM>(alphaT, po, xe[sk], P, pm_key(a.it, PH_A, gk, 1));
+                ue[sk] = v;
+                ureg[k] = v;
+            }
+        }
+        __syncthreads();  // every r value of the block has been read
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) re[k * N2 + ij] = ureg[k];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t ubytes = (uint32_t)(nel * N3 * sizeof(T));
+            tma_store_1d(a.p + e0 * N3, sU, ubytes);
+            tma_store_1d(a.x + e0 * N3, sX, ubytes);
+            bulk_commit();
+        }
+        un = re;
+    } else if (valid) {
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             T v = ue[isl ? cs.at(N, k) : k * N2 + ij];
@@ -321,7 +388,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             ureg[k] = v;
         }
     }
-    if (isl) {
+    if (isl && !TIO) {
         __syncthreads();  // every SL value of the block has been read
         if (valid) {
 #pragma unroll
@@ -355,7 +422,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
                 lds_row<T, N>(Drj, sD + j * N);
             }
             T urow[N], Dk[N];
-            lds_row<T, N>(urow, ue + k * N2 + j * N);   // u[k][j][:]
+            lds_row<T, N>(urow, un + k * N2 + j * N);   // u[k][j][:]
 #ifdef NBK_D_SMEM
             lds_row<T, N>(Dk, sD + k * N);   // D[k][:] (broadcast)
 #else
@@ -366,7 +433,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
 #pragma unroll
             for (int l = 0; l < N; ++l) ur = pfma<PM>(Dri[l], urow[l], ur, P, key(k, 2 + l));
 #pragma unroll
-            for (int l = 0; l < N; ++l) us = pfma<PM>(Drj[l], ue[k * N2 + l * N + i], us, P, key(k, 2 + N + l));
+            for (int l = 0; l < N; ++l) us = pfma<PM>(Drj[l], un[k * N2 + l * N + i], us, P, key(k, 2 + N + l));
 #pragma unroll
             for (int l = 0; l < N; ++l) ut = pfma<PM>(Dk[l], ureg[l], ut, P, key(k, 2 + 2 * N + l));
             const T g1 = Ge[0 * N3 + k * N2], g2 = Ge[1 * N3 + k * N2], g3 = Ge[2 * N3 + k * N2];
@@ -422,7 +489,8 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             T wv = padd<PM>(s, b[k], P, key(k, 11 + 6 * N));
             const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
             if (a.mask && masked) wv = 0;   // C5: assign +0
-            a.w[gout(k)] = wv;
+            if constexpr (TIO) sG[el * 6 * N3 + 2 * N3 + cs.at(N, k)] = wv;   // dead g3 slots, SL order
+            else a.w[gout(k)] = wv;
             if constexpr (FUSED) {
                 // element-interior points (m == 1) contribute w p c here; shared
                 // nodes contribute once per node in K_B (bitwise-equal exact sum).
@@ -431,10 +499,22 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N))
             }
         }
     }
+    if constexpr (TIO) {  // w leaves by bulk stores (one per element: the g3 slots are strided)
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            for (int q = 0; q < nel; ++q)
+                tma_store_1d(a.w + (e0 + q) * N3, sG + q * 6 * N3 + 2 * N3, (uint32_t)(N3 * sizeof(T)));
+            bulk_commit();
+        }
+    }
     pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
         if (threadIdx.x == 0) a.parts[blockIdx.x] = v;
+    }
+    if constexpr (TIO) {
+        if (tid == 0) bulk_wait_all();   // shared memory stays valid until the stores are done
     }
 }
 

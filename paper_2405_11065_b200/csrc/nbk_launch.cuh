@@ -69,7 +69,7 @@ inline cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_onl
                                bool pdl = false)
 {
     constexpr int EPB = ax_epb<T>(N);
-    const size_t smem = (size_t)ax_smem_bytes<T>(N);
+    const size_t smem = (size_t)ax_smem_bytes<T>(N, FUSED);
     if (attr_only)
         return cudaFuncSetAttribute(k_ax<T, N, FUSED, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem);
