@@ -134,6 +134,10 @@ static cudaError_t set_ax_attrs(nbk_ctx* c)
     a32.mesh = c->view;
     cudaError_t e;
 
+    if ((e = dssum_attrs<double, true>()) != cudaSuccess) return e;
+    if ((e = dssum_attrs<double, false>()) != cudaSuccess) return e;
+    if ((e = dssum_attrs<float, true>()) != cudaSuccess) return e;
+    if ((e = dssum_attrs<float, false>()) != cudaSuccess) return e;
     if ((e = launch_ax<double, 0>(a64, c->stream, true)) != cudaSuccess) return e;
     if (c->N <= NBK_VPREC_MAXN && (e = emulated_attrs(c)) != cudaSuccess) return e;
     if ((e = launch_ax<double, 1>(a64, c->stream, true)) != cudaSuccess) return e;

@@ -20,6 +20,8 @@ cudaError_t NBK_EMU_CAT(emulated_attrs_, NBK_EMU_MODE)(nbk_ctx* c)
     if (NBK_EMU_MODE != PM_VPREC && c->N > NBK_MC_MAXN) return cudaSuccess;
     AxArgs<double> a64{};
     a64.mesh = c->view;
+    cudaError_t e = dssum_attrs<double, true, NBK_EMU_MODE>();
+    if (e != cudaSuccess) return e;
     return launch_ax<double, 1, NBK_EMU_MODE>(a64, c->stream, true);
 }
 

@@ -145,7 +145,11 @@ __host__ __device__ constexpr int ax_blocks_by_smem(int N, int slabs)
 // p, x, w leave through bulk stores from shared memory -- no per-thread global
 // access to the split-layout vectors (their scattered column addresses cost
 // address arithmetic and L1 sectors).  Two more N^3 blocks per element: used
-// where they do not lower the CTAs per SM (N = 10); NBK_TIO_ALL forces it.
+// where they do not lower the CTAs per SM (N = 10), and for FP32 at N >= 10
+// while >= 3 CTAs fit (N = 12: 4 -> 3 CTAs, still faster).  Measured same-box
+// (DESIGN.md section 8): C5 FP32 K_A 2.74 vs 3.04 ms, FP64 5.54 vs 5.82; C3 FP32
+// 0.64 vs 0.67; N = 8 (7 -> 6 CTAs) and N = 12 FP64 (2 -> 1) slower.
+// NBK_TIO_ALL / NBK_TIO_NONE force it on / off.
 template <typename T>
 __host__ __device__ constexpr bool ax_tio(int N, int fused)
 {
@@ -155,7 +159,8 @@ __host__ __device__ constexpr bool ax_tio(int N, int fused)
 #elif defined(NBK_TIO_NONE)
     return false;
 #else
-    return ax_blocks_by_smem<T>(N, 9) == ax_blocks_by_smem<T>(N, 7);
+    return ax_blocks_by_smem<T>(N, 9) == ax_blocks_by_smem<T>(N, 7) ||
+           (sizeof(T) == 4 && N >= 10 && ax_blocks_by_smem<T>(N, 9) >= 3);
 #endif
 }
 template <typename T>
@@ -862,6 +867,104 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
     }
 }
 
+// Gather-phase K_B (staged tiles): the copies of a tile's nodes (and p at each
+// node's first copy) are fetched into shared memory by cp.async first -- every
+// load of the tile in flight at once, no registers held -- then each node's
+// chain is summed from shared memory and scattered.  Memory-level parallelism
+// of K_B is otherwise bounded by the registers of the per-thread node chains.
+// Dynamic shared memory: 2 index buffers, then the copy values and p values of
+// one tile (dssum_gather_smem).
+__device__ __forceinline__ void cp_async_4(void* dst_smem, const void* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* dst_smem, const void* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_t(T* dst_smem, const T* src)
+{
+    if constexpr (sizeof(T) == 4) cp_async_4(dst_smem, src); else cp_async_8(dst_smem, src);
+}
+
+template <typename T, bool FUSED, int PM = PM_NONE>
+__device__ __forceinline__ void dssum_tiles_gather(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
+                                                   int tile_smem, uint64_t* bars)
+{
+    constexpr bool PCOPY = FUSED && !pm_discontinuous(PM);
+    T* sval = reinterpret_cast<T*>(sbuf + 2 * tile_smem);      // tile_smem / 4 values
+    T* spv = sval + tile_smem / 4;                             // tile_smem / 8 values
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (int)blockIdx.x < a.ntiles)
+        tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - blockIdx.x : blockIdx.x, sbuf, &bars[0]);
+    int k = 0;
+    for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x, ++k) {
+        const int t = a.rev ? a.ntiles - 1 - i : i;
+        int s2, n2, s4, n4, s8, n8;
+        tile_range(a.toff, t, s2, n2, s4, n4, s8, n8);
+        const int b = k & 1;
+        const int inx = i + (int)gridDim.x;
+        if (threadIdx.x == 0 && inx < a.ntiles) {  // the other buffer was released by the last barrier
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - inx : inx,
+                       sbuf + (b ^ 1) * tile_smem, &bars[b ^ 1]);
+        }
+        mbar_wait(&bars[b], (k >> 1) & 1);
+        unsigned char* buf = sbuf + b * tile_smem;
+        const int b2 = (int)dssum_g2_bytes(s2, n2);
+        const int32_t* G2 = reinterpret_cast<const int32_t*>(buf + dssum_g2_lead(s2));
+        const int32_t* G4 = reinterpret_cast<const int32_t*>(buf + b2);
+        const int32_t* G8 = reinterpret_cast<const int32_t*>(buf + b2 + 16 * n4);
+        const int c2 = 2 * n2, c4 = c2 + 4 * n4, nc = c4 + 8 * n8, tot = n2 + n4 + n8;
+        // phase 1: every copy value (and p) of the tile in flight
+        for (int r = threadIdx.x; r < nc; r += blockDim.x) {
+            const int32_t ix = r < c2 ? G2[r] : (r < c4 ? G4[r - c2] : G8[r - c4]);
+            cp_async_t<T>(sval + r, a.w + ix);
+        }
+        if constexpr (PCOPY) {
+            for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+                const int32_t ix = q < n2 ? G2[2 * q] : (q < n2 + n4 ? G4[4 * (q - n2)] : G8[8 * (q - n2 - n4)]);
+                cp_async_t<T>(spv + q, a.p + ix);
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // phase 2: chains from shared memory (C4), scatter, pap
+        for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+            int m, r0;
+            const int32_t* row;
+            if (q < n2) { m = 2; r0 = 2 * q; row = G2 + r0; }
+            else if (q < n2 + n4) { m = 4; r0 = 4 * (q - n2); row = G4 + r0; r0 += c2; }
+            else { m = 8; r0 = 8 * (q - n2 - n4); row = G8 + r0; r0 += c4; }
+            T sum = sval[r0];
+            for (int c = 1; c < m; ++c) {
+                unsigned long long key = 0;
+                if constexpr (PM != PM_NONE)
+                    key = pm_key(a.it, PH_B, global_local_index(a.mesh, sl_natural(a.mesh, row[0])), c);
+                sum = padd<PM>(sum, sval[r0 + c], a.pm, key);
+            }
+            if (!FUSED && a.mask && masked_local<T>(a.mesh, row[0])) sum = 0;
+            for (int c = 0; c < m; ++c) a.w[row[c]] = sum;
+            if constexpr (FUSED && pm_discontinuous(PM)) {
+                const double cm = m == 2 ? 0.5 : (m == 4 ? 0.25 : 0.125);
+                for (int c = 0; c < m; ++c) acc.add(dot_term_pm<PM>(sum, __ldg(a.p + row[c]), cm, false, a.pm));
+            } else if constexpr (FUSED) {
+                add_node_pap<T, PM>(acc, sum, spv[q], m, a.single, a.pm);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 template <typename T, bool FUSED, int PM = PM_NONE>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_DSSUM_MINB64) k_dssum(DssumArgs<T> a)
 {
@@ -869,6 +972,10 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_D
     extern __shared__ __align__(128) unsigned char dsm_tiles[];
     __shared__ uint64_t dsm_bars[2];
     pdl_wait();
+#ifdef NBK_DSSUM_GATHER
+    if (a.stage) dssum_tiles_gather<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
+    else
+#endif
     dssum_tiles<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
     pdl_launch_dependents();
     if constexpr (FUSED) {

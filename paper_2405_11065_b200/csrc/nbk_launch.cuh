@@ -182,6 +182,18 @@ inline int dssum_stage_mode()
     return e ? atoi(e) : 1;
 }
 
+// dynamic shared memory of a staged K_B: two index buffers (+ the gather
+// variant's copy and p values of one tile)
+template <typename T>
+inline size_t dssum_stage_smem(int64_t tile_smem)
+{
+#ifdef NBK_DSSUM_GATHER
+    return 2 * (size_t)tile_smem + (size_t)tile_smem / 4 * sizeof(T) + (size_t)tile_smem / 8 * sizeof(T) + 16;
+#else
+    return 2 * (size_t)tile_smem;
+#endif
+}
+
 template <typename T, bool FUSED, int PM = PM_NONE>
 inline int dssum_grid_t(int ntiles, int64_t tile_smem, int* stage_out = nullptr)
 {
@@ -189,11 +201,19 @@ inline int dssum_grid_t(int ntiles, int64_t tile_smem, int* stage_out = nullptr)
     int stage = 0;
     int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 0);
     if (mode != 0) {
-        const int cap_s = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 2 * (size_t)tile_smem);
+        const int cap_s = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, dssum_stage_smem<T>(tile_smem));
         if (mode == 2 || ntiles >= 4 * cap_s) { stage = 1; cap = cap_s; }
     }
     if (stage_out) *stage_out = stage;
     return ntiles < 1 ? 1 : (ntiles > cap ? cap : ntiles);
+}
+
+// allow more than 48 KB of dynamic shared memory for a staged K_B (set-up, not captured)
+template <typename T, bool FUSED, int PM = PM_NONE>
+inline cudaError_t dssum_attrs()
+{
+    return cudaFuncSetAttribute(k_dssum<T, FUSED, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)dssum_stage_smem<T>(NBK_DSSUM_TILE_SMEM));
 }
 
 template <typename T, bool FUSED, int PM = PM_NONE>
@@ -201,7 +221,7 @@ inline cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl 
 {
     DssumArgs<T> d = a;
     const int grid = dssum_grid_t<T, FUSED, PM>(a.ntiles, a.tile_smem, &d.stage);
-    return launch_k(k_dssum<T, FUSED, PM>, grid, 256, d.stage ? 2 * (size_t)a.tile_smem : 0, s, pdl, d);
+    return launch_k(k_dssum<T, FUSED, PM>, grid, 256, d.stage ? dssum_stage_smem<T>(a.tile_smem) : 0, s, pdl, d);
 }
 
 // ------------------------------------------------------------ NCCL (dlopen)

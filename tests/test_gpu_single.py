@@ -198,7 +198,6 @@ def test_extreme_rhs_scaling_bitwise(nbk, ora, precision, scale_exp):
 
 
 # ------------------------------------------- the paper's binary32-accumulating solver (R11c)
-@pytest.mark.parametrize("args", [(2, 2, 2, 8, 0.0, 0, 1001), (3, 3, 3, 10, 0.1, 2005, 1005)])
 def _order_insensitive_window(ora, om, D, s, niter, ref):
     """Iterations over which the binary32-accumulating CG does not depend on the
     summation order: the oracle's own runs with 2 and 3 z-slabs (other, equally
@@ -213,6 +212,7 @@ def _order_insensitive_window(ora, om, D, s, niter, ref):
     return int(bad[0]) if len(bad) else niter + 1
 
 
+@pytest.mark.parametrize("args", [(2, 2, 2, 8, 0.0, 0, 1001), (3, 3, 3, 10, 0.1, 2005, 1005)])
 def test_accum32_solver_tracks_oracle(nbk, ora, args):
     """NEXT-2 as the paper ran it (R11c): binary32
     accumulation of every glsc3.  The oracle sums sequentially, the library by a
