@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
     const int nel = (int)((a.mesh.E - e0) < EPB ? (a.mesh.E - e0) : EPB);
     const bool valid = el < nel;
     const T* src_u = FUSED ? a.p : a.u;
+    NBK_ASSERT(nel >= 1 && e0 + nel <= a.mesh.E);
 
     T rreg[FUSED ? N : 1], xreg[FUSED ? N : 1], dreg[FUSED == 2 ? N : 1];
     // ---- stage G and u/p of the CTA's elements in shared memory.  G does not
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
     // storage of the thread's column (i, j, *): SL slots (CG vectors) or natural
     const SlCol cs = sl_col(N, i, j);
     const bool isl = FUSED || a.in_sl, osl = FUSED || a.out_sl;
+    NBK_ASSERT(!valid || (cs.at(N, 0) >= 0 && cs.at(N, N - 1) < N3 && cs.at(N, N / 2) < N3));
     auto gin = [&](int kk) -> int64_t { return isl ? e * N3 + cs.at(N, kk) : base + (int64_t)kk * N2; };
     auto gout = [&](int kk) -> int64_t { return osl ? e * N3 + cs.at(N, kk) : base + (int64_t)kk * N2; };
     T betaT = 0, alphaT = 0;
@@ -834,7 +836,10 @@ __device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, u
                 p0[h] = 0;
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                    if (c < m[h]) v[h][c] = a.w[ix[h][c]];
+                    if (c < m[h]) {
+                        NBK_ASSERT(ix[h][c] >= 0 && (int64_t)ix[h][c] < a.mesh.E * a.mesh.N * a.mesh.N * a.mesh.N);
+                        v[h][c] = a.w[ix[h][c]];
+                    }
                 if constexpr (FUSED && !pm_discontinuous(PM))
                     if (m[h]) p0[h] = __ldg(a.p + ix[h][0]);
             }
@@ -928,6 +933,8 @@ __device__ __forceinline__ void dssum_tiles_gather(const DssumArgs<T>& a, acc_t&
         // phase 1: every copy value (and p) of the tile in flight
         for (int r = threadIdx.x; r < nc; r += blockDim.x) {
             const int32_t ix = r < c2 ? G2[r] : (r < c4 ? G4[r - c2] : G8[r - c4]);
+            NBK_ASSERT(ix >= 0 && (int64_t)ix < a.mesh.E * a.mesh.N * a.mesh.N * a.mesh.N);
+            NBK_ASSERT(r < tile_smem / 4);
             cp_async_t<T>(sval + r, a.w + ix);
         }
         if constexpr (PCOPY) {
@@ -1282,6 +1289,7 @@ __device__ __forceinline__ void vec_loop(const VecArgs<T>& a, T am, acc_t& acc, 
         for (int u = 0; u < NBK_VEC_U; ++u) {
             const int64_t qu = q0 + u * stride;
             L[u] = (a.rev ? nch - 1 - qu : qu) * V;
+            NBK_ASSERT(L[u] >= 0 && L[u] + V <= a.n);
             C[u].load(a, L[u]);
         }
 #pragma unroll
@@ -1379,6 +1387,7 @@ __global__ void __launch_bounds__(256) k_vec_a(VecArgs<float> a)
     const int64_t nch = a.n / V, stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nch; q += stride) {
         const int64_t L = (a.rev ? nch - 1 - q : q) * V;
+        NBK_ASSERT(L >= 0 && L + V <= a.n);
         double c[V];
         chunk_weights_sl<V>(a.mesh, L, sl_tab, c);
         VecT<float, V> X, Y;
@@ -1479,6 +1488,7 @@ __global__ void __launch_bounds__(256) k_perm_sl(T* dst, const T* src, MeshView 
         const uint32_t q1 = fast_div(rem, m.n_mul, m.n_shr);
         const uint32_t q2 = fast_div(q1, m.n_mul, m.n_shr);
         const int64_t Ls = (int64_t)e * N3 + sl_slot(N, (int)(rem - q1 * N), (int)(q1 - q2 * N), (int)q2);
+        NBK_ASSERT(Ls >= (int64_t)e * N3 && Ls < (int64_t)(e + 1) * N3);
         if (TO_SL) dst[Ls] = src[L]; else dst[L] = src[Ls];
     }
 }

@@ -97,3 +97,23 @@ def test_partition_rejects_bad_rank_counts():
         nbk.partition(nbk.MeshSpec(4, 4, 6, 8), 4, 0)    # ez % P != 0
     with pytest.raises(nbk.NbkError):
         nbk.partition(nbk.MeshSpec(4, 4, 128, 8), 128, 0)  # > 64 ranks
+
+
+def test_bench_gpus_n_relaunches_under_torchrun():
+    """bench.py --gpus N outside torchrun re-executes itself under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous).  The reference
+    arm needs no GPU: rank 0 alone runs the oracle and prints the one JSON line
+    (n_gpus = N), the other ranks exit 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl",
+                          "reference", "--config", "C1", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
