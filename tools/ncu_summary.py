@@ -69,7 +69,7 @@ def stalls(h, r, top=5):
 def kernel_key(name):
     """Summary key of a CG-loop kernel: K_A k_ax<T, N, 1, 0>, K_B k_dssum<T, 1, 0>,
     K_C k_vec<T, V, 1, 0> (RUPD); None for the others."""
-    if "k_ax<" in name and name.replace(" ", "").endswith(",1,0>(AxArgs<T1>)"):
+    if "k_ax<" in name and name.replace(" ", "").split(">(")[0].endswith(",1,0"):
         return "k_ax_fused"
     if "k_dssum<" in name and ", 1, 0>" in name:
         return "k_dssum_fused"
