@@ -187,7 +187,9 @@ inline int dssum_stage_mode()
 template <typename T>
 inline size_t dssum_stage_smem(int64_t tile_smem)
 {
-#ifdef NBK_DSSUM_GATHER
+#if defined(NBK_DSSUM_GATHER2)
+    return 3 * (size_t)tile_smem + 2 * (size_t)dssum_vbuf_bytes<T>((int)tile_smem);
+#elif defined(NBK_DSSUM_GATHER)
     return 2 * (size_t)tile_smem + (size_t)tile_smem / 4 * sizeof(T) + (size_t)tile_smem / 8 * sizeof(T) + 16;
 #else
     return 2 * (size_t)tile_smem;
