@@ -655,11 +655,14 @@ __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, doubl
 #ifndef NBK_DSSUM_H
 #define NBK_DSSUM_H 2   // nodes per thread per step
 #endif
+// CTAs per SM of K_B (launch bounds; registers).  With the gather phase the
+// chains need few registers: 6 (FP32) / 4 (FP64) CTAs with 512-node tiles,
+// measured same-box: C5 FP64 K_B 0.74 vs 0.86 ms, C4 0.25 vs 0.29 ms, FP32 equal.
 #ifndef NBK_DSSUM_MINB64
-#define NBK_DSSUM_MINB64 2   // FP64: no spills at 2 CTAs per SM (+1.5 % FP64 C2 vs 3)
+#define NBK_DSSUM_MINB64 4
 #endif
 #ifndef NBK_DSSUM_MINB32
-#define NBK_DSSUM_MINB32 4
+#define NBK_DSSUM_MINB32 6
 #endif
 template <typename T>
 struct DssumArgs {
@@ -972,129 +975,14 @@ __device__ __forceinline__ void dssum_tiles_gather(const DssumArgs<T>& a, acc_t&
     }
 }
 
-// Double-buffered gather (NBK_DSSUM_GATHER2): three index buffers (TMA, two
-// tiles ahead) and two value buffers (cp.async, one tile ahead), so the copies
-// of tile k+1 are in flight while tile k is summed and scattered.
-struct TileView {
-    const int32_t *G2, *G4, *G8;
-    int n2, n4, n8;
-};
-__device__ __forceinline__ TileView tile_view(const int32_t* toff, int t, unsigned char* buf)
-{
-    int s2, n2, s4, n4, s8, n8;
-    tile_range(toff, t, s2, n2, s4, n4, s8, n8);
-    const int b2 = (int)dssum_g2_bytes(s2, n2);
-    TileView v;
-    v.G2 = reinterpret_cast<const int32_t*>(buf + dssum_g2_lead(s2));
-    v.G4 = reinterpret_cast<const int32_t*>(buf + b2);
-    v.G8 = reinterpret_cast<const int32_t*>(buf + b2 + 16 * n4);
-    v.n2 = n2; v.n4 = n4; v.n8 = n8;
-    return v;
-}
-template <typename T, bool PCOPY>
-__device__ __forceinline__ void tile_gather(const DssumArgs<T>& a, const TileView& v, T* sval, T* spv)
-{
-    const int c2 = 2 * v.n2, c4 = c2 + 4 * v.n4, nc = c4 + 8 * v.n8, tot = v.n2 + v.n4 + v.n8;
-    for (int r = threadIdx.x; r < nc; r += blockDim.x) {
-        const int32_t ix = r < c2 ? v.G2[r] : (r < c4 ? v.G4[r - c2] : v.G8[r - c4]);
-        NBK_ASSERT(ix >= 0 && (int64_t)ix < a.mesh.E * a.mesh.N * a.mesh.N * a.mesh.N);
-        cp_async_t<T>(sval + r, a.w + ix);
-    }
-    if constexpr (PCOPY) {
-        for (int q = threadIdx.x; q < tot; q += blockDim.x) {
-            const int32_t ix = q < v.n2 ? v.G2[2 * q]
-                                        : (q < v.n2 + v.n4 ? v.G4[4 * (q - v.n2)] : v.G8[8 * (q - v.n2 - v.n4)]);
-            cp_async_t<T>(spv + q, a.p + ix);
-        }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <typename T>
-__host__ __device__ constexpr int dssum_vbuf_bytes(int tile_smem)
-{
-    return ((tile_smem / 4 * (int)sizeof(T) + tile_smem / 8 * (int)sizeof(T)) + 15) & ~15;
-}
-
-template <typename T, bool FUSED, int PM = PM_NONE>
-__device__ __forceinline__ void dssum_tiles_gather2(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
-                                                    int tile_smem, uint64_t* bars)
-{
-    constexpr bool PCOPY = FUSED && !pm_discontinuous(PM);
-    const int VB = dssum_vbuf_bytes<T>(tile_smem);
-    unsigned char* vbase = sbuf + 3 * tile_smem;
-    const int K = a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    auto tid_of = [&](int k) { const int i = blockIdx.x + k * gridDim.x; return a.rev ? a.ntiles - 1 - i : i; };
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], 1);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (K > 0) tile_stage(a.g2, a.g4, a.g8, a.toff, tid_of(0), sbuf, &bars[0]);
-        if (K > 1) tile_stage(a.g2, a.g4, a.g8, a.toff, tid_of(1), sbuf + tile_smem, &bars[1]);
-    }
-    if (K > 0) {
-        mbar_wait(&bars[0], 0);
-        T* sv = reinterpret_cast<T*>(vbase);
-        tile_gather<T, PCOPY>(a, tile_view(a.toff, tid_of(0), sbuf), sv, sv + tile_smem / 4);
-    }
-    for (int k = 0; k < K; ++k) {
-        const int ib = k % 3, vb = k & 1;
-        if (k + 1 < K) {  // the next tile's copies in flight during this tile's chains
-            const int jb = (k + 1) % 3;
-            mbar_wait(&bars[jb], ((k + 1) / 3) & 1);
-            T* sv = reinterpret_cast<T*>(vbase + (vb ^ 1) * VB);
-            tile_gather<T, PCOPY>(a, tile_view(a.toff, tid_of(k + 1), sbuf + jb * tile_smem), sv, sv + tile_smem / 4);
-        }
-        if (threadIdx.x == 0 && k + 2 < K) {  // buffer (k+2)%3 was released by the last barrier
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tile_stage(a.g2, a.g4, a.g8, a.toff, tid_of(k + 2), sbuf + ((k + 2) % 3) * tile_smem, &bars[(k + 2) % 3]);
-        }
-        if (k + 1 < K) asm volatile("cp.async.wait_group 1;" ::: "memory");
-        else asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
-        const TileView v = tile_view(a.toff, tid_of(k), sbuf + ib * tile_smem);
-        const T* sval = reinterpret_cast<const T*>(vbase + vb * VB);
-        const T* spv = sval + tile_smem / 4;
-        const int c2 = 2 * v.n2, c4 = c2 + 4 * v.n4, tot = v.n2 + v.n4 + v.n8;
-        for (int q = threadIdx.x; q < tot; q += blockDim.x) {
-            int m, r0;
-            const int32_t* row;
-            if (q < v.n2) { m = 2; r0 = 2 * q; row = v.G2 + r0; }
-            else if (q < v.n2 + v.n4) { m = 4; r0 = 4 * (q - v.n2); row = v.G4 + r0; r0 += c2; }
-            else { m = 8; r0 = 8 * (q - v.n2 - v.n4); row = v.G8 + r0; r0 += c4; }
-            T sum = sval[r0];
-            for (int c = 1; c < m; ++c) {
-                unsigned long long key = 0;
-                if constexpr (PM != PM_NONE)
-                    key = pm_key(a.it, PH_B, global_local_index(a.mesh, sl_natural(a.mesh, row[0])), c);
-                sum = padd<PM>(sum, sval[r0 + c], a.pm, key);
-            }
-            if (!FUSED && a.mask && masked_local<T>(a.mesh, row[0])) sum = 0;
-            for (int c = 0; c < m; ++c) a.w[row[c]] = sum;
-            if constexpr (FUSED && pm_discontinuous(PM)) {
-                const double cm = m == 2 ? 0.5 : (m == 4 ? 0.25 : 0.125);
-                for (int c = 0; c < m; ++c) acc.add(dot_term_pm<PM>(sum, __ldg(a.p + row[c]), cm, false, a.pm));
-            } else if constexpr (FUSED) {
-                add_node_pap<T, PM>(acc, sum, spv[q], m, a.single, a.pm);
-            }
-        }
-        __syncthreads();
-    }
-}
-
 template <typename T, bool FUSED, int PM = PM_NONE>
 __global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_DSSUM_MINB64) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
     extern __shared__ __align__(128) unsigned char dsm_tiles[];
-    __shared__ uint64_t dsm_bars[3];
+    __shared__ uint64_t dsm_bars[2];
     pdl_wait();
-#if defined(NBK_DSSUM_GATHER2)
-    if (a.stage) dssum_tiles_gather2<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
-    else
-#elif defined(NBK_DSSUM_GATHER)
+#if defined(NBK_DSSUM_GATHER)
     if (a.stage) dssum_tiles_gather<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
     else
 #endif

@@ -187,9 +187,7 @@ inline int dssum_stage_mode()
 template <typename T>
 inline size_t dssum_stage_smem(int64_t tile_smem)
 {
-#if defined(NBK_DSSUM_GATHER2)
-    return 3 * (size_t)tile_smem + 2 * (size_t)dssum_vbuf_bytes<T>((int)tile_smem);
-#elif defined(NBK_DSSUM_GATHER)
+#if defined(NBK_DSSUM_GATHER)
     return 2 * (size_t)tile_smem + (size_t)tile_smem / 4 * sizeof(T) + (size_t)tile_smem / 8 * sizeof(T) + 16;
 #else
     return 2 * (size_t)tile_smem;
@@ -204,7 +202,12 @@ inline int dssum_grid_t(int ntiles, int64_t tile_smem, int* stage_out = nullptr)
     int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 0);
     if (mode != 0) {
         const int cap_s = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, dssum_stage_smem<T>(tile_smem));
-        if (mode == 2 || ntiles >= 4 * cap_s) { stage = 1; cap = cap_s; }
+#ifdef NBK_DSSUM_GATHER
+        const bool auto_stage = true;   // the gather phase works on staged tiles
+#else
+        const bool auto_stage = ntiles >= 4 * cap_s;
+#endif
+        if (mode == 2 || auto_stage) { stage = 1; cap = cap_s; }
     }
     if (stage_out) *stage_out = stage;
     return ntiles < 1 ? 1 : (ntiles > cap ? cap : ntiles);

@@ -553,7 +553,7 @@ cudaError_t build_plan(nbk_ctx* ctx)
     // dssum tiles: ~tile_nodes nodes per tile (several per thread of a 256-thread block)
     const int64_t N3 = (int64_t)ctx->N * ctx->N * ctx->N;
     const int64_t per_elem = (ns + ctx->E - 1) / ctx->E;
-    int64_t tile_nodes = 1024;
+    int64_t tile_nodes = 512;   // K_B gather phase: 512-node tiles
     if (const char* env = getenv("NBK_DSSUM_TILE_NODES")) tile_nodes = atol(env) > 0 ? atol(env) : tile_nodes;
     int64_t te = (tile_nodes + per_elem - 1) / per_elem;
     if (te < 1) te = 1;
