@@ -796,7 +796,7 @@ nbk_status nbk_solve_launches(const nbk_ctx* c, int32_t niter, nbk_precision pre
     const int64_t multi = c->nranks > 1 ? 1 : 0;
     // init (+fin), per iteration K_A, K_B, K_C (+ pack, merge, 2 fin), tail_x, [upcast],
     // final check K_A, K_B, K_C (+ pack, merge, fin)
-    *launches = (1 + multi) + (3 + 4 * multi) * (int64_t)niter + 1 +
+    *launches = (1 + multi) + (2 + 4 * multi + ka_launches(c, multi != 0)) * (int64_t)niter + 1 +
                 ((prec == NBK_FP32 || prec == NBK_FP32S || prec == NBK_FP32A) ? 1 : 0) +
                 (prec == NBK_FP32A ? (1 + multi) * (int64_t)niter : 0) +   // the binary32 pap kernel (+ fin)
                 (3 + 3 * multi);

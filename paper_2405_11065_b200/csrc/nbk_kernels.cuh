@@ -199,6 +199,11 @@ struct AxArgs {
     int p_ready;       // fused: p is final before the PDL wait (CG iterations >= 2)
     int in_sl, out_sl; // plain ax: u / w in the split layout (SL) instead of natural order
                        // (the fused CG step always works on SL vectors)
+    // element ranges of this launch: blocks cover [eb0, eb0 + en0) then
+    // [eb1, eb1 + en1) (multi-rank: the slab-boundary layers first, so the face
+    // exchange overlaps the interior elements); pap partials at part_off + block
+    int64_t eb0, en0, eb1, en1;
+    int part_off;
 };
 
 // D as a kernel parameter: k_ax reads D[k][*] (t-derivative, t-transpose) with
@@ -237,9 +242,12 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
     const int tid = threadIdx.x;
     const int el = tid / N2, ij = tid - el * N2;
     const int i = ij % N, j = ij / N;
-    const int64_t e0 = (int64_t)(a.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * EPB;
+    const int64_t bl = (int64_t)(a.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
+    const int64_t nb0 = (a.en0 + EPB - 1) / EPB;
+    const int64_t e0 = bl < nb0 ? a.eb0 + bl * EPB : a.eb1 + (bl - nb0) * EPB;
+    const int64_t eend = bl < nb0 ? a.eb0 + a.en0 : a.eb1 + a.en1;
     const int64_t e = e0 + el;
-    const int nel = (int)((a.mesh.E - e0) < EPB ? (a.mesh.E - e0) : EPB);
+    const int nel = (int)((eend - e0) < EPB ? (eend - e0) : EPB);
     const bool valid = el < nel;
     const T* src_u = FUSED ? a.p : a.u;
     NBK_ASSERT(nel >= 1 && e0 + nel <= a.mesh.E);
@@ -518,7 +526,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
     pdl_launch_dependents();
     if constexpr (FUSED) {
         dd v = block_reduce_dd(acc.get());
-        if (threadIdx.x == 0) a.parts[blockIdx.x] = v;
+        if (threadIdx.x == 0) a.parts[a.part_off + blockIdx.x] = v;
     }
     if constexpr (TIO) {
         if (tid == 0) bulk_wait_all();   // shared memory stays valid until the stores are done

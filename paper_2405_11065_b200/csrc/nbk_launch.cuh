@@ -73,7 +73,8 @@ inline cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_onl
     if (attr_only)
         return cudaFuncSetAttribute(k_ax<T, N, FUSED, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem);
-    const unsigned grid = (unsigned)((a.mesh.E + EPB - 1) / EPB);
+    const unsigned grid = (unsigned)((a.en0 + EPB - 1) / EPB + (a.en1 + EPB - 1) / EPB);
+    if (grid == 0) return cudaSuccess;
     DConst<T> dc{};
     for (int q = 0; q < N * N; ++q) dc.v[q] = a.Dh[q];
     return launch_k(k_ax<T, N, FUSED, PM>, grid, ax_threads<T>(N), smem, s, pdl, a, dc);
@@ -359,6 +360,7 @@ template <typename T>
 inline AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
 {
     AxArgs<T> a{};
+    a.eb0 = 0; a.en0 = c->E; a.eb1 = 0; a.en1 = 0; a.part_off = 0;   // all elements, one range
     a.D = D;
     if constexpr (sizeof(T) == 8) a.Dh = (const T*)c->Dh64; else a.Dh = (const T*)c->Dh32;
     a.G = G;
@@ -368,13 +370,6 @@ inline AxArgs<T> ax_args(nbk_ctx* c, const T* D, const T* G)
     return a;
 }
 
-template <typename T, int PM = PM_NONE>
-inline int ax_blocks_n(int64_t E, int N)
-{
-#define EPBN(n) (int)((E + ax_epb<T>(n) - 1) / ax_epb<T>(n))
-    NBK_SWITCH_N(N, EPBN)
-#undef EPBN
-}
 
 template <typename T>
 inline DssumArgs<T> dssum_args(nbk_ctx* c, T* w)
@@ -402,6 +397,79 @@ inline FaceArgs<T> face_args(nbk_ctx* c, T* w)
 // vector kernels: two banks of NBK_VEC_GRID_MAX partials (rtr, rtz) at the end
 inline dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - 2 * NBK_VEC_GRID_MAX; }
 
+// Pack the slab-boundary face layers of every member and start the exchange
+// (NCCL send / recv on each member's comm stream, event fork / join).
+template <typename T>
+inline cudaError_t faces_begin(const Team& t, const std::vector<T*>& w, std::string& err)
+{
+    cudaError_t e;
+    for (size_t q = 0; q < t.m.size(); ++q) {
+        FaceArgs<T> f = face_args<T>(t.m[q], w[q]);
+        k_face_pack<T><<<vec_grid(2 * t.m[q]->nlayer), 256, 0, t.s>>>(f);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    for (nbk_ctx* c : t.m) {
+        if (!c->comm) continue;
+        if ((e = cudaEventRecord(c->ev_pack, t.s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0)) != cudaSuccess) return e;
+        if ((e = xchg_faces<T>(team_self(c), c->comm_stream, err)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(c->ev_xchg, c->comm_stream)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// Element ranges of the fused K_A of one member.  One rank: everything.  Several
+// ranks: launch 0 = the element layers at the slab faces that are exchanged
+// (bottom if has_lo, top if has_hi), launch 1 = the interior layers.
+struct KaSplit {
+    int64_t eb[2][2], en[2][2];   // [launch][range]
+};
+inline KaSplit ka_split(const nbk_ctx* c, bool multi)
+{
+    KaSplit k{};
+    if (!multi) {
+        k.en[0][0] = c->E;
+        return k;
+    }
+    const int64_t exy = (int64_t)c->view.ex * c->view.ey, L = c->view.ez_local;
+    const bool lo = c->has_lo, hi = c->has_hi && (L > 1 || !lo);
+    if (lo) { k.eb[0][0] = 0; k.en[0][0] = exy; }
+    if (hi) { k.eb[0][1] = (L - 1) * exy; k.en[0][1] = exy; }
+    const int64_t ib = lo ? exy : 0, ie = (hi ? (L - 1) * exy : L * exy);
+    if (ie > ib) { k.eb[1][0] = ib; k.en[1][0] = ie - ib; }
+    return k;
+}
+// K_A blocks over n elements (EPB elements per block)
+template <typename T>
+inline int ka_blocks(const nbk_ctx* c, int64_t n)
+{
+    int epb = 1;
+#define EPBC(nn) case nn: epb = ax_epb<T>(nn); break;
+    switch (c->N) {
+    EPBC(2) EPBC(3) EPBC(4) EPBC(5) EPBC(6) EPBC(7) EPBC(8) EPBC(9) EPBC(10) EPBC(11) EPBC(12)
+    EPBC(13) EPBC(14) EPBC(15) EPBC(16)
+    default: break;
+    }
+#undef EPBC
+    return (int)((n + epb - 1) / epb);
+}
+// K_A launches of a member in one CG step (an empty launch is skipped)
+inline int ka_launches(const nbk_ctx* c, bool multi)
+{
+    const KaSplit k = ka_split(c, multi);
+    return (k.en[0][0] + k.en[0][1] > 0 ? 1 : 0) + (k.en[1][0] + k.en[1][1] > 0 ? 1 : 0);
+}
+// K_A pap partials of a member in the CG step (all launches)
+template <typename T, int PM = PM_NONE>
+inline int ka_parts(const nbk_ctx* c, bool multi)
+{
+    const KaSplit k = ka_split(c, multi);
+    int n = 0;
+    for (int l = 0; l < 2; ++l)
+        for (int r = 0; r < 2; ++r) n += ka_blocks<T>(c, k.en[l][r]);
+    return n;
+}
+
 // dssum (+ mask) of w over a team.  fused: shared-node pap terms, alpha.
 // One rank: K_B (its last block forms alpha).  Several: K_B (publish only) and
 // the face pack, exchange, face merge (reduces this rank's pap), all-gather,
@@ -409,28 +477,17 @@ inline dd* vec_parts(nbk_ctx* c) { return c->parts + c->nparts - 2 * NBK_VEC_GRI
 template <typename T, bool FUSED, int PM = PM_NONE>
 inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std::vector<const T*>& p,
                               int mask, bool pdl, std::string& err, int rev = 0, int single = 0,
-                              PmArgs pm = PmArgs{52, 0}, int it = 0)
+                              PmArgs pm = PmArgs{52, 0}, int it = 0, bool faces_started = false)
 {
     cudaError_t e;
     const cudaStream_t s = t.s;
-    // Several ranks: pack the slab-boundary face layers first (K_B never
-    // touches plane nodes), so that the NCCL face exchange runs on the
-    // context's comm stream while K_B sums the local shared nodes; the merge
-    // waits for both.  (Virtual slabs: the exchange is pointer aliasing.)
-    if (t.multi) {
-        for (size_t q = 0; q < t.m.size(); ++q) {
-            FaceArgs<T> f = face_args<T>(t.m[q], w[q]);
-            k_face_pack<T><<<vec_grid(2 * t.m[q]->nlayer), 256, 0, s>>>(f);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        }
-        for (nbk_ctx* c : t.m) {
-            if (!c->comm) continue;
-            if ((e = cudaEventRecord(c->ev_pack, s)) != cudaSuccess) return e;
-            if ((e = cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0)) != cudaSuccess) return e;
-            if ((e = xchg_faces<T>(team_self(c), c->comm_stream, err)) != cudaSuccess) return e;
-            if ((e = cudaEventRecord(c->ev_xchg, c->comm_stream)) != cudaSuccess) return e;
-        }
-    }
+    // Several ranks: pack the slab-boundary face layers and start their NCCL
+    // exchange on the comm stream (faces_begin) -- in the CG step right after
+    // K_A's slab-boundary layers, so that it overlaps the interior elements'
+    // ax and the local dssum (K_B never touches plane nodes); the merge waits
+    // for both.  (Virtual slabs: the exchange is pointer aliasing.)
+    if (t.multi && !faces_started)
+        if ((e = faces_begin<T>(t, w, err)) != cudaSuccess) return e;
     for (size_t q = 0; q < t.m.size(); ++q) {
         nbk_ctx* c = t.m[q];
         DssumArgs<T> d = dssum_args<T>(c, w[q]);
@@ -442,7 +499,7 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         if (FUSED) {
             d.p = p[q];
             d.parts = c->parts;
-            d.nA = ax_blocks_n<T, PM>(c->E, c->N);
+            d.nA = ka_parts<T, PM>(c, t.multi);
             d.fin = t.multi ? 0 : 1;
         }
         if ((e = launch_dssum<T, FUSED, PM>(d, s, pdl && !t.multi)) != cudaSuccess) return e;
@@ -457,8 +514,8 @@ inline cudaError_t dssum_team(const Team& t, const std::vector<T*>& w, const std
         f.single = single;
         if (FUSED) {
             f.p = p[q];
-            f.nprev = ax_blocks_n<T, PM>(c->E, c->N) + dssum_grid_t<T, FUSED, PM>((int)c->ntiles, c->tile_smem);
-            f.nskip = ax_blocks_n<T, PM>(c->E, c->N);
+            f.nprev = ka_parts<T, PM>(c, t.multi) + dssum_grid_t<T, FUSED, PM>((int)c->ntiles, c->tile_smem);
+            f.nskip = ka_parts<T, PM>(c, t.multi);
         }
         const int64_t nodes = (int64_t)(c->has_lo + c->has_hi) * c->nplane;
         k_face_merge<T, FUSED><<<vec_grid(nodes), 256, 0, s>>>(f);
@@ -636,24 +693,34 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
         const bool prof = g && profiling && P == 1;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1)], s, cudaEventRecordExternal);
         const bool pdl = !prof;  // events between kernels break PDL edges
-        for (size_t q = 0; q < P; ++q) {
-            nbk_ctx* c = t.m[q];
-            AxArgs<T> aa = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
-                                : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
-            aa.u = nullptr; aa.w = w[q]; aa.p = p[q]; aa.r = r[q]; aa.x = x[q]; aa.mask = 1;
-            aa.rev = rev;
-            aa.dinv = fld<T>(c, 4, fp32);
-            aa.single = single;
-            aa.pm = pm;
-            aa.it = k;
-            aa.p_ready = k >= 2 && g_p_early;
-            const bool pa = pdl && (g_pdl_mask & 1);
-            e = jac ? launch_ax<T, 2>(aa, s, false, pa) : launch_ax<T, 1, PM>(aa, s, false, pa);
-            if (e != cudaSuccess) return e;
+        // K_A; several ranks: slab-face layers, start of the face exchange, interior layers
+        for (int l = 0; l < (t.multi ? 2 : 1); ++l) {
+            if (l == 1 && (e = faces_begin<T>(t, w, err)) != cudaSuccess) return e;
+            for (size_t q = 0; q < P; ++q) {
+                nbk_ctx* c = t.m[q];
+                AxArgs<T> aa = fp32 ? ax_args<T>(c, (const T*)c->D32, (const T*)c->G32)
+                                    : ax_args<T>(c, (const T*)c->D64, (const T*)c->G64);
+                aa.u = nullptr; aa.w = w[q]; aa.p = p[q]; aa.r = r[q]; aa.x = x[q]; aa.mask = 1;
+                aa.rev = rev;
+                aa.dinv = fld<T>(c, 4, fp32);
+                aa.single = single;
+                aa.pm = pm;
+                aa.it = k;
+                aa.p_ready = k >= 2 && g_p_early;
+                const KaSplit ks = ka_split(c, t.multi);
+                aa.eb0 = ks.eb[l][0]; aa.en0 = ks.en[l][0];
+                aa.eb1 = ks.eb[l][1]; aa.en1 = ks.en[l][1];
+                aa.part_off = l == 0 ? 0 : ka_blocks<T>(c, ks.en[0][0]) + ka_blocks<T>(c, ks.en[0][1]);
+                const bool pa = pdl && (g_pdl_mask & 1) && l == 0;
+                e = jac ? launch_ax<T, 2>(aa, s, false, pa) : launch_ax<T, 1, PM>(aa, s, false, pa);
+                if (e != cudaSuccess) return e;
+            }
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 1], s, cudaEventRecordExternal);
         if (acc32) {
-            if ((e = dssum_team<T, false>(t, w, {}, 0, false, err, !rev)) != cudaSuccess) return e;
+            if ((e = dssum_team<T, false>(t, w, {}, 0, false, err, !rev, 0, PmArgs{52, 0}, 0, t.multi)) !=
+                cudaSuccess)
+                return e;
             if constexpr (sizeof(T) == 4) {
                 std::vector<VecArgs<float>> vp(P);
                 for (size_t q = 0; q < P; ++q) {
@@ -664,8 +731,8 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
                 if ((e = vec_a_team<VA_PAP>(t, vp, err)) != cudaSuccess) return e;
             }
             launches += (int64_t)P * (1 + per_fin);
-        } else if ((e = dssum_team<T, true, PM>(t, w, pc, 0, pdl && (g_pdl_mask & 2), err, !rev, single, pm, k)) !=
-                   cudaSuccess) {
+        } else if ((e = dssum_team<T, true, PM>(t, w, pc, 0, pdl && (g_pdl_mask & 2), err, !rev, single, pm, k,
+                                                t.multi)) != cudaSuccess) {
             return e;
         }
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 2], s, cudaEventRecordExternal);
@@ -686,7 +753,8 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
         if (e != cudaSuccess) return e;
         if (prof) cudaEventRecordWithFlags(g->prof_events[4 * (k - 1) + 3], s, cudaEventRecordExternal);
         rev = !rev;
-        launches += (int64_t)P * (3 + nface + 2 * per_fin);
+        launches += (int64_t)P * (2 + nface + 2 * per_fin);
+        for (size_t q = 0; q < P; ++q) launches += ka_launches(t.m[q], t.multi);
     }
     for (size_t q = 0; q < P; ++q) {
         nbk_ctx* c = t.m[q];
