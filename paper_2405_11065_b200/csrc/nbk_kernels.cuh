@@ -114,10 +114,16 @@ template <typename T>
 #ifndef NBK_EPB8_F64
 #define NBK_EPB8_F64 1
 #endif
+#ifndef NBK_EPB10_F32
+#define NBK_EPB10_F32 2
+#endif
+#ifndef NBK_AX_KP
+#define NBK_AX_KP 1   // planes per step of K_A's transpose pass (interleaved chains)
+#endif
 __host__ __device__ constexpr int ax_epb(int N)
 {
     if (N == 8) return sizeof(T) == 4 ? NBK_EPB8_F32 : NBK_EPB8_F64;
-    if (N == 10) return sizeof(T) == 4 ? 2 : 1;
+    if (N == 10) return sizeof(T) == 4 ? NBK_EPB10_F32 : 1;
     if (N == 12) return 1;
     int by_thr = 256 / (N * N) > 0 ? 256 / (N * N) : 1;
     int by_smem = (int)(57344 / (7 * N * N * N * (int)sizeof(T)));
@@ -487,30 +493,44 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
             lds_row<T, N>(Dci, sDt + i * N);   // D[:][i]
             lds_row<T, N>(Dcj, sDt + j * N);   // D[:][j]
         }
+        // KP planes per step: their chains are independent and interleaved
+        // (each point's chain keeps its canonical order)
+        constexpr int KP = (N % NBK_AX_KP == 0 && PM == PM_NONE) ? NBK_AX_KP : 1;
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
+        for (int k0 = 0; k0 < N; k0 += KP) {
             if constexpr (!DREG) {
                 lds_row<T, N>(Dci, sDt + i * N);
                 lds_row<T, N>(Dcj, sDt + j * N);
             }
-            T wrow[N];
-            lds_row<T, N>(wrow, wre + k * N2 + j * N);  // wr[k][j][:]
-            T s = 0;
+            T wrow[KP][N], s[KP];
 #pragma unroll
-            for (int l = 0; l < N; ++l) s = pfma<PM>(Dci[l], wrow[l], s, P, key(k, 11 + 3 * N + l));
+            for (int q = 0; q < KP; ++q) {
+                lds_row<T, N>(wrow[q], wre + (k0 + q) * N2 + j * N);  // wr[k][j][:]
+                s[q] = 0;
+            }
 #pragma unroll
             for (int l = 0; l < N; ++l)
-                s = pfma<PM>(Dcj[l], wse[k * N2 + l * N + i], s, P, key(k, 11 + 4 * N + l));
-            T wv = padd<PM>(s, b[k], P, key(k, 11 + 6 * N));
-            const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
-            if (a.mask && masked) wv = 0;   // C5: assign +0
-            if constexpr (TIO) sG[el * 6 * N3 + 2 * N3 + cs.at(N, k)] = wv;   // dead g3 slots, SL order
-            else a.w[gout(k)] = wv;
-            if constexpr (FUSED) {
-                // element-interior points (m == 1) contribute w p c here; shared
-                // nodes contribute once per node in K_B (bitwise-equal exact sum).
-                const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
-                if (!sxy && !sz) acc.add(dot_term_pm<PM>(wv, ureg[k], 1.0, a.single, P));
+#pragma unroll
+                for (int q = 0; q < KP; ++q) s[q] = pfma<PM>(Dci[l], wrow[q][l], s[q], P, key(k0 + q, 11 + 3 * N + l));
+#pragma unroll
+            for (int l = 0; l < N; ++l)
+#pragma unroll
+                for (int q = 0; q < KP; ++q)
+                    s[q] = pfma<PM>(Dcj[l], wse[(k0 + q) * N2 + l * N + i], s[q], P, key(k0 + q, 11 + 4 * N + l));
+#pragma unroll
+            for (int q = 0; q < KP; ++q) {
+                const int k = k0 + q;
+                T wv = padd<PM>(s[q], b[k], P, key(k, 11 + 6 * N));
+                const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
+                if (a.mask && masked) wv = 0;   // C5: assign +0
+                if constexpr (TIO) sG[el * 6 * N3 + 2 * N3 + cs.at(N, k)] = wv;   // dead g3 slots, SL order
+                else a.w[gout(k)] = wv;
+                if constexpr (FUSED) {
+                    // element-interior points (m == 1) contribute w p c here; shared
+                    // nodes contribute once per node in K_B (bitwise-equal exact sum).
+                    const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
+                    if (!sxy && !sz) acc.add(dot_term_pm<PM>(wv, ureg[k], 1.0, a.single, P));
+                }
             }
         }
     }
