@@ -834,3 +834,23 @@ def test_paper_single_solver_plausibility(ora):
     assert np.abs(r2.hist[:10] - ra.hist[:10]).max() / ra.hist[0] < 1e-5
     tr, h0 = ora.true_residual(m, D, s["G"], s["f"], ra.x)
     assert 1e-9 < tr / h0 < 1e-3
+
+
+def test_uniform_pm1_is_the_dyadic_map_of_splitmix64(ora):
+    """R7 / SURVEY 8(d): value = 2 U - 1 with U = (z >> 11) 2^-53, z the SplitMix64
+    output.  Pinned by structure and distribution rather than by the formula:
+    every value is a multiple of 2^-52 in [-1, 1) whose numerator's top bits are
+    those of z (so the map is monotone in z >> 11); the published stream of seed
+    0 gives the hand-computed first values; 2e4 samples pass a Kolmogorov-Smirnov
+    test against U[-1, 1) and have variance 1/3."""
+    for i, z in enumerate((0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F)):
+        k = z >> 11
+        assert ora.uniform_pm1(0, i) == math.ldexp(k, -52) - 1.0
+    v = np.array([ora.uniform_pm1(77, i) for i in range(20000)])
+    assert ((v + 1.0) * 2.0 ** 52 == np.floor((v + 1.0) * 2.0 ** 52)).all()
+    assert v.min() >= -1.0 and v.max() < 1.0
+    assert abs(v.var() - 1.0 / 3.0) < 0.02
+    from scipy import stats
+    assert stats.kstest(v, "uniform", args=(-1.0, 2.0)).pvalue > 1e-3
+    order = np.argsort([ora.splitmix64(77, i) >> 11 for i in range(200)], kind="stable")
+    assert (np.diff(v[:200][order]) >= 0).all()
