@@ -117,8 +117,11 @@ template <typename T>
 #ifndef NBK_EPB10_F32
 #define NBK_EPB10_F32 2
 #endif
-#ifndef NBK_AX_KP
-#define NBK_AX_KP 1   // planes per step of K_A's transpose pass (interleaved chains)
+#ifndef NBK_AX_KP32
+#define NBK_AX_KP32 1   // planes per step of K_A's transpose pass (interleaved chains), FP32
+#endif
+#ifndef NBK_AX_KP64
+#define NBK_AX_KP64 2   // ... FP64
 #endif
 __host__ __device__ constexpr int ax_epb(int N)
 {
@@ -495,7 +498,9 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
         }
         // KP planes per step: their chains are independent and interleaved
         // (each point's chain keeps its canonical order)
-        constexpr int KP = (N % NBK_AX_KP == 0 && PM == PM_NONE) ? NBK_AX_KP : 1;
+        // (FP64: 2 planes -- C5 FP64 K_A 5.32 vs 5.61 ms same-box; FP32: no gain, 1)
+        constexpr int KPW = sizeof(T) == 8 ? NBK_AX_KP64 : NBK_AX_KP32;
+        constexpr int KP = (N % KPW == 0 && PM == PM_NONE) ? KPW : 1;
 #pragma unroll
         for (int k0 = 0; k0 < N; k0 += KP) {
             if constexpr (!DREG) {
