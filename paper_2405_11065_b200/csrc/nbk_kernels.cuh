@@ -123,6 +123,9 @@ template <typename T>
 #ifndef NBK_AX_KP64
 #define NBK_AX_KP64 2   // ... FP64
 #endif
+#ifndef NBK_AX_G1P64
+#define NBK_AX_G1P64 1  // planes per step of K_A's gradient pass, FP64
+#endif
 __host__ __device__ constexpr int ax_epb(int N)
 {
     if (N == 8) return sizeof(T) == 4 ? NBK_EPB8_F32 : NBK_EPB8_F64;
@@ -436,47 +439,68 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
             lds_row<T, N>(Dri, sD + i * N);
             lds_row<T, N>(Drj, sD + j * N);
         }
+        // G1P planes per step (their ur / us / ut chains interleaved; the b update
+        // of plane k precedes that of plane k + 1, so every chain keeps its order)
+        constexpr int GW = sizeof(T) == 8 ? NBK_AX_G1P64 : 1;
+        constexpr int G1P = (N % GW == 0 && PM == PM_NONE) ? GW : 1;
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
+        for (int k0 = 0; k0 < N; k0 += G1P) {
             if constexpr (TMA) {
-                if (k == 0) mbar_wait(&bar[1], 0);
+                if (k0 == 0) mbar_wait(&bar[1], 0);
             }
             if constexpr (!DREG) {
                 lds_row<T, N>(Dri, sD + i * N);
                 lds_row<T, N>(Drj, sD + j * N);
             }
-            T urow[N], Dk[N];
-            lds_row<T, N>(urow, un + k * N2 + j * N);   // u[k][j][:]
+            T wtq[G1P];
+#pragma unroll
+            for (int q = 0; q < G1P; ++q) {
+                const int k = k0 + q;
+                T urow[N], Dk[N];
+                lds_row<T, N>(urow, un + k * N2 + j * N);   // u[k][j][:]
 #ifdef NBK_D_SMEM
-            lds_row<T, N>(Dk, sD + k * N);   // D[k][:] (broadcast)
+                lds_row<T, N>(Dk, sD + k * N);   // D[k][:] (broadcast)
 #else
 #pragma unroll
-            for (int l = 0; l < N; ++l) Dk[l] = dc.v[k * N + l];   // D[k][:] (kernel parameter)
+                for (int l = 0; l < N; ++l) Dk[l] = dc.v[k * N + l];   // D[k][:] (kernel parameter)
 #endif
-            T ur = 0, us = 0, ut = 0;
+                T ur = 0, us = 0, ut = 0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) ur = pfma<PM>(Dri[l], urow[l], ur, P, key(k, 2 + l));
+                for (int l = 0; l < N; ++l) ur = pfma<PM>(Dri[l], urow[l], ur, P, key(k, 2 + l));
 #pragma unroll
-            for (int l = 0; l < N; ++l) us = pfma<PM>(Drj[l], un[k * N2 + l * N + i], us, P, key(k, 2 + N + l));
+                for (int l = 0; l < N; ++l) us = pfma<PM>(Drj[l], un[k * N2 + l * N + i], us, P, key(k, 2 + N + l));
 #pragma unroll
-            for (int l = 0; l < N; ++l) ut = pfma<PM>(Dk[l], ureg[l], ut, P, key(k, 2 + 2 * N + l));
-            const T g1 = Ge[0 * N3 + k * N2], g2 = Ge[1 * N3 + k * N2], g3 = Ge[2 * N3 + k * N2];
-            const T g4 = Ge[3 * N3 + k * N2], g5 = Ge[4 * N3 + k * N2], g6 = Ge[5 * N3 + k * N2];
-            const int om = 2 + 3 * N;
-            T wr = pmul<PM>(g1, ur, P, key(k, om));
-            wr = pfma<PM>(g2, us, wr, P, key(k, om + 1));
-            wr = pfma<PM>(g3, ut, wr, P, key(k, om + 2));
-            T ws = pmul<PM>(g2, ur, P, key(k, om + 3));
-            ws = pfma<PM>(g4, us, ws, P, key(k, om + 4));
-            ws = pfma<PM>(g5, ut, ws, P, key(k, om + 5));
-            T wt = pmul<PM>(g3, ur, P, key(k, om + 6));
-            wt = pfma<PM>(g5, us, wt, P, key(k, om + 7));
-            wt = pfma<PM>(g6, ut, wt, P, key(k, om + 8));
-            // own (i,j,k) slot of g1/g2 is dead after the reads above
-            wre[k * N2 + ij] = wr;
-            wse[k * N2 + ij] = ws;
-            // b[kk] = fma(D[k][kk], wt, b[kk]): op 11+5N+k of point (i, j, kk)
-            fma_row<T, N, PM>(b, Dk, wt, &P, key(0, 11 + 5 * N + k), key(1, 0) - key(0, 0));
+                for (int l = 0; l < N; ++l) ut = pfma<PM>(Dk[l], ureg[l], ut, P, key(k, 2 + 2 * N + l));
+                const T g1 = Ge[0 * N3 + k * N2], g2 = Ge[1 * N3 + k * N2], g3 = Ge[2 * N3 + k * N2];
+                const T g4 = Ge[3 * N3 + k * N2], g5 = Ge[4 * N3 + k * N2], g6 = Ge[5 * N3 + k * N2];
+                const int om = 2 + 3 * N;
+                T wr = pmul<PM>(g1, ur, P, key(k, om));
+                wr = pfma<PM>(g2, us, wr, P, key(k, om + 1));
+                wr = pfma<PM>(g3, ut, wr, P, key(k, om + 2));
+                T ws = pmul<PM>(g2, ur, P, key(k, om + 3));
+                ws = pfma<PM>(g4, us, ws, P, key(k, om + 4));
+                ws = pfma<PM>(g5, ut, ws, P, key(k, om + 5));
+                T wt = pmul<PM>(g3, ur, P, key(k, om + 6));
+                wt = pfma<PM>(g5, us, wt, P, key(k, om + 7));
+                wt = pfma<PM>(g6, ut, wt, P, key(k, om + 8));
+                // own (i,j,k) slot of g1/g2 is dead after the reads above
+                wre[k * N2 + ij] = wr;
+                wse[k * N2 + ij] = ws;
+                wtq[q] = wt;
+            }
+#pragma unroll
+            for (int q = 0; q < G1P; ++q) {
+                const int k = k0 + q;
+                T Dk[N];
+#ifdef NBK_D_SMEM
+                lds_row<T, N>(Dk, sD + k * N);
+#else
+#pragma unroll
+                for (int l = 0; l < N; ++l) Dk[l] = dc.v[k * N + l];
+#endif
+                // b[kk] = fma(D[k][kk], wt, b[kk]): op 11+5N+k of point (i, j, kk)
+                fma_row<T, N, PM>(b, Dk, wtq[q], &P, key(0, 11 + 5 * N + k), key(1, 0) - key(0, 0));
+            }
         }
     }
     __syncthreads();
