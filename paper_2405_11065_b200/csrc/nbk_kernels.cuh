@@ -126,6 +126,9 @@ template <typename T>
 #ifndef NBK_AX_G1P64
 #define NBK_AX_G1P64 1  // planes per step of K_A's gradient pass, FP64
 #endif
+#ifndef NBK_AX_G1P32
+#define NBK_AX_G1P32 1  // ... FP32
+#endif
 __host__ __device__ constexpr int ax_epb(int N)
 {
     if (N == 8) return sizeof(T) == 4 ? NBK_EPB8_F32 : NBK_EPB8_F64;
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
         }
         // G1P planes per step (their ur / us / ut chains interleaved; the b update
         // of plane k precedes that of plane k + 1, so every chain keeps its order)
-        constexpr int GW = sizeof(T) == 8 ? NBK_AX_G1P64 : 1;
+        constexpr int GW = sizeof(T) == 8 ? NBK_AX_G1P64 : NBK_AX_G1P32;
         constexpr int G1P = (N % GW == 0 && PM == PM_NONE) ? GW : 1;
 #pragma unroll
         for (int k0 = 0; k0 < N; k0 += G1P) {
