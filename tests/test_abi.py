@@ -54,11 +54,23 @@ def test_kernels_are_sm100a_and_use_no_contraction(lib):
             funcs[cur] = []
         elif cur:
             funcs[cur].append(line)
-    fused64 = "\n".join(funcs["_ZN3nbk4k_axIdLi8ELi1ELi0EEEvNS_6AxArgsIT_EE"])
-    fused32 = "\n".join(funcs["_ZN3nbk4k_axIfLi8ELi1ELi0EEEvNS_6AxArgsIT_EE"])
+    def body(prefix):
+        names = [f for f in funcs if f.startswith(prefix)]
+        assert len(names) == 1, (prefix, names)
+        return "\n".join(funcs[names[0]])
+    fused64 = body("_ZN3nbk4k_axIdLi8ELi1ELi0EE")
+    fused32 = body("_ZN3nbk4k_axIfLi8ELi1ELi0EE")
     assert "DFMA" in fused64 and "FFMA" in fused32
     # TMA 1-D bulk copies (cp.async.bulk -> UBLKCP) stage G and p in shared memory
     assert "UBLKCP" in fused64 and "UBLKCP" in fused32
+    # N = 10 (TIO): r, x bulk-loaded and p, x, w bulk-stored -- no per-thread global
+    # loads / stores of the CG vectors, only the parameter / scalar loads
+    tio32 = body("_ZN3nbk4k_axIfLi10ELi1ELi0EE")
+    assert tio32.count("UBLKCP.G.S") >= 3 and tio32.count("UBLKCP.S.G") >= 3
+    assert tio32.count("STG") <= 2   # only the pap partial (dd) of the block
+    # K_B: compact plan rows staged by TMA, copies gathered by cp.async (LDGSTS)
+    kb32 = body("_ZN3nbk7k_dssumIfLb1ELi0EE")
+    assert "UBLKCP" in kb32 and "LDGSTS" in kb32
 
 
 def test_workspace_size_query_without_gpu_is_rejected_cleanly(lib):
