@@ -56,8 +56,7 @@ struct nbk_ctx {
     int64_t nparts = 0;
     int32_t *seg_off = nullptr, *seg_idx = nullptr;
     int32_t *grp = nullptr;                               // group index storage
-    int32_t *g2 = nullptr, *g4 = nullptr, *g8 = nullptr;  // segments grouped by multiplicity (set-up)
-    const uint16_t *h2 = nullptr, *h4 = nullptr, *h8 = nullptr;  // compact plan used by K_B
+    int32_t *g2 = nullptr, *g4 = nullptr, *g8 = nullptr;  // segments grouped by multiplicity
     int64_t n2 = 0, n4 = 0, n8 = 0, nother = 0;
     int32_t* toff = nullptr;              // dssum tiles: (ntiles + 1) x 3 offsets
     int64_t ntiles = 0, tile_elems = 1;

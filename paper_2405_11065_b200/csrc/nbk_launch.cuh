@@ -172,35 +172,62 @@ inline cudaError_t launch_vec(const VecArgs<T>& a, cudaStream_t s, bool pdl = fa
     return a.mesh.N % 2 == 0 ? launch_vec_v<T, 4, MODE, PM>(a, s, pdl) : launch_vec_v<T, 1, MODE, PM>(a, s, pdl);
 }
 
-// dynamic shared memory of K_B: two index buffers, the copy values and the p
-// values of one tile (a copy takes 2 bytes of index rows: <= tile_smem / 2
-// copies, <= tile_smem / 4 nodes)
+// K_B index staging: a block's next tile is prefetched while it processes the
+// current one, which only pays when blocks own several tiles (large meshes;
+// measured: C4 +2-4 %, C2 -2 % where every block owns one tile).
+// NBK_DSSUM_STAGE (read at every launch / graph capture): 0 off, 1 auto
+// (default: on when the tiles are >= 4 per block), 2 always (tests).
+inline int dssum_stage_mode()
+{
+    const char* e = getenv("NBK_DSSUM_STAGE");
+    return e ? atoi(e) : 1;
+}
+
+// dynamic shared memory of a staged K_B: two index buffers (+ the gather
+// variant's copy and p values of one tile)
 template <typename T>
 inline size_t dssum_stage_smem(int64_t tile_smem)
 {
-    return 2 * (size_t)tile_smem + (size_t)tile_smem / 2 * sizeof(T) + (size_t)tile_smem / 4 * sizeof(T) + 16;
+#if defined(NBK_DSSUM_GATHER)
+    return 2 * (size_t)tile_smem + (size_t)tile_smem / 4 * sizeof(T) + (size_t)tile_smem / 8 * sizeof(T) + 16;
+#else
+    return 2 * (size_t)tile_smem;
+#endif
 }
 
 template <typename T, bool FUSED, int PM = PM_NONE>
-inline int dssum_grid_t(int ntiles, int64_t tile_smem)
+inline int dssum_grid_t(int ntiles, int64_t tile_smem, int* stage_out = nullptr)
 {
-    const int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, dssum_stage_smem<T>(tile_smem));
+    const int mode = dssum_stage_mode();
+    int stage = 0;
+    int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 0);
+    if (mode != 0) {
+        const int cap_s = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, dssum_stage_smem<T>(tile_smem));
+#ifdef NBK_DSSUM_GATHER
+        const bool auto_stage = true;   // the gather phase works on staged tiles
+#else
+        const bool auto_stage = ntiles >= 4 * cap_s;
+#endif
+        if (mode == 2 || auto_stage) { stage = 1; cap = cap_s; }
+    }
+    if (stage_out) *stage_out = stage;
     return ntiles < 1 ? 1 : (ntiles > cap ? cap : ntiles);
 }
 
-// allow more than 48 KB of dynamic shared memory for K_B (set-up, not captured)
+// allow more than 48 KB of dynamic shared memory for a staged K_B (set-up, not captured)
 template <typename T, bool FUSED, int PM = PM_NONE>
 inline cudaError_t dssum_attrs()
 {
     return cudaFuncSetAttribute(k_dssum<T, FUSED, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)dssum_stage_smem<T>(NBK_DSSUM_TILE_SMEM + 16));
+                                (int)dssum_stage_smem<T>(NBK_DSSUM_TILE_SMEM));
 }
 
 template <typename T, bool FUSED, int PM = PM_NONE>
 inline cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl = false)
 {
-    const int grid = dssum_grid_t<T, FUSED, PM>(a.ntiles, a.tile_smem);   // >= 1: the last block forms alpha
-    return launch_k(k_dssum<T, FUSED, PM>, grid, 256, dssum_stage_smem<T>(a.tile_smem), s, pdl, a);
+    DssumArgs<T> d = a;
+    const int grid = dssum_grid_t<T, FUSED, PM>(a.ntiles, a.tile_smem, &d.stage);
+    return launch_k(k_dssum<T, FUSED, PM>, grid, 256, d.stage ? dssum_stage_smem<T>(a.tile_smem) : 0, s, pdl, d);
 }
 
 // ------------------------------------------------------------ NCCL (dlopen)
@@ -349,8 +376,8 @@ inline DssumArgs<T> dssum_args(nbk_ctx* c, T* w)
 {
     DssumArgs<T> d{};
     d.w = w;
-    d.h2 = c->h2; d.h4 = c->h4; d.h8 = c->h8;
-    d.toff = c->toff; d.ntiles = (int)c->ntiles; d.tile_smem = (int)c->tile_smem; d.te = (int)c->tile_elems;
+    d.g2 = c->g2; d.g4 = c->g4; d.g8 = c->g8;
+    d.toff = c->toff; d.ntiles = (int)c->ntiles; d.tile_smem = (int)c->tile_smem;
     d.st = c->st; d.trace = c->trace; d.mesh = c->view; d.mask = 0; d.fin = 1;
     return d;
 }

@@ -434,41 +434,6 @@ __global__ void __launch_bounds__(256) k_tile_offsets(const int32_t* g2, const i
     }
 }
 
-// Compact dssum plan: copy c of a node -> 16 bits: SL slot (12 bits) + element
-// code (3 bits): first copy -- its element minus the tile's first element
-// (te <= 8); other copies -- the offset a + b ex + c ex ey (a, b, c in {0, 1})
-// from the first copy's element, as code a + 2b + 4c.  *bad != 0 if a copy does
-// not fit.
-__global__ void __launch_bounds__(256) k_encode_compact(const int32_t* g2, const int32_t* g4, const int32_t* g8,
-                                                        int64_t n2, int64_t n4, int64_t n8, int64_t te,
-                                                        int64_t N3, MeshView m, uint16_t* h2, uint16_t* h4,
-                                                        uint16_t* h8, int32_t* bad)
-{
-    const int64_t exy = (int64_t)m.ex * m.ey;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n2 + n4 + n8;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t* row;
-        uint16_t* out;
-        int mm;
-        if (q < n2) { mm = 2; row = g2 + 2 * q; out = h2 + 2 * q; }
-        else if (q < n2 + n4) { mm = 4; row = g4 + 4 * (q - n2); out = h4 + 4 * (q - n2); }
-        else { mm = 8; row = g8 + 8 * (q - n2 - n4); out = h8 + 8 * (q - n2 - n4); }
-        const int64_t e0 = row[0] / N3;
-        const int64_t t = e0 / te;
-        const int64_t s0 = row[0] - e0 * N3;
-        if (s0 > 0xFFF || e0 - t * te > 7) atomicExch(bad, 1);
-        out[0] = (uint16_t)(((e0 - t * te) << 12) | s0);
-        for (int c = 1; c < mm; ++c) {
-            const int64_t ec = row[c] / N3, sc = row[c] - ec * N3, d = ec - e0;
-            int code = -1;
-            for (int k = 0; k < 8 && code < 0; ++k)
-                if ((k & 1) + ((k >> 1) & 1) * (int64_t)m.ex + (k >> 2) * exy == d) code = k;
-            if (code < 0 || sc > 0xFFF) { atomicExch(bad, 1); code = 0; }
-            out[c] = (uint16_t)((code << 12) | sc);
-        }
-    }
-}
-
 static int grid_for(int64_t n, int cap = 148 * 16)
 {
     int64_t g = (n + 255) / 256;
@@ -592,7 +557,6 @@ cudaError_t build_plan(nbk_ctx* ctx)
     if (const char* env = getenv("NBK_DSSUM_TILE_NODES")) tile_nodes = atol(env) > 0 ? atol(env) : tile_nodes;
     int64_t te = (tile_nodes + per_elem - 1) / per_elem;
     if (te < 1) te = 1;
-    if (te > 8) te = 8;   // the compact plan names a first copy's element in 3 bits
     // K_B stages each tile's index rows in shared memory (double-buffered bulk
     // copies): halve the tile until its rows fit NBK_DSSUM_TILE_SMEM bytes.
     std::vector<int32_t> th;
@@ -608,37 +572,14 @@ cudaError_t build_plan(nbk_ctx* ctx)
         if (err != cudaSuccess) return err;
         int64_t mx = 0;
         for (int64_t t = 0; t < ctx->ntiles; ++t) {
-            const int64_t b = nbk::dssum_tile_bytes(th[3 * t], th[3 * t + 3] - th[3 * t], th[3 * t + 1],
+            const int64_t b = nbk::dssum_tile_bytes(th[3 * t], th[3 * t + 3] - th[3 * t],
                                                     th[3 * t + 4] - th[3 * t + 1], th[3 * t + 5] - th[3 * t + 2]);
             mx = b > mx ? b : mx;
         }
-        ctx->tile_smem = (mx + 15) & ~(int64_t)15;
+        ctx->tile_smem = mx;
         if (mx <= NBK_DSSUM_TILE_SMEM || te == 1) break;
         te = (te + 1) / 2;
     }
-    // compact plan (16-bit copies, nbk_kernels.cuh K_B): encoded into the
-    // scratch region, then copied over the int32 rows
-    const int64_t b2 = (4 * ctx->n2 + 15) & ~(int64_t)15, b4 = (8 * ctx->n4 + 15) & ~(int64_t)15;
-    uint16_t* hs = (uint16_t*)base;
-    int32_t* bad = (int32_t*)(base + align256(b2 + b4 + 16 * ctx->n8 + 16));
-    err = cudaMemsetAsync(bad, 0, 4, s);
-    if (err != cudaSuccess) return err;
-    const int64_t rows = ctx->n2 + ctx->n4 + ctx->n8;
-    if (rows > 0)
-        k_encode_compact<<<grid_for(rows), 256, 0, s>>>(ctx->g2, ctx->g4, ctx->g8, ctx->n2, ctx->n4, ctx->n8,
-                                                        te, N3, ctx->view, hs, hs + b2 / 2, hs + (b2 + b4) / 2,
-                                                        bad);
-    err = cudaMemcpyAsync(ctx->grp, hs, b2 + b4 + 16 * ctx->n8, cudaMemcpyDeviceToDevice, s);
-    if (err != cudaSuccess) return err;
-    int32_t hbad = 0;
-    err = cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s);
-    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
-    if (err != cudaSuccess) return err;
-    if (hbad) return cudaErrorInvalidValue;   // a copy outside the 2 x 2 x 2 elements of its node
-    ctx->h2 = (const uint16_t*)ctx->grp;
-    ctx->h4 = (const uint16_t*)((const unsigned char*)ctx->grp + b2);
-    ctx->h8 = (const uint16_t*)((const unsigned char*)ctx->grp + b2 + b4);
-    ctx->g2 = ctx->g4 = ctx->g8 = nullptr;   // the int32 rows are gone
     return cudaGetLastError();
 }
 

@@ -1,7 +1,5 @@
-"""K_B (compact 16-bit plan rows staged in shared memory by double-buffered bulk
-copies, gather phase) on many small tiles per block and on virtual slabs:
-bitwise against the oracle.  (NBK_DSSUM_STAGE is accepted but staging is
-always on since the gather phase; the fixtures keep exercising the paths.)
+"""K_B with the tile index rows staged in shared memory (double-buffered bulk
+copies, NBK_DSSUM_STAGE): the staged kernel must give the unstaged bits.
 
 NBK_DSSUM_STAGE=2 forces staging on the small meshes the oracle can follow;
 NBK_DSSUM_TILE_NODES=64 cuts C2 into ~4096 one-element tiles so that every
