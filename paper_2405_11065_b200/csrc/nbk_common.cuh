@@ -488,20 +488,23 @@ __device__ __forceinline__ float add_t<float>(float a, float b)
 // Byte layout of one dssum tile's index rows in shared memory: the g2 rows
 // (8 B each) from the 16-byte boundary at or below the first, rounded up to 16
 // bytes, then the g4 rows (16 B), then the g8 rows (32 B).
-#ifndef NBK_DSSUM_TILE_SMEM
-#define NBK_DSSUM_TILE_SMEM 11264   // bytes of compact index rows per staging buffer (two buffers)
+// K_B gathers each staged tile's copies into shared memory first (cp.async;
+// measured same-box: C5 FP32 K_B 0.53 vs 0.63 ms, C4 0.18 vs 0.23 ms);
+// NBK_DSSUM_NOGATHER restores the per-thread chains.
+#if !defined(NBK_DSSUM_NOGATHER) && !defined(NBK_DSSUM_GATHER)
+#define NBK_DSSUM_GATHER 1
 #endif
-// Compact dssum plan (K_B): a group with rows of R bytes (4, 8, 16 for m = 2,
-// 4, 8 copies of 2 bytes); a tile's rows [s, s + n) are staged as the 16-byte
-// aligned byte range around them.
-__host__ __device__ inline int64_t dssum_grp_lead(int64_t R, int64_t s) { return (R * s) & 15; }
-__host__ __device__ inline int64_t dssum_grp_bytes(int64_t R, int64_t s, int64_t n)
+#ifndef NBK_DSSUM_TILE_SMEM
+#define NBK_DSSUM_TILE_SMEM 22528   // per buffer; two buffers per CTA
+#endif
+__host__ __device__ inline int64_t dssum_g2_lead(int64_t s2) { return (8 * s2) & 15; }
+__host__ __device__ inline int64_t dssum_g2_bytes(int64_t s2, int64_t n2)
 {
-    return n ? ((R * (s + n) + 15) & ~(int64_t)15) - ((R * s) & ~(int64_t)15) : 0;
+    return n2 ? ((8 * (s2 + n2) + 15) & ~(int64_t)15) - ((8 * s2) & ~(int64_t)15) : 0;
 }
-__host__ __device__ inline int64_t dssum_tile_bytes(int64_t s2, int64_t n2, int64_t s4, int64_t n4, int64_t n8)
+__host__ __device__ inline int64_t dssum_tile_bytes(int64_t s2, int64_t n2, int64_t n4, int64_t n8)
 {
-    return dssum_grp_bytes(4, s2, n2) + dssum_grp_bytes(8, s4, n4) + 16 * n8;
+    return dssum_g2_bytes(s2, n2) + 16 * n4 + 32 * n8;
 }
 
 // ------------------------------------------------------------ TMA / mbarrier

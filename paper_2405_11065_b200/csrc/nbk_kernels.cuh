@@ -704,23 +704,20 @@ __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, doubl
 
 // ---------------------------------------------------------------- K_B
 // The dssum plan groups the segments (unique shared nodes) by multiplicity
-// m in {2, 4, 8}: group m is a dense array of m copies per node, ascending in
-// the NATURAL local index (the chain order C4), each group ordered by the
-// node's first copy.  The domain is cut into tiles of te <= 8 consecutive
-// elements; toff[3t + g] is the first node of group g whose first copy lies in
-// tile t or later.  A copy is stored in 16 bits (the compact plan, 4 B per node
-// of m = 2 instead of 8): the 12 low bits are its SL slot in its element
-// (N^3 <= 4096), the 3 high bits name the element -- for the first copy its
-// offset from the tile's first element, for the others its offset from the
-// first copy's element, a + b ex + c ex ey with a, b, c in {0, 1} (the copies
-// of a node lie in the 2 x 2 x 2 elements around it).  A block processes whole
-// tiles: the tile's rows are bulk-copied (TMA) into shared memory one tile
-// ahead, every copy value (and p at each node's first copy) is gathered into
-// shared memory by cp.async -- the whole tile's loads in flight at once --
-// then each node's chain is summed from shared memory and scattered.
-// CTAs per SM of K_B (launch bounds; registers): 6 (FP32) / 4 (FP64) with
-// 512-node tiles, measured same-box: C5 FP64 K_B 0.74 vs 0.86 ms (4 / 2 CTAs,
-// 1024 nodes), C4 0.25 vs 0.29 ms, FP32 equal.
+// m in {2, 4, 8}: group m is a dense int32 array of m ascending local indices
+// per node (one vector load), each group ordered by the node's first copy.
+// The domain is cut into tiles of `te` consecutive elements; toff[3t + g] is
+// the first node of group g whose first copy lies in tile t or later.  A block
+// processes whole tiles -- all three groups of a tile back to back -- so the
+// sectors of w a tile touches (its own elements and the neighbours at +1,
+// +ex, +ex*ey) are re-used from L2 instead of being streamed from HBM once
+// per group.
+#ifndef NBK_DSSUM_H
+#define NBK_DSSUM_H 2   // nodes per thread per step
+#endif
+// CTAs per SM of K_B (launch bounds; registers).  With the gather phase the
+// chains need few registers: 6 (FP32) / 4 (FP64) CTAs with 512-node tiles,
+// measured same-box: C5 FP64 K_B 0.74 vs 0.86 ms, C4 0.25 vs 0.29 ms, FP32 equal.
 #ifndef NBK_DSSUM_MINB64
 #define NBK_DSSUM_MINB64 4
 #endif
@@ -731,12 +728,11 @@ template <typename T>
 struct DssumArgs {
     T* w;
     const T* p;               // fused: p (shared-node pap term)
-    const uint16_t* h2;       // n2 x 2 compact copies
-    const uint16_t* h4;       // n4 x 4
-    const uint16_t* h8;       // n8 x 8
-    const int32_t* toff;      // (ntiles + 1) x 3 tile offsets into h2, h4, h8
+    const int32_t* g2;        // n2 x 2
+    const int32_t* g4;        // n4 x 4
+    const int32_t* g8;        // n8 x 8
+    const int32_t* toff;      // (ntiles + 1) x 3 tile offsets into g2, g4, g8
     int ntiles;
-    int te;                   // elements per tile (<= 8)
     dd* parts;                // fused: partials [0, nA) from K_A, [nA, nA+gridDim) here
     int nA;
     CgState* st;
@@ -747,7 +743,8 @@ struct DssumArgs {
     int single;               // paper-literal single mode (NEXT-2)
     PmArgs pm;                // precision emulation (NEXT-4)
     int it;                   // CG iteration (emulation keys)
-    int tile_smem;            // bytes per index staging buffer (two buffers)
+    int stage;                // index rows of each tile staged in smem by bulk copies
+    int tile_smem;            // bytes per staging buffer (two buffers)
     MeshView mesh;
 };
 
@@ -795,6 +792,34 @@ __device__ __forceinline__ bool masked_local(const MeshView& m, int32_t Ls)
     return is_masked(m, ec, i, j, k);
 }
 
+// Load the (ascending) local indices of node q of a tile (q counts the tile's
+// g2 nodes, then its g4, then its g8 nodes); returns the multiplicity.
+__device__ __forceinline__ int tile_seg_load(const int32_t* g2, const int32_t* g4, const int32_t* g8,
+                                             int s2, int n2, int s4, int n4, int s8, int q,
+                                             int32_t (&ix)[8])
+{
+    if (q < n2) {
+        const int2 v = reinterpret_cast<const int2*>(g2)[s2 + q];
+        ix[0] = v.x; ix[1] = v.y;
+        return 2;
+    }
+    q -= n2;
+    if (q < n4) {
+        const int4 v = reinterpret_cast<const int4*>(g4)[s4 + q];
+        ix[0] = v.x; ix[1] = v.y; ix[2] = v.z; ix[3] = v.w;
+        return 4;
+    }
+    q -= n4;
+    const int4* g = reinterpret_cast<const int4*>(g8) + 2 * (int64_t)(s8 + q);
+    const int4 v0 = g[0], v1 = g[1];
+    ix[0] = v0.x; ix[1] = v0.y; ix[2] = v0.z; ix[3] = v0.w;
+    ix[4] = v1.x; ix[5] = v1.y; ix[6] = v1.z; ix[7] = v1.w;
+    return 8;
+}
+
+// The tiles of this block (grid-stride), node by node (all multiplicities of
+// a tile in one loop, two nodes per thread per step, every load of both
+// issued before use; p by the read-only path).
 // Tile t's segment offsets.
 __device__ __forceinline__ void tile_range(const int32_t* toff, int t, int& s2, int& n2, int& s4, int& n4,
                                            int& s8, int& n8)
@@ -803,40 +828,120 @@ __device__ __forceinline__ void tile_range(const int32_t* toff, int t, int& s2, 
     n2 = __ldg(&toff[3 * t + 3]) - s2; n4 = __ldg(&toff[3 * t + 4]) - s4; n8 = __ldg(&toff[3 * t + 5]) - s8;
 }
 
-// Thread 0: bulk-copy tile t's compact rows into buf: the m = 2, 4, 8 groups,
-// each as its 16-byte aligned byte range (layout: dssum_grp_bytes / _lead).
-__device__ __forceinline__ void tile_stage(const uint16_t* h2, const uint16_t* h4, const uint16_t* h8,
+// Thread 0: bulk-copy tile t's index rows into buf (layout: dssum_tile_bytes).
+__device__ __forceinline__ void tile_stage(const int32_t* g2, const int32_t* g4, const int32_t* g8,
                                            const int32_t* toff, int t, unsigned char* buf, uint64_t* bar)
 {
     int s2, n2, s4, n4, s8, n8;
     tile_range(toff, t, s2, n2, s4, n4, s8, n8);
-    const uint32_t b2 = (uint32_t)dssum_grp_bytes(4, s2, n2), b4 = (uint32_t)dssum_grp_bytes(8, s4, n4);
-    const uint32_t b8 = (uint32_t)dssum_grp_bytes(16, s8, n8);
+    const uint32_t b2 = (uint32_t)dssum_g2_bytes(s2, n2), b4 = 16u * n4, b8 = 32u * n8;
     mbar_arrive_expect_tx(bar, b2 + b4 + b8);
-    const unsigned char* g2 = reinterpret_cast<const unsigned char*>(h2);
-    const unsigned char* g4 = reinterpret_cast<const unsigned char*>(h4);
-    const unsigned char* g8 = reinterpret_cast<const unsigned char*>(h8);
-    if (b2) tma_load_1d(buf, g2 + ((4 * (int64_t)s2) & ~(int64_t)15), b2, bar);
-    if (b4) tma_load_1d(buf + b2, g4 + ((8 * (int64_t)s4) & ~(int64_t)15), b4, bar);
-    if (b8) tma_load_1d(buf + b2 + b4, g8 + 16 * (int64_t)s8, b8, bar);
+    if (b2) tma_load_1d(buf, reinterpret_cast<const unsigned char*>(g2) + ((8 * (int64_t)s2) & ~(int64_t)15), b2, bar);
+    if (b4) tma_load_1d(buf + b2, g4 + 4 * (int64_t)s4, b4, bar);
+    if (b8) tma_load_1d(buf + b2 + b4, g8 + 8 * (int64_t)s8, b8, bar);
 }
 
-// Element of a compact copy code (3 high bits): a + b ex + c ex ey
-__device__ __forceinline__ int dssum_edelta(const MeshView& m, int code)
+// The tiles of this block (grid-stride), node by node (all multiplicities of
+// a tile in one loop, NBK_DSSUM_H nodes per thread per step, every load of
+// them issued before use; p by the read-only path).  stage: the index rows of
+// the block's next tile are bulk-copied into the other shared-memory buffer
+// while this tile is processed, so the per-step dependent chain is one global
+// latency (w) instead of two (indices, then w).
+template <typename T, bool FUSED, int PM = PM_NONE>
+__device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
+                                            int tile_smem, uint64_t* bars)
 {
-    return (code & 1) + ((code >> 1) & 1) * m.ex + (code >> 2) * m.ex * m.ey;
-}
-// SL local index of copy c of a node (row = its compact copies, eb = tile's first element)
-__device__ __forceinline__ int32_t dssum_copy(const MeshView& m, const uint16_t* row, int c, int eb)
-{
-    const int N3 = m.N * m.N * m.N;
-    const int h0 = row[0];
-    const int e0 = eb + (h0 >> 12);
-    if (c == 0) return e0 * N3 + (h0 & 0xFFF);
-    const int hc = row[c];
-    return (e0 + dssum_edelta(m, hc >> 12)) * N3 + (hc & 0xFFF);
+    if (a.stage) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && (int)blockIdx.x < a.ntiles)
+            tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - blockIdx.x : blockIdx.x, sbuf, &bars[0]);
+    }
+    int k = 0;
+    for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x, ++k) {
+        const int t = a.rev ? a.ntiles - 1 - i : i;
+        int s2, n2, s4, n4, s8, n8;
+        tile_range(a.toff, t, s2, n2, s4, n4, s8, n8);
+        const int32_t *G2 = a.g2, *G4 = a.g4, *G8 = a.g8;
+        int S2 = s2, S4 = s4, S8 = s8;
+        if (a.stage) {
+            const int b = k & 1;
+            const int inx = i + (int)gridDim.x;
+            if (threadIdx.x == 0 && inx < a.ntiles) {  // the other buffer was released by the last barrier
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - inx : inx,
+                           sbuf + (b ^ 1) * tile_smem, &bars[b ^ 1]);
+            }
+            mbar_wait(&bars[b], (k >> 1) & 1);
+            unsigned char* buf = sbuf + b * tile_smem;
+            const int b2 = (int)dssum_g2_bytes(s2, n2);
+            G2 = reinterpret_cast<const int32_t*>(buf + dssum_g2_lead(s2));
+            G4 = reinterpret_cast<const int32_t*>(buf + b2);
+            G8 = reinterpret_cast<const int32_t*>(buf + b2 + 16 * n4);
+            S2 = S4 = S8 = 0;
+        }
+        const int tot = n2 + n4 + n8;
+        for (int q = threadIdx.x; q < tot; q += NBK_DSSUM_H * blockDim.x) {
+            int32_t ix[NBK_DSSUM_H][8];
+            int m[NBK_DSSUM_H];
+#pragma unroll
+            for (int h = 0; h < NBK_DSSUM_H; ++h) {
+                const int qh = q + h * blockDim.x;
+                m[h] = qh < tot ? tile_seg_load(G2, G4, G8, S2, n2, S4, n4, S8, qh, ix[h]) : 0;
+            }
+            T v[NBK_DSSUM_H][8];
+            T p0[NBK_DSSUM_H];
+#pragma unroll
+            for (int h = 0; h < NBK_DSSUM_H; ++h) {
+                p0[h] = 0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < m[h]) {
+                        NBK_ASSERT(ix[h][c] >= 0 && (int64_t)ix[h][c] < a.mesh.E * a.mesh.N * a.mesh.N * a.mesh.N);
+                        v[h][c] = a.w[ix[h][c]];
+                    }
+                if constexpr (FUSED && !pm_discontinuous(PM))
+                    if (m[h]) p0[h] = __ldg(a.p + ix[h][0]);
+            }
+#pragma unroll
+            for (int h = 0; h < NBK_DSSUM_H; ++h) {
+                if (!m[h]) continue;
+                T sum = v[h][0];                          // C4: ascending local index
+#pragma unroll
+                for (int c = 1; c < 8; ++c)
+                    if (c < m[h])  // chain add c of the node (key: its first copy)
+                        sum = padd<PM>(sum, v[h][c], a.pm,
+                                       pm_key(a.it, PH_B, global_local_index(a.mesh, sl_natural(a.mesh, ix[h][0])), c));
+                if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[h][0])) sum = 0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < m[h]) a.w[ix[h][c]] = sum;
+                if constexpr (FUSED && pm_discontinuous(PM)) {
+                    // RR / MCA: the copies of p differ -- one term RN(RN(w p_c) / m) per copy
+                    // (C6 over every local point, as the oracle's glsc3)
+                    const double cm = m[h] == 2 ? 0.5 : (m[h] == 4 ? 0.25 : 0.125);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        if (c < m[h]) acc.add(dot_term_pm<PM>(sum, __ldg(a.p + ix[h][c]), cm, false, a.pm));
+                } else if constexpr (FUSED) {
+                    add_node_pap<T, PM>(acc, sum, p0[h], m[h], a.single, a.pm);
+                }
+            }
+        }
+        if (a.stage) __syncthreads();
+    }
 }
 
+// Gather-phase K_B (staged tiles): the copies of a tile's nodes (and p at each
+// node's first copy) are fetched into shared memory by cp.async first -- every
+// load of the tile in flight at once, no registers held -- then each node's
+// chain is summed from shared memory and scattered.  Memory-level parallelism
+// of K_B is otherwise bounded by the registers of the per-thread node chains.
+// Dynamic shared memory: 2 index buffers, then the copy values and p values of
+// one tile (dssum_gather_smem).
 __device__ __forceinline__ void cp_async_4(void* dst_smem, const void* src)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
@@ -856,79 +961,72 @@ __device__ __forceinline__ void cp_async_t(T* dst_smem, const T* src)
 }
 
 template <typename T, bool FUSED, int PM = PM_NONE>
-__device__ __forceinline__ void dssum_tiles(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
-                                            int tile_smem, uint64_t* bars)
+__device__ __forceinline__ void dssum_tiles_gather(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
+                                                   int tile_smem, uint64_t* bars)
 {
     constexpr bool PCOPY = FUSED && !pm_discontinuous(PM);
-    T* sval = reinterpret_cast<T*>(sbuf + 2 * tile_smem);      // tile_smem / 2 values
-    T* spv = sval + tile_smem / 2;                             // tile_smem / 4 values
+    T* sval = reinterpret_cast<T*>(sbuf + 2 * tile_smem);      // tile_smem / 4 values
+    T* spv = sval + tile_smem / 4;                             // tile_smem / 8 values
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
     }
     __syncthreads();
     if (threadIdx.x == 0 && (int)blockIdx.x < a.ntiles)
-        tile_stage(a.h2, a.h4, a.h8, a.toff, a.rev ? a.ntiles - 1 - blockIdx.x : blockIdx.x, sbuf, &bars[0]);
+        tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - blockIdx.x : blockIdx.x, sbuf, &bars[0]);
     int k = 0;
     for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x, ++k) {
         const int t = a.rev ? a.ntiles - 1 - i : i;
-        const int eb = t * a.te;
         int s2, n2, s4, n4, s8, n8;
         tile_range(a.toff, t, s2, n2, s4, n4, s8, n8);
         const int b = k & 1;
         const int inx = i + (int)gridDim.x;
         if (threadIdx.x == 0 && inx < a.ntiles) {  // the other buffer was released by the last barrier
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            tile_stage(a.h2, a.h4, a.h8, a.toff, a.rev ? a.ntiles - 1 - inx : inx,
+            tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - inx : inx,
                        sbuf + (b ^ 1) * tile_smem, &bars[b ^ 1]);
         }
         mbar_wait(&bars[b], (k >> 1) & 1);
         unsigned char* buf = sbuf + b * tile_smem;
-        const int b2 = (int)dssum_grp_bytes(4, s2, n2), b4 = (int)dssum_grp_bytes(8, s4, n4);
-        const uint16_t* H2 = reinterpret_cast<const uint16_t*>(buf + dssum_grp_lead(4, s2));
-        const uint16_t* H4 = reinterpret_cast<const uint16_t*>(buf + b2 + dssum_grp_lead(8, s4));
-        const uint16_t* H8 = reinterpret_cast<const uint16_t*>(buf + b2 + b4);
+        const int b2 = (int)dssum_g2_bytes(s2, n2);
+        const int32_t* G2 = reinterpret_cast<const int32_t*>(buf + dssum_g2_lead(s2));
+        const int32_t* G4 = reinterpret_cast<const int32_t*>(buf + b2);
+        const int32_t* G8 = reinterpret_cast<const int32_t*>(buf + b2 + 16 * n4);
         const int c2 = 2 * n2, c4 = c2 + 4 * n4, nc = c4 + 8 * n8, tot = n2 + n4 + n8;
         // phase 1: every copy value (and p) of the tile in flight
         for (int r = threadIdx.x; r < nc; r += blockDim.x) {
-            int32_t ix;
-            if (r < c2) ix = dssum_copy(a.mesh, H2 + (r & ~1), r & 1, eb);
-            else if (r < c4) ix = dssum_copy(a.mesh, H4 + ((r - c2) & ~3), (r - c2) & 3, eb);
-            else ix = dssum_copy(a.mesh, H8 + ((r - c4) & ~7), (r - c4) & 7, eb);
+            const int32_t ix = r < c2 ? G2[r] : (r < c4 ? G4[r - c2] : G8[r - c4]);
             NBK_ASSERT(ix >= 0 && (int64_t)ix < a.mesh.E * a.mesh.N * a.mesh.N * a.mesh.N);
-            NBK_ASSERT(r < tile_smem / 2);
+            NBK_ASSERT(r < tile_smem / 4);
             cp_async_t<T>(sval + r, a.w + ix);
         }
         if constexpr (PCOPY) {
             for (int q = threadIdx.x; q < tot; q += blockDim.x) {
-                const uint16_t* row = q < n2 ? H2 + 2 * q : (q < n2 + n4 ? H4 + 4 * (q - n2) : H8 + 8 * (q - n2 - n4));
-                cp_async_t<T>(spv + q, a.p + dssum_copy(a.mesh, row, 0, eb));
+                const int32_t ix = q < n2 ? G2[2 * q] : (q < n2 + n4 ? G4[4 * (q - n2)] : G8[8 * (q - n2 - n4)]);
+                cp_async_t<T>(spv + q, a.p + ix);
             }
         }
         cp_async_wait_all();
         __syncthreads();
-        // phase 2: chains from shared memory (C4: ascending natural local index), scatter, pap
+        // phase 2: chains from shared memory (C4), scatter, pap
         for (int q = threadIdx.x; q < tot; q += blockDim.x) {
             int m, r0;
-            const uint16_t* row;
-            if (q < n2) { m = 2; r0 = 2 * q; row = H2 + r0; }
-            else if (q < n2 + n4) { m = 4; r0 = 4 * (q - n2); row = H4 + r0; r0 += c2; }
-            else { m = 8; r0 = 8 * (q - n2 - n4); row = H8 + r0; r0 += c4; }
-            const int32_t L0 = dssum_copy(a.mesh, row, 0, eb);
+            const int32_t* row;
+            if (q < n2) { m = 2; r0 = 2 * q; row = G2 + r0; }
+            else if (q < n2 + n4) { m = 4; r0 = 4 * (q - n2); row = G4 + r0; r0 += c2; }
+            else { m = 8; r0 = 8 * (q - n2 - n4); row = G8 + r0; r0 += c4; }
             T sum = sval[r0];
             for (int c = 1; c < m; ++c) {
                 unsigned long long key = 0;
                 if constexpr (PM != PM_NONE)
-                    key = pm_key(a.it, PH_B, global_local_index(a.mesh, sl_natural(a.mesh, L0)), c);
+                    key = pm_key(a.it, PH_B, global_local_index(a.mesh, sl_natural(a.mesh, row[0])), c);
                 sum = padd<PM>(sum, sval[r0 + c], a.pm, key);
             }
-            if (!FUSED && a.mask && masked_local<T>(a.mesh, L0)) sum = 0;
-            a.w[L0] = sum;
-            for (int c = 1; c < m; ++c) a.w[dssum_copy(a.mesh, row, c, eb)] = sum;
+            if (!FUSED && a.mask && masked_local<T>(a.mesh, row[0])) sum = 0;
+            for (int c = 0; c < m; ++c) a.w[row[c]] = sum;
             if constexpr (FUSED && pm_discontinuous(PM)) {
                 const double cm = m == 2 ? 0.5 : (m == 4 ? 0.25 : 0.125);
-                for (int c = 0; c < m; ++c)
-                    acc.add(dot_term_pm<PM>(sum, __ldg(a.p + dssum_copy(a.mesh, row, c, eb)), cm, false, a.pm));
+                for (int c = 0; c < m; ++c) acc.add(dot_term_pm<PM>(sum, __ldg(a.p + row[c]), cm, false, a.pm));
             } else if constexpr (FUSED) {
                 add_node_pap<T, PM>(acc, sum, spv[q], m, a.single, a.pm);
             }
@@ -944,6 +1042,10 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_D
     extern __shared__ __align__(128) unsigned char dsm_tiles[];
     __shared__ uint64_t dsm_bars[2];
     pdl_wait();
+#if defined(NBK_DSSUM_GATHER)
+    if (a.stage) dssum_tiles_gather<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
+    else
+#endif
     dssum_tiles<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
     pdl_launch_dependents();
     if constexpr (FUSED) {
