@@ -123,6 +123,9 @@ template <typename T>
 #ifndef NBK_AX_KP64
 #define NBK_AX_KP64 2   // ... FP64
 #endif
+#ifndef NBK_DREG_BYTES
+#define NBK_DREG_BYTES 48   // D rows / columns of K_A kept in registers up to this row size
+#endif
 #ifndef NBK_AX_G1P64
 #define NBK_AX_G1P64 1  // planes per step of K_A's gradient pass, FP64
 #endif
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(ax_threads<T>(N), ax_min_blocks<T>(N, FUSED))
 
     // D rows / columns of this thread: D[i][l], D[j][l] (gradient) and
     // D[l][i], D[l][j] (transpose), in registers when they fit.
-    constexpr bool DREG = N * sizeof(T) <= 48;
+    constexpr bool DREG = N * (int)sizeof(T) <= NBK_DREG_BYTES;
 
     // ---- gradient (C1), metric (C2), t-part of the transpose (C3: b chain)
     T b[N];
