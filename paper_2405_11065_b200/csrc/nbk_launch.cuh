@@ -16,6 +16,7 @@
 
 #include "nbk_internal.h"
 #include "nbk_kernels.cuh"
+#include "nbk_axl.cuh"
 
 namespace nbk {
 
@@ -68,6 +69,21 @@ template <typename T, int N, int FUSED, int PM = PM_NONE>
 inline cudaError_t launch_ax_n(const AxArgs<T>& a, cudaStream_t s, bool attr_only = false,
                                bool pdl = false)
 {
+    if constexpr (axl_on<T>(N, FUSED, PM)) {  // line-owner K_A (nbk_axl.cuh)
+        constexpr int EPB = axl_epb<T>(N);
+        const size_t smem = (size_t)axl_smem_bytes<T>(N);
+        if (attr_only)
+            return cudaFuncSetAttribute(k_axl<T, N, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem);
+        const unsigned grid = (unsigned)((a.en0 + EPB - 1) / EPB + (a.en1 + EPB - 1) / EPB);
+        if (grid == 0) return cudaSuccess;
+        DMat<T, N> dc{};
+        for (int q = 0; q < N * N; ++q) {
+            dc.d[q] = a.Dh[q];
+            dc.dt[(q % N) * N + q / N] = a.Dh[q];
+        }
+        return launch_k(k_axl<T, N, FUSED>, grid, axl_threads<T>(N), smem, s, pdl, a, dc);
+    }
     constexpr int EPB = ax_epb<T>(N);
     const size_t smem = (size_t)ax_smem_bytes<T>(N, FUSED);
     if (attr_only)
@@ -440,11 +456,11 @@ inline KaSplit ka_split(const nbk_ctx* c, bool multi)
     return k;
 }
 // K_A blocks over n elements (EPB elements per block)
-template <typename T>
+template <typename T, int PM = PM_NONE>
 inline int ka_blocks(const nbk_ctx* c, int64_t n)
 {
     int epb = 1;
-#define EPBC(nn) case nn: epb = ax_epb<T>(nn); break;
+#define EPBC(nn) case nn: epb = axl_on<T>(nn, 1, PM) ? axl_epb<T>(nn) : ax_epb<T>(nn); break;
     switch (c->N) {
     EPBC(2) EPBC(3) EPBC(4) EPBC(5) EPBC(6) EPBC(7) EPBC(8) EPBC(9) EPBC(10) EPBC(11) EPBC(12)
     EPBC(13) EPBC(14) EPBC(15) EPBC(16)
@@ -466,7 +482,7 @@ inline int ka_parts(const nbk_ctx* c, bool multi)
     const KaSplit k = ka_split(c, multi);
     int n = 0;
     for (int l = 0; l < 2; ++l)
-        for (int r = 0; r < 2; ++r) n += ka_blocks<T>(c, k.en[l][r]);
+        for (int r = 0; r < 2; ++r) n += ka_blocks<T, PM>(c, k.en[l][r]);
     return n;
 }
 
@@ -710,7 +726,7 @@ inline cudaError_t enqueue_solve(const Team& t, int niter, nbk_graph* g, bool fp
                 const KaSplit ks = ka_split(c, t.multi);
                 aa.eb0 = ks.eb[l][0]; aa.en0 = ks.en[l][0];
                 aa.eb1 = ks.eb[l][1]; aa.en1 = ks.en[l][1];
-                aa.part_off = l == 0 ? 0 : ka_blocks<T>(c, ks.en[0][0]) + ka_blocks<T>(c, ks.en[0][1]);
+                aa.part_off = l == 0 ? 0 : ka_blocks<T, PM>(c, ks.en[0][0]) + ka_blocks<T, PM>(c, ks.en[0][1]);
                 const bool pa = pdl && (g_pdl_mask & 1) && l == 0;
                 e = jac ? launch_ax<T, 2>(aa, s, false, pa) : launch_ax<T, 1, PM>(aa, s, false, pa);
                 if (e != cudaSuccess) return e;

@@ -58,16 +58,19 @@ def test_kernels_are_sm100a_and_use_no_contraction(lib):
         names = [f for f in funcs if f.startswith(prefix)]
         assert len(names) == 1, (prefix, names)
         return "\n".join(funcs[names[0]])
-    fused64 = body("_ZN3nbk4k_axIdLi8ELi1ELi0EE")
-    fused32 = body("_ZN3nbk4k_axIfLi8ELi1ELi0EE")
+    # the fused CG step of K_A: line-owner kernel k_axl (nbk_axl.cuh)
+    fused64 = body("_ZN3nbk5k_axlIdLi10ELi1EEE")
+    fused32 = body("_ZN3nbk5k_axlIfLi8ELi1EEE")
     assert "DFMA" in fused64 and "FFMA" in fused32
-    # TMA 1-D bulk copies (cp.async.bulk -> UBLKCP) stage G and p in shared memory
-    assert "UBLKCP" in fused64 and "UBLKCP" in fused32
-    # N = 10 (TIO): r, x bulk-loaded and p, x, w bulk-stored -- no per-thread global
-    # loads / stores of the CG vectors, only the parameter / scalar loads
-    tio32 = body("_ZN3nbk4k_axIfLi10ELi1ELi0EE")
-    assert tio32.count("UBLKCP.G.S") >= 3 and tio32.count("UBLKCP.S.G") >= 3
-    assert tio32.count("STG") <= 2   # only the pap partial (dd) of the block
+    # TMA 1-D bulk copies (cp.async.bulk -> UBLKCP) stage G and p in shared memory,
+    # w leaves by a bulk store; r / x / p' / x' move as 16-byte vectors in slot order
+    for n in (8, 10, 12):
+        k32 = body(f"_ZN3nbk5k_axlIfLi{n}ELi1EEE")
+        assert k32.count("UBLKCP.S.G") >= 2 and k32.count("UBLKCP.G.S") >= 1, n   # loads p, G; store w
+        assert "LDG.E.128" in k32 and "STG.E.128" in k32, n
+    # the plain operator (nbk_ax_apply) keeps the pencil kernel
+    plain32 = body("_ZN3nbk4k_axIfLi10ELi0ELi0EE")
+    assert "UBLKCP" in plain32 and "FFMA" in plain32
     # K_B: compact plan rows staged by TMA, copies gathered by cp.async (LDGSTS)
     kb32 = body("_ZN3nbk7k_dssumIfLb1ELi0EE")
     assert "UBLKCP" in kb32 and "LDGSTS" in kb32
