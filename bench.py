@@ -488,11 +488,11 @@ def run_gpu(args):
     achieved = bytes_ka / (ka_avg_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(args.config, prec),
-                "kernel": "k_ax<fused> (p,x update + ax_e + mask + interior pap)",
+                "kernel": "k_axl<fused> (line-owner K_A: p,x update + ax_e + mask + interior pap)",
                 "algorithmic_bytes_per_launch": bytes_ka, "avg_launch_ms": ka_avg_ms,
                 "share_of_step": kt["share_K_A"],
                 "ncu_share_of_iteration": None,
-                "timing": f"CUDA events on the context stream around each k_ax launch, in a "
+                "timing": f"CUDA events on the context stream around each K_A launch, in a "
                           f"replay of {args.prof_steps} solves (events disable the PDL overlap)",
                 "traffic_source": "profiles/ncu_summary.json (ncu --set full, same config)",
                 "peak_source": peak_src}

@@ -20,7 +20,7 @@ SOURCES = [("nbk_capi.cu", "nbk_capi", []), ("nbk_setup.cu", "nbk_setup", []),
            ("nbk_emu.cu", "nbk_emu1", ["-DNBK_EMU_MODE=1"]),
            ("nbk_emu.cu", "nbk_emu2", ["-DNBK_EMU_MODE=2"]),
            ("nbk_emu.cu", "nbk_emu3", ["-DNBK_EMU_MODE=3"])]
-HEADERS = ["nbk_common.cuh", "nbk_kernels.cuh", "nbk_axl.cuh", "nbk_launch.cuh", "nbk_internal.h",
+HEADERS = ["nbk_common.cuh", "nbk_kernels.cuh", "nbk_axl.cuh", "nbk_kbw.cuh", "nbk_launch.cuh", "nbk_internal.h",
            "../../include/nbk.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

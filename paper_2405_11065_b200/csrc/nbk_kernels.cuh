@@ -721,6 +721,9 @@ __device__ __forceinline__ void fin_rtr(CgState* st, dd rtr_dd, dd rtz_dd, doubl
 // CTAs per SM of K_B (launch bounds; registers).  With the gather phase the
 // chains need few registers: 6 (FP32) / 4 (FP64) CTAs with 512-node tiles,
 // measured same-box: C5 FP64 K_B 0.74 vs 0.86 ms, C4 0.25 vs 0.29 ms, FP32 equal.
+#ifndef NBK_DSSUM_THREADS
+#define NBK_DSSUM_THREADS 256   // threads per K_B block
+#endif
 #ifndef NBK_DSSUM_MINB64
 #define NBK_DSSUM_MINB64 4
 #endif
@@ -1038,8 +1041,11 @@ __device__ __forceinline__ void dssum_tiles_gather(const DssumArgs<T>& a, acc_t&
     }
 }
 
+template <typename T, int PM>
+__device__ __forceinline__ void dssum_fused_epilogue(const DssumArgs<T>& a, acc_t& acc);
+
 template <typename T, bool FUSED, int PM = PM_NONE>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_DSSUM_MINB64) k_dssum(DssumArgs<T> a)
+__global__ void __launch_bounds__(NBK_DSSUM_THREADS, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_DSSUM_MINB64) k_dssum(DssumArgs<T> a)
 {
     acc_t acc;
     extern __shared__ __align__(128) unsigned char dsm_tiles[];
@@ -1051,7 +1057,15 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? NBK_DSSUM_MINB32 : NBK_D
 #endif
     dssum_tiles<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
     pdl_launch_dependents();
-    if constexpr (FUSED) {
+    if constexpr (FUSED) dssum_fused_epilogue<T, PM>(a, acc);
+}
+
+// Fused K_B epilogue (all threads of the block): fold K_A's partials, publish
+// the block's pap partial; one rank: the last block forms alpha.
+template <typename T, int PM>
+__device__ __forceinline__ void dssum_fused_epilogue(const DssumArgs<T>& a, acc_t& acc)
+{
+    {
         // K_A's nA pap partials are folded in here, a fixed slice per block, so
         // that the serial last-block reduction sees gridDim partials, not nA + gridDim
         dd ka{0.0, 0.0};

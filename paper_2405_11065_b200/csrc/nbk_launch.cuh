@@ -17,6 +17,7 @@
 #include "nbk_internal.h"
 #include "nbk_kernels.cuh"
 #include "nbk_axl.cuh"
+#include "nbk_kbw.cuh"
 
 namespace nbk {
 
@@ -214,11 +215,17 @@ inline size_t dssum_stage_smem(int64_t tile_smem)
 template <typename T, bool FUSED, int PM = PM_NONE>
 inline int dssum_grid_t(int ntiles, int64_t tile_smem, int* stage_out = nullptr)
 {
+    if constexpr (kbw_on<T, FUSED, PM>()) {  // warp-stream K_B: one resident wave, no staging
+        if (stage_out) *stage_out = 0;
+        const int cap = resident_grid((const void*)k_dssum_w<T, FUSED, PM>, 256, 0);
+        const int want = (ntiles + 7) / 8;   // a warp per tile at least
+        return want < 1 ? 1 : (want > cap ? cap : want);
+    }
     const int mode = dssum_stage_mode();
     int stage = 0;
-    int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, 0);
+    int cap = resident_grid((const void*)k_dssum<T, FUSED, PM>, NBK_DSSUM_THREADS, 0);
     if (mode != 0) {
-        const int cap_s = resident_grid((const void*)k_dssum<T, FUSED, PM>, 256, dssum_stage_smem<T>(tile_smem));
+        const int cap_s = resident_grid((const void*)k_dssum<T, FUSED, PM>, NBK_DSSUM_THREADS, dssum_stage_smem<T>(tile_smem));
 #ifdef NBK_DSSUM_GATHER
         const bool auto_stage = true;   // the gather phase works on staged tiles
 #else
@@ -243,7 +250,8 @@ inline cudaError_t launch_dssum(const DssumArgs<T>& a, cudaStream_t s, bool pdl 
 {
     DssumArgs<T> d = a;
     const int grid = dssum_grid_t<T, FUSED, PM>(a.ntiles, a.tile_smem, &d.stage);
-    return launch_k(k_dssum<T, FUSED, PM>, grid, 256, d.stage ? dssum_stage_smem<T>(a.tile_smem) : 0, s, pdl, d);
+    if constexpr (kbw_on<T, FUSED, PM>()) return launch_k(k_dssum_w<T, FUSED, PM>, grid, 256, 0, s, pdl, d);
+    return launch_k(k_dssum<T, FUSED, PM>, grid, NBK_DSSUM_THREADS, d.stage ? dssum_stage_smem<T>(a.tile_smem) : 0, s, pdl, d);
 }
 
 // ------------------------------------------------------------ NCCL (dlopen)

@@ -71,6 +71,8 @@ def kernel_key(name):
     K_C k_vec<T, V, 1, 0> (RUPD); None for the others."""
     if "k_ax<" in name and name.replace(" ", "").split(">(")[0].endswith(",1,0"):
         return "k_ax_fused"
+    if "k_axl<" in name and name.replace(" ", "").replace("(int)", "").split(">(")[0].endswith(",1"):
+        return "k_ax_fused"   # the line-owner K_A (nbk_axl.cuh)
     if "k_dssum<" in name and ", 1, 0>" in name:
         return "k_dssum_fused"
     if "k_vec<" in name and name.replace(" ", "").split(">(")[0].endswith(",1,0"):
