@@ -63,9 +63,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
         procs.append((stem, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
     for stem, pr in procs:
-        out, err = pr.communicate()
+        sout, err = pr.communicate()
         if pr.returncode != 0:
-            sys.stderr.write(out + err)
+            sys.stderr.write(sout + err)
             raise RuntimeError(f"nvcc failed on {stem}")
         if verbose:
             sys.stderr.write(err)

@@ -21,9 +21,10 @@
 //                    s-line (i, k): us(i, ., k) = D u(i, ., k)   (in place in T)
 //   P3  pencil: ut = D u(i, j, .) from registers, metric (C2), wr -> U, ws -> T
 //       in place; the t-part of the transpose b (C3) accumulated in registers.
-//   P4  r-line owners: a(., j, k) = sum_l D[l][.] wr(l, j, k)  -> P block (natural)
+//   P4  r-line owners: a(., j, k) = sum_l D[l][.] wr(l, j, k)  -> A (padded layout
+//       in the dead G region, fewer bank conflicts for the column accesses)
 //   P5  s-line owners: a(i, ., k) += sum_l D[l][.] ws(i, l, k)  (the same chain,
-//       continued) -> U (natural)
+//       continued), in place in A
 //   P6  pencil: w = a + b, mask (C5) -> P block in SL order (one TMA bulk store),
 //       element-interior pap terms (C6).
 // Shared memory per element: G (6 N^3, TMA) + P, U, T (N^3 each) = 9 N^3 values.
@@ -35,6 +36,9 @@ namespace nbk {
 #ifndef NBK_AXL_EPB10_F32
 #define NBK_AXL_EPB10_F32 1
 #endif
+#ifndef NBK_AXL_EPB8_F64
+#define NBK_AXL_EPB8_F64 2
+#endif
 // N for which the fused CG step uses k_axl (bit N), FP32 / FP64.  Measured
 // same-box against the pencil k_ax: C5 (N = 10) FP32 K_A
 // 2.42 vs 2.76 ms, FP64 4.78 vs 5.28; C3 (N = 12) FP32 0.60 vs 0.645; C4
@@ -43,7 +47,7 @@ namespace nbk {
 #define NBK_AXL_MASK32 ((1 << 4) | (1 << 6) | (1 << 8) | (1 << 10) | (1 << 12))
 #endif
 #ifndef NBK_AXL_MASK64
-#define NBK_AXL_MASK64 ((1 << 4) | (1 << 6) | (1 << 10))
+#define NBK_AXL_MASK64 ((1 << 4) | (1 << 6) | (1 << 10) | (1 << 12))
 #endif
 #ifdef NBK_AXL_MASK   // one mask for both (A/B builds)
 #undef NBK_AXL_MASK32
@@ -56,25 +60,57 @@ template <typename T>
 __host__ __device__ constexpr int axl_epb(int N)
 {
     if (N == 10) return sizeof(T) == 4 ? NBK_AXL_EPB10_F32 : 1;
+    if (N == 8 && sizeof(T) == 8) return NBK_AXL_EPB8_F64;
     if (N >= 10) return 1;
     // at least 2 warps of work per CTA
     int e = 128 / (N * N);
     return e < 1 ? 1 : e;
+}
+// Padded layout of the transpose chain a(i, j, k) (P4 -> P5 -> P6) in the dead
+// G region: a at i + R j + P k.  Chosen by a bank-conflict search over the
+// P4 row stores, the P5 column loads / stores and the P6 pencil loads (lane
+// maps as used below): N = 10 wavefront estimate 380 -> 260 per warp group.
+#ifndef NBK_AXL_PAD
+#define NBK_AXL_PAD 1   // 0: natural layout (A/B)
+#endif
+__host__ __device__ constexpr int axl_pr(int N)
+{
+    return !NBK_AXL_PAD ? N : (N == 8 ? 9 : (N == 10 || N == 12 ? 17 : N));
+}
+__host__ __device__ constexpr int axl_pp(int N)
+{
+    return !NBK_AXL_PAD ? N * N : (N == 8 ? 72 : (N == 10 ? 170 : (N == 12 ? 204 : N * N)));
 }
 template <typename T>
 __host__ __device__ constexpr int axl_threads(int N)
 {
     return (N * N * axl_epb<T>(N) + 31) / 32 * 32;
 }
+// NBK_AXL_SMEM8: 8 N^3 values per element -- p arrives by vector loads and its
+// SL block sits in the T buffer until the copies are made, w leaves from the
+// dead G region (one bulk store per element); 0: 9 N^3 (p by TMA into its own block).
+// Default (-1): where it was measured faster (same-box, bench events): FP64 N = 12 (124 ->
+// 111 KB per element, 1 -> 2 CTAs/SM: C3 FP64 K_A 1.16 vs 1.32 ms with the pencil kernel)
+// and FP32 N = 10 (7 instead of 6 CTAs/SM at 72 registers: C5 K_A 2.16 vs 2.21 ms).  Not
+// elsewhere: FP64 N = 10 spills (4.77 vs 4.42 ms), FP32 N = 8 / 12 lose (0.53 vs 0.52 ms).
+#ifndef NBK_AXL_SMEM8
+#define NBK_AXL_SMEM8 -1
+#endif
+template <typename T>
+__host__ __device__ constexpr bool axl_s8(int N)
+{
+    return NBK_AXL_SMEM8 >= 0 ? NBK_AXL_SMEM8 != 0 : (sizeof(T) == 8 ? N == 12 : N == 10);
+}
 template <typename T>
 __host__ __device__ constexpr int axl_smem_bytes(int N)
 {
-    return 9 * axl_epb<T>(N) * N * N * N * (int)sizeof(T);
+    return (axl_s8<T>(N) ? 8 : 9) * axl_epb<T>(N) * N * N * N * (int)sizeof(T);
 }
 template <typename T>
 __host__ __device__ constexpr int axl_min_blocks(int N)
 {
-    int by_smem = (232448 - 1024) / (axl_smem_bytes<T>(N) + 1024 + 600);
+    // 228 KB of shared memory per SM; per CTA 1 KB reserved + the static 128 B (bars, red)
+    int by_smem = 233472 / (axl_smem_bytes<T>(N) + 1024 + 256);
     int by_thr = 2048 / axl_threads<T>(N);
     int m = by_smem < by_thr ? by_smem : by_thr;
     return m < 1 ? 1 : m;
@@ -197,12 +233,13 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
     constexpr int VN = Vec16<T>::n;
     constexpr int NVT = (EPB * N3 / VN + NT - 1) / NT;   // vectors per thread in P1
     static_assert((N3 * (int)sizeof(T)) % 16 == 0, "k_axl needs 16-byte element blocks");
+    constexpr bool S8 = axl_s8<T>(N);
     __shared__ __align__(8) uint64_t bar[2];   // 0: p block, 1: G block
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    T* sG = reinterpret_cast<T*>(smem_raw);   // EPB * 6 N^3
-    T* sP = sG + EPB * 6 * N3;                // EPB * N^3: p (SL) -> a partial (natural) -> w (SL)
-    T* sU = sP + EPB * N3;                    // EPB * N^3: u -> ur -> wr -> a (natural)
-    T* sT = sU + EPB * N3;                    // EPB * N^3: u^T -> us^T -> ws^T (j fastest)
+    T* sG = reinterpret_cast<T*>(smem_raw);   // EPB * 6 N^3: G -> a (padded) + w (SL, S8)
+    T* sP = sG + EPB * 6 * N3;                // !S8: EPB * N^3: p (SL) -> w (SL)
+    T* sU = S8 ? sP : sP + EPB * N3;          // EPB * N^3: u -> ur -> wr (natural)
+    T* sT = sU + EPB * N3;                    // EPB * N^3: (S8: p SL ->) u^T -> us^T -> ws^T
 
     const int tid = threadIdx.x;
     const int el = tid / N2, ij = tid - el * N2;
@@ -224,7 +261,7 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
-        if (a.p_ready) {
+        if (!S8 && a.p_ready) {
             mbar_arrive_expect_tx(&bar[0], pbytes);
             tma_load_1d(sP, a.p + e0 * N3, pbytes, &bar[0]);
         }
@@ -235,13 +272,15 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
     const V* xg = reinterpret_cast<const V*>(a.x + e0 * N3);
     const V* rg = reinterpret_cast<const V*>(a.r + e0 * N3);
     const V* dg = reinterpret_cast<const V*>(FUSED == 2 ? a.dinv + e0 * N3 : a.r);
-    V xv[NVT], rv[NVT], dv[FUSED == 2 ? NVT : 1];
+    const V* pgi = reinterpret_cast<const V*>(a.p + e0 * N3);
+    V xv[NVT], rv[NVT], dv[FUSED == 2 ? NVT : 1], pv[S8 ? NVT : 1];
     auto load_xd = [&]() {
 #pragma unroll
         for (int q = 0; q < NVT; ++q) {
             const int v = tid + q * NT;
             if (v < nv) {
                 xv[q] = xg[v];
+                if constexpr (S8) pv[q] = pgi[v];
                 if constexpr (FUSED == 2) dv[q] = __ldg(dg + v);
             }
         }
@@ -249,7 +288,7 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
     if (a.p_ready) load_xd();
     pdl_wait();
     if (!a.p_ready) {
-        if (tid == 0) {
+        if (!S8 && tid == 0) {
             mbar_arrive_expect_tx(&bar[0], pbytes);
             tma_load_1d(sP, a.p + e0 * N3, pbytes, &bar[0]);
         }
@@ -269,18 +308,20 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
         alphaT = (T)a.st->alpha32;
     }
     __syncthreads();   // barrier init visible
-    mbar_wait(&bar[0], 0);
+    if constexpr (!S8) mbar_wait(&bar[0], 0);
 
     // ---- P1: p = fma(beta, p, z), x = fma(alpha_prev, p_prev, x)  (C8), slot order
     {
-        V* sPv = reinterpret_cast<V*>(sP);
+        V* sPv = reinterpret_cast<V*>(S8 ? sT : sP);   // p' in SL order
         V* pg = reinterpret_cast<V*>(a.p + e0 * N3);
         V* xo = reinterpret_cast<V*>(a.x + e0 * N3);
 #pragma unroll
         for (int q = 0; q < NVT; ++q) {
             const int v = tid + q * NT;
             if (v < nv) {
-                const V po = sPv[v];
+                V po;
+                if constexpr (S8) po = pv[q];
+                else po = sPv[v];
                 V pn, xn;
 #pragma unroll
                 for (int c = 0; c < VN; ++c) {
@@ -298,15 +339,31 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
     }
     __syncthreads();
 
-    T* Pe = sP + el * N3;
     T* Ue = sU + el * N3;
     T* Te = sT + el * N3;
+    // w in SL order: !S8 the p block, S8 the dead G region behind the padded a
+    T* We = S8 ? sG + el * 6 * N3 + 3 * N3 : sP + el * N3;
     const SlCol cs = sl_col(N, i, j);
     NBK_ASSERT(!valid || (cs.at(N, 0) >= 0 && cs.at(N, N - 1) < N3 && cs.at(N, N / 2) < N3));
 
     // ---- P1b: the pencil's column of p' (registers) + natural and transposed copies
     T ureg[N];
-    if (valid) {
+    if constexpr (S8) {
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const T v = Te[cs.at(N, k)];
+                ureg[k] = v;
+                Ue[k * N2 + j * N + i] = v;
+            }
+        }
+        __syncthreads();   // the SL block in T is consumed
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) Te[k * N2 + i * N + j] = ureg[k];
+        }
+    } else if (valid) {
+        const T* Pe = sP + el * N3;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
             const T v = Pe[cs.at(N, k)];
@@ -372,24 +429,29 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
     }
     __syncthreads();
 
-    // ---- P4: r-part of the transpose chain (C3) by r-line owners -> P (natural)
+    // ---- P4: r-part of the transpose chain (C3) by r-line owners -> A (padded,
+    // in the dead G region)
+    constexpr int PR = axl_pr(N), PP = axl_pp(N);
+    static_assert(PR * (N - 1) + N <= PP && PP * N <= 3 * N3, "k_axl: padded a does not fit");
+    T* Ae = sG + el * 6 * N3;
     if (valid) {
         T v[N], o[N];
         lds_row<T, N>(v, Ue + ko * N2 + lo * N);   // wr(., lo, ko)
         line_chains<T, N, 1>(o, v, dc);            // a(o, lo, ko) = sum_l D[l][o] wr(l, lo, ko)
-        sts_row<T, N>(Pe + ko * N2 + lo * N, o);
+#pragma unroll
+        for (int q = 0; q < N; ++q) Ae[q + PR * lo + PP * ko] = o[q];
     }
     __syncthreads();
 
-    // ---- P5: s-part of the same chain by s-line owners -> U (natural)
+    // ---- P5: s-part of the same chain by s-line owners, in place in A
     if (valid) {
         T v[N], s[N];
 #pragma unroll
-        for (int o = 0; o < N; ++o) s[o] = Pe[ko * N2 + o * N + lo];   // a(lo, o, ko)
+        for (int o = 0; o < N; ++o) s[o] = Ae[lo + PR * o + PP * ko];   // a(lo, o, ko)
         lds_row<T, N>(v, Te + ko * N2 + lo * N);                        // ws(lo, ., ko)
         line_chains_cont<T, N>(s, v, dc);
 #pragma unroll
-        for (int o = 0; o < N; ++o) Ue[ko * N2 + o * N + lo] = s[o];
+        for (int o = 0; o < N; ++o) Ae[lo + PR * o + PP * ko] = s[o];
     }
     __syncthreads();
 
@@ -405,10 +467,10 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
         const bool mz0 = ec.azg == 0, mz1 = ec.azg == a.mesh.ezg - 1;
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            T wv = add_t<T>(Ue[k * N2 + j * N + i], b[k]);
+            T wv = add_t<T>(Ae[i + PR * j + PP * k], b[k]);
             const bool masked = mxy || (k == 0 && mz0) || (k == n1 && mz1);
             if (a.mask && masked) wv = 0;   // C5: assign +0
-            Pe[cs.at(N, k)] = wv;
+            We[cs.at(N, k)] = wv;
             // element-interior points only; the others add +0, a no-op of the
             // accumulator (its sum starts at +0 and is never -0), so no branch
             const bool sz = (k == 0 && !mz0) || (k == n1 && !mz1);
@@ -425,7 +487,12 @@ __global__ void __launch_bounds__(axl_threads<T>(N), axl_min_blocks<T>(N))
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-        tma_store_1d(a.w + e0 * N3, sP, pbytes);
+        if constexpr (S8) {
+            for (int q = 0; q < nel; ++q)
+                tma_store_1d(a.w + (e0 + q) * N3, sG + q * 6 * N3 + 3 * N3, (uint32_t)(N3 * sizeof(T)));
+        } else {
+            tma_store_1d(a.w + e0 * N3, sP, pbytes);
+        }
         bulk_commit();
     }
     pdl_launch_dependents();

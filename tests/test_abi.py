@@ -66,7 +66,8 @@ def test_kernels_are_sm100a_and_use_no_contraction(lib):
     # w leaves by a bulk store; r / x / p' / x' move as 16-byte vectors in slot order
     for n in (8, 10, 12):
         k32 = body(f"_ZN3nbk5k_axlIfLi{n}ELi1EEE")
-        assert k32.count("UBLKCP.S.G") >= 2 and k32.count("UBLKCP.G.S") >= 1, n   # loads p, G; store w
+        # bulk loads of G (and p where its block is staged: 9 N^3 layout), bulk store of w
+        assert k32.count("UBLKCP.S.G") >= (1 if n == 10 else 2) and k32.count("UBLKCP.G.S") >= 1, n
         assert "LDG.E.128" in k32 and "STG.E.128" in k32, n
     # the plain operator (nbk_ax_apply) keeps the pencil kernel
     plain32 = body("_ZN3nbk4k_axIfLi10ELi0ELi0EE")
