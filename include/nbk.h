@@ -219,6 +219,25 @@ nbk_status nbk_cg_solve_host(nbk_ctx* ctx, const double* f_host, int32_t niter,
                              nbk_precision precision, double* x_host, double* hist_host,
                              nbk_result* result);
 
+/* Batched end-to-end form (several right-hand sides of one operator, the
+ * paper's repeated solves P:559): solves RHS k = 0..nrhs-1 from f_hosts[k]
+ * (e_local*N^3 FP64 each, natural order; pinned host memory lets the copies
+ * overlap) and writes solution k to x_hosts[k] (x_hosts or an entry may be
+ * NULL).  The host->device copy of RHS k+1 and the device->host copy of
+ * solution k-1 run on two library-owned copy streams while solve k runs (PCIe
+ * is full duplex), so only the first copy in and the last copy out are
+ * exposed.  Every RHS gets its own h0 (as nbk_cg_solve_host); hist_hosts
+ * (NULL or nrhs*(niter+1) doubles) and results (NULL or nrhs entries) are per
+ * RHS.  Allocates two n-double staging buffers on first use (freed by
+ * nbk_destroy).  Same results as nrhs calls of nbk_cg_solve_host.  Returns
+ * NBK_EDEFECT if any solve flagged a defect.  Synchronous (returns when
+ * solution nrhs-1 is in host memory).  Errors: NBK_EINVAL (NULL ctx / f_hosts /
+ * f_hosts[k], nrhs < 1), else as nbk_cg_solve. */
+nbk_status nbk_cg_solve_host_batch(nbk_ctx* ctx, int32_t nrhs, const double* const* f_hosts,
+                                   int32_t niter, nbk_precision precision,
+                                   double* const* x_hosts, double* hist_hosts,
+                                   nbk_result* results);
+
 /* Copy the last solution (FP64 view: exact upcast of the FP32 solver's x) to
  * host memory, e_local*N^3 doubles.  Synchronous. */
 nbk_status nbk_get_solution(nbk_ctx* ctx, double* x_host);

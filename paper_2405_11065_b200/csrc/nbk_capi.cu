@@ -756,6 +756,60 @@ nbk_status nbk_cg_solve_host(nbk_ctx* c, const double* f_host, int32_t niter, nb
     return st;
 }
 
+nbk_status nbk_cg_solve_host_batch(nbk_ctx* c, int32_t nrhs, const double* const* f_hosts, int32_t niter,
+                                   nbk_precision prec, double* const* x_hosts, double* hist_hosts,
+                                   nbk_result* results)
+{
+    if (!c || nrhs < 1 || !f_hosts) return fail(c, NBK_EINVAL, "NULL ctx / f_hosts or nrhs < 1");
+    for (int32_t k = 0; k < nrhs; ++k)
+        if (!f_hosts[k]) return fail(c, NBK_EINVAL, "f_hosts[k] is NULL");
+    const size_t bytes = 8 * (size_t)c->n;
+    if (!c->stage_f) {
+        NBK_CUDA(c, cudaMalloc(&c->stage_f, bytes));
+        NBK_CUDA(c, cudaMalloc(&c->stage_x, bytes));
+        NBK_CUDA(c, cudaStreamCreateWithFlags(&c->xs_in, cudaStreamNonBlocking));
+        NBK_CUDA(c, cudaStreamCreateWithFlags(&c->xs_out, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&c->ev_in, &c->ev_fused, &c->ev_xready, &c->ev_out})
+            NBK_CUDA(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    // RHS 0 in, after the work already queued on the context stream; the context
+    // stream is ordered after the copy streams' previous work
+    NBK_CUDA(c, cudaEventRecord(c->ev_out, c->xs_out));
+    NBK_CUDA(c, cudaEventRecord(c->ev_fused, c->stream));
+    NBK_CUDA(c, cudaStreamWaitEvent(c->xs_in, c->ev_fused, 0));
+    NBK_CUDA(c, cudaMemcpyAsync(c->stage_f, f_hosts[0], bytes, cudaMemcpyHostToDevice, c->xs_in));
+    NBK_CUDA(c, cudaEventRecord(c->ev_in, c->xs_in));
+    nbk_status st_all = NBK_OK;
+    for (int32_t k = 0; k < nrhs; ++k) {
+        // RHS k into the solver's SL vector; then RHS k+1 streams in during solve k
+        NBK_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_in, 0));
+        NBK_CUDA(c, perm_sl<double>(c, c->f64, c->stage_f, true, c->stream));
+        NBK_CUDA(c, cudaEventRecord(c->ev_fused, c->stream));
+        c->h0_dirty = 1;
+        if (k + 1 < nrhs) {
+            NBK_CUDA(c, cudaStreamWaitEvent(c->xs_in, c->ev_fused, 0));
+            NBK_CUDA(c, cudaMemcpyAsync(c->stage_f, f_hosts[k + 1], bytes, cudaMemcpyHostToDevice, c->xs_in));
+            NBK_CUDA(c, cudaEventRecord(c->ev_in, c->xs_in));
+        }
+        nbk_status st = nbk_cg_solve(c, niter, prec, hist_hosts ? hist_hosts + (size_t)k * (niter + 1) : nullptr,
+                                     nullptr, results ? results + k : nullptr);
+        if (st != NBK_OK && st != NBK_EDEFECT) return st;
+        if (st == NBK_EDEFECT) st_all = NBK_EDEFECT;
+        // solution k out (natural order) while solve k+1 runs; stage_x is free once x_{k-1} left
+        if (x_hosts && x_hosts[k]) {
+            NBK_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_out, 0));
+            NBK_CUDA(c, perm_sl<double>(c, c->stage_x, c->x64, false, c->stream));
+            NBK_CUDA(c, cudaEventRecord(c->ev_xready, c->stream));
+            NBK_CUDA(c, cudaStreamWaitEvent(c->xs_out, c->ev_xready, 0));
+            NBK_CUDA(c, cudaMemcpyAsync(x_hosts[k], c->stage_x, bytes, cudaMemcpyDeviceToHost, c->xs_out));
+            NBK_CUDA(c, cudaEventRecord(c->ev_out, c->xs_out));
+        }
+    }
+    NBK_CUDA(c, cudaStreamSynchronize(c->xs_out));
+    NBK_CUDA(c, cudaStreamSynchronize(c->xs_in));
+    return st_all;
+}
+
 nbk_status nbk_get_solution(nbk_ctx* c, double* x_host)
 {
     if (!c || !x_host) return fail(c, NBK_EINVAL, "NULL argument");
@@ -899,6 +953,16 @@ void nbk_destroy(nbk_ctx* c)
     if (c->ev_pack) cudaEventDestroy(c->ev_pack);
     if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->xs_in) {
+        cudaStreamSynchronize(c->xs_in);
+        cudaStreamSynchronize(c->xs_out);
+        cudaStreamDestroy(c->xs_in);
+        cudaStreamDestroy(c->xs_out);
+        for (cudaEvent_t e : {c->ev_in, c->ev_fused, c->ev_xready, c->ev_out})
+            if (e) cudaEventDestroy(e);
+    }
+    if (c->stage_f) cudaFree(c->stage_f);
+    if (c->stage_x) cudaFree(c->stage_x);
     if (c->own_stream) {
         cudaStreamSynchronize(c->own_stream);
         cudaStreamDestroy(c->own_stream);

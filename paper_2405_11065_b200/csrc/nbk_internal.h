@@ -82,6 +82,11 @@ struct nbk_ctx {
     std::map<std::tuple<int, int, int>, nbk_graph> graphs;  // (precision, niter, profiling)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int last_solved_precision = -1;
+    // nbk_cg_solve_host_batch: library-owned staging buffers (natural order, n doubles each,
+    // allocated on first use) and the two copy streams (H2D, D2H run concurrently)
+    double *stage_f = nullptr, *stage_x = nullptr;
+    cudaStream_t xs_in = nullptr, xs_out = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_fused = nullptr, ev_xready = nullptr, ev_out = nullptr;
 };
 
 namespace nbk {

@@ -33,7 +33,7 @@ EMU = {"vprec": 1, "rr": 2, "mca": 3}
 # every symbol include/nbk.h declares
 SYMBOLS = ["nbk_workspace_bytes", "nbk_partition", "nbk_nccl_unique_id", "nbk_cg_setup",
            "nbk_load_arrays", "nbk_get_arrays", "nbk_ax_apply", "nbk_dssum", "nbk_glsc3",
-           "nbk_cg_solve", "nbk_cg_solve_host", "nbk_get_solution", "nbk_solution_ptr",
+           "nbk_cg_solve", "nbk_cg_solve_host", "nbk_cg_solve_host_batch", "nbk_get_solution", "nbk_solution_ptr",
            "nbk_set_emulation", "nbk_set_vprec", "nbk_set_precond", "nbk_load_precond", "nbk_get_precond", "nbk_set_profiling",
            "nbk_query", "nbk_solve_launches", "nbk_group_link",
            "nbk_group_ax_apply", "nbk_group_dssum", "nbk_group_glsc3", "nbk_group_cg_solve",
@@ -103,6 +103,7 @@ def load() -> ctypes.CDLL:
         "nbk_glsc3": [vp, vp, vp, ctypes.c_int, P(ctypes.c_double)],
         "nbk_cg_solve": [vp, i32, ctypes.c_int, vp, vp, P(CResult)],
         "nbk_cg_solve_host": [vp, vp, i32, ctypes.c_int, vp, vp, P(CResult)],
+        "nbk_cg_solve_host_batch": [vp, i32, P(vp), i32, ctypes.c_int, P(vp), vp, P(CResult)],
         "nbk_get_solution": [vp, vp],
         "nbk_solution_ptr": [vp, ctypes.c_int, P(vp)],
         "nbk_set_profiling": [vp, i32],
@@ -344,6 +345,21 @@ class Context:
                                         _ptr(x_host), _ptr(hist), ctypes.byref(res))
         _check(st, self._ctx, ok=(NBK_OK, NBK_EDEFECT))
         return hist, {k: getattr(res, k) for k, _ in CResult._fields_}
+
+    def cg_solve_host_batch(self, f_hosts, niter: int, precision: str = "fp32", x_hosts=None):
+        """nbk_cg_solve_host_batch: RHS f_hosts[k] -> solution x_hosts[k] (host arrays,
+        pinned for overlapped copies); returns (hist[nrhs, niter+1], [result dicts])."""
+        k = len(f_hosts)
+        fs = [np.ascontiguousarray(f, dtype=np.float64) for f in f_hosts]
+        fp = (ctypes.c_void_p * k)(*[_ptr(f) for f in fs])
+        xp = None
+        if x_hosts is not None:
+            xp = (ctypes.c_void_p * k)(*[_ptr(x) for x in x_hosts])
+        hist = np.zeros((k, niter + 1))
+        res = (CResult * k)()
+        st = self.lib.nbk_cg_solve_host_batch(self._ctx, k, fp, niter, PREC[precision], xp, _ptr(hist), res)
+        _check(st, self._ctx, ok=(NBK_OK, NBK_EDEFECT))
+        return hist, [{n: getattr(r, n) for n, _ in CResult._fields_} for r in res]
 
     def solution(self) -> np.ndarray:
         x = np.zeros(self.shape)

@@ -121,3 +121,29 @@ def test_emulation_with_jacobi_rejected(nbk):
     ctx.set_precond("none")
     ctx.cg_solve(10, "vprec")
     ctx.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_batch_host_solve_equals_oracle_per_rhs(nbk, ora, prec):
+    """nbk_cg_solve_host_batch: three right-hand sides of one operator, the
+    copies overlapped with the solves on the library's copy streams -- every
+    history and solution bitwise the oracle's for its own RHS (and the same as
+    nbk_cg_solve_host)."""
+    ctx = nbk.cg_setup(nbk.MeshSpec(3, 2, 2, 6, 0.1, 5, 11), "fp32")
+    om = ora.Mesh(3, 2, 2, 6, 0.1, 5, 11)
+    _, _, D = ora.gll(6)
+    s = ora.setup(om, want=("G", "f"))
+    ctx.load_arrays(D, s["G"], s["f"])
+    fs = [ora.setup(ora.Mesh(3, 2, 2, 6, 0.1, 5, seed), want=("f",))["f"] for seed in (11, 12, 13)]
+    fh = [torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)).pin_memory() for f in fs]
+    xh = [torch.zeros(ctx.shape, dtype=torch.float64).pin_memory() for _ in fs]
+    hist, res = ctx.cg_solve_host_batch([f.numpy() for f in fh], 30, prec, [x.numpy() for x in xh])
+    assert hist.shape == (3, 31) and len(res) == 3
+    for k, f in enumerate(fs):
+        ref = ora.cg(om, D, s["G"], f, 30, prec)
+        assert bits_equal(hist[k], ref.hist), k
+        assert bits_equal(xh[k].numpy(), np.asarray(ref.x, dtype=np.float64)), k   # FP32 x: exact upcast
+        x1 = np.zeros(ctx.shape)
+        h1, _ = ctx.cg_solve_host(f, 30, prec, x1)
+        assert bits_equal(h1, hist[k]) and bits_equal(x1, xh[k].numpy()), k
+    ctx.close()

@@ -45,6 +45,8 @@ def test_bench_line_contract_small():
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    # the copies are inside the timed region: end to end cannot beat the device-resident value
+    assert e["value"] <= d["value"] * 1.02 and 0 < e["single_call_value"] <= d["value"] * 1.02
     assert d["clocks"]["sm_max_mhz"] and "reasons" in d["clocks"]
     assert d["config"]["workload"].startswith("C2")
     assert d["fp64"]["value"] > 0 and d["speedup_fp32_vs_fp64"] > 1.0
