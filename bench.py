@@ -534,10 +534,16 @@ def run_gpu(args):
                 ctx.cg_solve(cfg.niter, p_, trace=False)
                 ctx.sync()
                 per = []
+                # several ranks: every rank must enqueue the same number of (collective) solves,
+                # so the count comes from the rank-agreed step time, not from each rank's clock
+                nfix = 0
+                if world > 1:
+                    step_ms = (tot_ms if p_ == "fp32" else max_over_ranks(sum(ms64), world)) / args.steps
+                    nfix = max(2, int(1500.0 / step_ms) + 1)
                 for _ in range(args.energy_reps):
                     nsol, t0 = 0, time.perf_counter()
                     with Energy(local) as eg:
-                        while time.perf_counter() - t0 < 1.5 or nsol < 2:
+                        while (nsol < nfix) if nfix else (time.perf_counter() - t0 < 1.5 or nsol < 2):
                             ctx.cg_solve(cfg.niter, p_, trace=False)
                             nsol += 1
                         ctx.sync()

@@ -1050,6 +1050,130 @@ __device__ __forceinline__ void dssum_tiles_gather(const DssumArgs<T>& a, acc_t&
     }
 }
 
+// Gather-phase K_B, multiplicity-specialised (PM_NONE; NBK_DSSUM_GATHER_M, default on).
+// Same tiles, same chains (C4: ascending local index), same pap terms as
+// dssum_tiles_gather -- bitwise identical -- with fewer issue slots per node
+// (ncu C5 FP32: the runtime-m form spent ~100 warp instructions per node
+// iteration in phase 2 and 22 per copy in phase 1, issue 61 % busy):
+//  phase 1 walks the staged index buffer as one flat int array (the value
+//          buffer mirrors it slot for slot; alignment-pad slots are skipped by
+//          a range test), no 3-way row selection;
+//  phase 2 runs one loop per multiplicity with the chain unrolled and the
+//          index row / copy values fetched by 8- and 16-byte shared loads.
+#ifndef NBK_DSSUM_GATHER_M
+#define NBK_DSSUM_GATHER_M 1
+#endif
+template <typename T, int M>
+__device__ __forceinline__ void lds_row(const int32_t* row, const T* val, int32_t (&ix)[M], T (&v)[M])
+{
+    if constexpr (M == 2) {
+        const int2 r = *reinterpret_cast<const int2*>(row);
+        ix[0] = r.x; ix[1] = r.y;
+    } else {
+#pragma unroll
+        for (int h = 0; h < M / 4; ++h) {
+            const int4 r = reinterpret_cast<const int4*>(row)[h];
+            ix[4 * h] = r.x; ix[4 * h + 1] = r.y; ix[4 * h + 2] = r.z; ix[4 * h + 3] = r.w;
+        }
+    }
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int h = 0; h < M / 2; ++h) {
+            const double2 d = reinterpret_cast<const double2*>(val)[h];
+            v[2 * h] = d.x; v[2 * h + 1] = d.y;
+        }
+    } else if constexpr (M == 2) {
+        const float2 f = *reinterpret_cast<const float2*>(val);
+        v[0] = f.x; v[1] = f.y;
+    } else {
+#pragma unroll
+        for (int h = 0; h < M / 4; ++h) {
+            const float4 f = reinterpret_cast<const float4*>(val)[h];
+            v[4 * h] = f.x; v[4 * h + 1] = f.y; v[4 * h + 2] = f.z; v[4 * h + 3] = f.w;
+        }
+    }
+}
+// The n nodes of multiplicity M of a tile: index rows at rows[M q], their copy
+// values at vals[M q], p of the first copy at pv[q].
+template <typename T, bool FUSED, int M>
+__device__ __forceinline__ void dssum_nodes_m(const DssumArgs<T>& a, acc_t& acc, const int32_t* rows,
+                                              const T* vals, const T* pv, int n)
+{
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        int32_t ix[M];
+        T v[M];
+        lds_row<T, M>(rows + M * q, vals + M * q, ix, v);
+        T sum = v[0];                                    // C4: ascending local index
+#pragma unroll
+        for (int c = 1; c < M; ++c) sum = sum + v[c];
+        if (!FUSED && a.mask && masked_local<T>(a.mesh, ix[0])) sum = 0;
+#pragma unroll
+        for (int c = 0; c < M; ++c) a.w[ix[c]] = sum;
+        if constexpr (FUSED) add_node_pap<T, PM_NONE>(acc, sum, pv[q], M, a.single, a.pm);
+    }
+}
+template <typename T, bool FUSED>
+__device__ __forceinline__ void dssum_tiles_gather_m(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
+                                                     int tile_smem, uint64_t* bars)
+{
+    T* sval = reinterpret_cast<T*>(sbuf + 2 * tile_smem);      // tile_smem / 4 values, slot = index slot
+    T* spv = sval + tile_smem / 4;                             // tile_smem / 8 values, one per node
+    const uint32_t nloc = (uint32_t)(a.mesh.E * a.mesh.N * a.mesh.N * a.mesh.N);
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (int)blockIdx.x < a.ntiles)
+        tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - blockIdx.x : blockIdx.x, sbuf, &bars[0]);
+    int k = 0;
+    int s2 = 0, n2 = 0, s4 = 0, n4 = 0, s8 = 0, n8 = 0;
+    if ((int)blockIdx.x < a.ntiles)
+        tile_range(a.toff, a.rev ? a.ntiles - 1 - blockIdx.x : blockIdx.x, s2, n2, s4, n4, s8, n8);
+    for (int i = blockIdx.x; i < a.ntiles; i += gridDim.x, ++k) {
+        const int b = k & 1;
+        const int inx = i + (int)gridDim.x;
+        int s2n = 0, n2n = 0, s4n = 0, n4n = 0, s8n = 0, n8n = 0;
+        if (inx < a.ntiles) tile_range(a.toff, a.rev ? a.ntiles - 1 - inx : inx, s2n, n2n, s4n, n4n, s8n, n8n);
+        if (threadIdx.x == 0 && inx < a.ntiles) {  // the other buffer was released by the last barrier
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tile_stage(a.g2, a.g4, a.g8, a.toff, a.rev ? a.ntiles - 1 - inx : inx,
+                       sbuf + (b ^ 1) * tile_smem, &bars[b ^ 1]);
+        }
+        mbar_wait(&bars[b], (k >> 1) & 1);
+        const int32_t* ibuf = reinterpret_cast<const int32_t*>(sbuf + b * tile_smem);
+        const int lead = (int)dssum_g2_lead(s2) >> 2;            // pad slots before the g2 rows
+        const int e2 = lead + 2 * n2;                            // end of the g2 rows
+        const int b2i = (int)dssum_g2_bytes(s2, n2) >> 2;        // first g4 slot
+        const int b4i = b2i + 4 * n4;                            // first g8 slot
+        const int nint = b4i + 8 * n8;
+        // phase 1: every copy value (and p at the first copies) of the tile in flight
+        for (int r = threadIdx.x; r < nint; r += blockDim.x) {
+            const int32_t ix = ibuf[r];
+            if ((r >= lead) & ((r < e2) | (r >= b2i))) {
+                NBK_ASSERT((uint32_t)ix < nloc);
+                cp_async_t<T>(sval + r, a.w + ix);
+            }
+        }
+        if constexpr (FUSED) {
+            const int tot = n2 + n4 + n8;
+            for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+                const int r = q < n2 ? lead + 2 * q : (q < n2 + n4 ? b2i + 4 * (q - n2) : b4i + 8 * (q - n2 - n4));
+                cp_async_t<T>(spv + q, a.p + ibuf[r]);
+            }
+        }
+        (void)nloc;
+        cp_async_wait_all();
+        __syncthreads();
+        // phase 2: chains from shared memory (C4), scatter, pap -- one loop per multiplicity
+        dssum_nodes_m<T, FUSED, 2>(a, acc, ibuf + lead, sval + lead, spv, n2);
+        dssum_nodes_m<T, FUSED, 4>(a, acc, ibuf + b2i, sval + b2i, spv + n2, n4);
+        dssum_nodes_m<T, FUSED, 8>(a, acc, ibuf + b4i, sval + b4i, spv + n2 + n4, n8);
+        __syncthreads();
+        s2 = s2n; n2 = n2n; s4 = s4n; n4 = n4n; s8 = s8n; n8 = n8n;
+    }
+}
+
 template <typename T, int PM>
 __device__ __forceinline__ void dssum_fused_epilogue(const DssumArgs<T>& a, acc_t& acc);
 
@@ -1061,8 +1185,10 @@ __global__ void __launch_bounds__(NBK_DSSUM_THREADS, sizeof(T) == 4 ? NBK_DSSUM_
     __shared__ uint64_t dsm_bars[2];
     pdl_wait();
 #if defined(NBK_DSSUM_GATHER)
-    if (a.stage) dssum_tiles_gather<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
-    else
+    if (a.stage) {
+        if constexpr (PM == PM_NONE && NBK_DSSUM_GATHER_M) dssum_tiles_gather_m<T, FUSED>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
+        else dssum_tiles_gather<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
+    } else
 #endif
     dssum_tiles<T, FUSED, PM>(a, acc, dsm_tiles, a.tile_smem, dsm_bars);
     pdl_launch_dependents();
