@@ -1112,6 +1112,27 @@ __device__ __forceinline__ void dssum_nodes_m(const DssumArgs<T>& a, acc_t& acc,
         if constexpr (FUSED) add_node_pap<T, PM_NONE>(acc, sum, pv[q], M, a.single, a.pm);
     }
 }
+// Thread-private fetch of the copies (and p) of the nodes dssum_nodes_m gives this thread.
+template <typename T, bool FUSED, int M>
+__device__ __forceinline__ void dssum_fetch_m(const DssumArgs<T>& a, const int32_t* rows, T* vals, T* pv, int n)
+{
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        int32_t ix[M];
+        if constexpr (M == 2) {
+            const int2 r = *reinterpret_cast<const int2*>(rows + 2 * q);
+            ix[0] = r.x; ix[1] = r.y;
+        } else {
+#pragma unroll
+            for (int h = 0; h < M / 4; ++h) {
+                const int4 r = reinterpret_cast<const int4*>(rows + M * q)[h];
+                ix[4 * h] = r.x; ix[4 * h + 1] = r.y; ix[4 * h + 2] = r.z; ix[4 * h + 3] = r.w;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < M; ++c) cp_async_t<T>(vals + M * q + c, a.w + ix[c]);
+        if constexpr (FUSED) cp_async_t<T>(pv + q, a.p + ix[0]);
+    }
+}
 template <typename T, bool FUSED>
 __device__ __forceinline__ void dssum_tiles_gather_m(const DssumArgs<T>& a, acc_t& acc, unsigned char* sbuf,
                                                      int tile_smem, uint64_t* bars)
@@ -1148,6 +1169,16 @@ __device__ __forceinline__ void dssum_tiles_gather_m(const DssumArgs<T>& a, acc_
         const int b4i = b2i + 4 * n4;                            // first g8 slot
         const int nint = b4i + 8 * n8;
         // phase 1: every copy value (and p at the first copies) of the tile in flight
+#if NBK_DSSUM_GATHER_M == 2
+        // thread-private form: a thread fetches the copies of exactly the nodes it sums in
+        // phase 2 (same q loops), so its own cp.async wait orders the data -- no block
+        // barrier between the phases, the warps of a block drift apart within a tile
+        dssum_fetch_m<T, FUSED, 2>(a, ibuf + lead, sval + lead, spv, n2);
+        dssum_fetch_m<T, FUSED, 4>(a, ibuf + b2i, sval + b2i, spv + n2, n4);
+        dssum_fetch_m<T, FUSED, 8>(a, ibuf + b4i, sval + b4i, spv + n2 + n4, n8);
+        (void)nloc; (void)e2; (void)nint;
+        cp_async_wait_all();
+#else
         for (int r = threadIdx.x; r < nint; r += blockDim.x) {
             const int32_t ix = ibuf[r];
             if ((r >= lead) & ((r < e2) | (r >= b2i))) {
@@ -1165,6 +1196,7 @@ __device__ __forceinline__ void dssum_tiles_gather_m(const DssumArgs<T>& a, acc_
         (void)nloc;
         cp_async_wait_all();
         __syncthreads();
+#endif
         // phase 2: chains from shared memory (C4), scatter, pap -- one loop per multiplicity
         dssum_nodes_m<T, FUSED, 2>(a, acc, ibuf + lead, sval + lead, spv, n2);
         dssum_nodes_m<T, FUSED, 4>(a, acc, ibuf + b2i, sval + b2i, spv + n2, n4);
