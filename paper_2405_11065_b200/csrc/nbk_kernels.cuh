@@ -1163,7 +1163,7 @@ __device__ __forceinline__ void dssum_tiles_gather_m(const DssumArgs<T>& a, acc_
         }
         mbar_wait(&bars[b], (k >> 1) & 1);
         const int32_t* ibuf = reinterpret_cast<const int32_t*>(sbuf + b * tile_smem);
-        const int lead = (int)dssum_g2_lead(s2) >> 2;            // pad slots before the g2 rows
+        const int lead = n2 ? (int)dssum_g2_lead(s2) >> 2 : 0;   // pad slots before the g2 rows (none without g2 rows)
         const int e2 = lead + 2 * n2;                            // end of the g2 rows
         const int b2i = (int)dssum_g2_bytes(s2, n2) >> 2;        // first g4 slot
         const int b4i = b2i + 4 * n4;                            // first g8 slot
