@@ -1063,6 +1063,9 @@ __device__ __forceinline__ void dssum_tiles_gather(const DssumArgs<T>& a, acc_t&
 #ifndef NBK_DSSUM_GATHER_M
 #define NBK_DSSUM_GATHER_M 1
 #endif
+#ifndef NBK_DSSUM_PF_L2
+#define NBK_DSSUM_PF_L2 0   // 1: prefetch.global.L2 of the next tile's copies during phase 2 (experiment)
+#endif
 template <typename T, int M>
 __device__ __forceinline__ void lds_row(const int32_t* row, const T* val, int32_t (&ix)[M], T (&v)[M])
 {
@@ -1196,6 +1199,21 @@ __device__ __forceinline__ void dssum_tiles_gather_m(const DssumArgs<T>& a, acc_
         (void)nloc;
         cp_async_wait_all();
         __syncthreads();
+#endif
+#if NBK_DSSUM_PF_L2
+        // L2 prefetch of the next tile's copies (its index rows were bulk-copied during this
+        // tile's gather): the next gather then meets L2 instead of DRAM latency
+        if (inx < a.ntiles) {
+            mbar_wait(&bars[b ^ 1], ((k + 1) >> 1) & 1);
+            const int32_t* inext = reinterpret_cast<const int32_t*>(sbuf + (b ^ 1) * tile_smem);
+            const int leadn = n2n ? (int)dssum_g2_lead(s2n) >> 2 : 0, e2n = leadn + 2 * n2n;
+            const int b2n = (int)dssum_g2_bytes(s2n, n2n) >> 2, nintn = b2n + 4 * n4n + 8 * n8n;
+            for (int r = threadIdx.x; r < nintn; r += blockDim.x) {
+                const int32_t ix = inext[r];
+                if ((r >= leadn) & ((r < e2n) | (r >= b2n)))
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.w + ix));
+            }
+        }
 #endif
         // phase 2: chains from shared memory (C4), scatter, pap -- one loop per multiplicity
         dssum_nodes_m<T, FUSED, 2>(a, acc, ibuf + lead, sval + lead, spv, n2);
